@@ -1,0 +1,323 @@
+"""Pins for the Python planner oracle (oracle/planner.py).
+
+Pinned against: the paper's tables (Table 2 AoSU/AoSV/SoA shapes, Table 3 K-Means
+shapes, Table 4 plan shapes), SPEC.md's worked examples (affinity sums, the
+K-Means tie-break trace, enumeration counts, run-node counts, the Medical moved
+set), closed forms (Bell numbers), exhaustive brute force (ODS and PDL), and the
+SPEC.md invariants (partition, capacity, positive merge, determinism, scale
+invariance, affinity-sum preservation, profile precedence).
+"""
+import random
+
+import pytest
+
+from oracle import planner as P
+from tests.conftest import golden
+
+
+def load(prog, arch, prof=None):
+    p = P.program_from_json(golden(prog))
+    a = P.arch_from_json(golden(arch))
+    pr = P.profile_from_json(golden(prof)) if prof else None
+    return p, a, pr
+
+
+def simple_program(groups, trip=10, fields=("A", "B", "C"), eb=4):
+    p = P.Program("t", 100, [P.Field(n, eb, i) for i, n in enumerate(fields)],
+                  [P.Section("s", trip, tuple(groups), ("cpu", "gpu"))], ["s"])
+    return p
+
+
+CPU = P.Device("cpu", 64, 1.0, 1.0, False, 2.0, 64)
+GPU = P.Device("gpu", 128, 1.0, 10.0, True, 2.0, 128)
+
+
+# ---------------------------------------------------------------- SPEC worked examples
+
+def test_affinity_hand_sum(expected):
+    e = expected["affinity_example"]
+    p = simple_program([P.AccessGroup(("A", "B"), 2.0, "irregular"),
+                        P.AccessGroup(("B", "C"), 1.0, "irregular")], trip=e["trip"])
+    nodes, w = P.build_affinity_graph(p.sections[0], CPU, p.decl())
+    assert nodes == ["A", "B", "C"]
+    assert w.get(("A", "B"), 0.0) == e["weights"]["A,B"]
+    assert w.get(("B", "C"), 0.0) == e["weights"]["B,C"]
+    assert w.get(("A", "C"), 0.0) == e["weights"]["A,C"]
+
+
+def test_affinity_single_field_has_no_edges():
+    p = simple_program([P.AccessGroup(("A",), 1.0, "streaming")])
+    nodes, w = P.build_affinity_graph(p.sections[0], CPU, p.decl())
+    assert nodes == ["A"] and w == {}
+
+
+def test_kmeans_coalescing_weight_and_soa(expected):
+    p, a, _ = load("kmeans_program.json", "kmeans_table3_arch.json")
+    gpu = a.device("gpu")
+    _, w = P.build_affinity_graph(p.sections[0], gpu, p.decl())
+    assert len(w) == 32 * 31 // 2
+    assert set(w.values()) == {expected["affinity_kmeans_coalescing"]["weight"]}
+    assert P.layout_string(P.ods(p.sections[0], gpu, p)) == expected["kmeans_coalescing_soa"]["value"]
+
+
+def test_kmeans_cap32_four_aos_of_eight(expected):
+    p, a, _ = load("kmeans_program.json", "kmeans_table3_arch.json")
+    cpu = a.device("cpu")
+    assert P.layout_string(P.ods(p.sections[0], cpu, p)) == expected["kmeans_cap32_noncoalescing"]["value"]
+    # merged K-Means sections 1+2 on the non-coalescing device -> 4 clusters of 8
+    m = P.merge_sections(p.sections)
+    assert P.layout_string(P.ods(m, cpu, p)) == expected["kmeans_cap32_noncoalescing"]["value"]
+
+
+def test_medical_aosu(expected):
+    p, a, _ = load("medical_aosu_program.json", "medical_arch.json")
+    l = P.ods(p.sections[0], a.device("cpu"), p)
+    assert P.layout_string(l) == expected["medical_aosu"]["value"]
+    # SPEC acceptance 5: greedy == brute force on the criteria-1 fixture
+    bl, _ = P.brute_force_ods(p.sections[0], a.device("cpu"), p)
+    assert bl == l
+
+
+def test_medical_aosv_and_soa(expected):
+    p, a, _ = load("medical_program.json", "medical_arch.json")
+    s = {x.id: x for x in p.sections}
+    m13 = P.merge_sections([s["s1"], s["s2"], s["s3"]])
+    assert P.layout_string(P.ods(m13, a.device("cpu"), p)) == expected["medical_aosv"]["value"]
+    m47 = P.merge_sections([s["s4"], s["s5"], s["s6"], s["s7"]])
+    assert P.layout_string(P.ods(m47, a.device("gpu"), p)) == expected["medical_soa"]["value"]
+
+
+def test_c3_structured_program_hybrid(expected):
+    p, a, _ = load("c3_program.json", "b200_arch.json")
+    l = P.ods(p.sections[0], a.device("b200"), p)
+    e = expected["c3_hybrid"]
+    assert P.layout_string(l) == e["value"]
+    assert len(l) == e["n_clusters"]
+    eb = p.elem_bytes()
+    assert [P.cluster_bytes(c, eb) for c in l] == e["strides"]
+
+
+def test_canonical_string_round_trip_and_paper_notation(expected):
+    decl = {n: i for i, n in enumerate(["V1", "V2", "V3", "U1", "U2", "U3", "S", "T", "interpT"])}
+    paper = "V1,V2,V3,{U1,U2,U3},S,T,interpT"                  # PAPER.md:112 notation
+    assert P.layout_string(P.parse_layout(paper, decl)) == expected["medical_aosu"]["value"]
+    assert P.layout_string(P.parse_layout("{V1,V2,V3},U1,U2,U3,S,T,interpT", decl)) == \
+        expected["medical_aosv"]["value"]
+    rng = random.Random(4)
+    names = list(decl)
+    for _ in range(100):
+        labels = [rng.randrange(9) for _ in names]
+        groups = {}
+        for n, lab in zip(names, labels):
+            groups.setdefault(lab, []).append(n)
+        l = P.canonical(list(groups.values()), decl)
+        s = P.layout_string(l)
+        assert P.parse_layout(s, decl) == l
+        assert P.canonical(l, decl) == l                      # idempotent
+    with pytest.raises(P.PlannerError):
+        P.parse_layout("{V1,V2}", decl)                       # not a partition of the fields
+
+
+def test_enumeration_counts(expected):
+    e = expected["enumerate_counts"]
+    decl = {n: i for i, n in enumerate("ABCDEFGH")}
+    eb = {n: 4 for n in decl}
+    assert len(P.enumerate_layouts(["A"], eb, None, decl)) == e["1_field"]
+    assert len(P.enumerate_layouts(list("ABC"), eb, None, decl)) == e["3_fields_unbounded"]
+    assert len(P.enumerate_layouts(list("ABCD"), eb, 8, decl)) == e["4_fields_4B_cap8"]
+    bell = expected["bell_numbers"]["value"]
+    for k in range(1, 8):
+        ls = P.enumerate_layouts(list("ABCDEFGH"[:k]), eb, None, decl)
+        assert len(ls) == bell[k] and len(set(ls)) == len(ls)
+
+
+def test_run_node_counts(expected):
+    e = expected["run_node_counts"]
+    p, a, pr = load("medical_program.json", "medical_arch.json", "medical_profile.json")
+    assert len(P.build_run_graph(p, a, pr)) == e["k7_d2"]
+    for k, key in [(1, "k1_d2"), (2, "k2_d2")]:
+        q = P.Program(p.name, p.record_count, p.fields, p.sections[:k], p.order[:k])
+        assert len(P.build_run_graph(q, a, pr)) == e[key]
+
+
+def test_medical_plan_table4(expected):
+    e = expected["medical_plan"]
+    p, a, pr = load("medical_program.json", "medical_arch.json", "medical_profile.json")
+    plan = P.shortest_plan(p, a, pr)
+    got = [[p.order[r.begin:r.end + 1], r.device, P.layout_string(r.layout)] for r in plan.runs]
+    assert got == e["runs"]
+    assert len(plan.remaps) == 1 and plan.remaps[0][1] == e["remap_moved"]
+    nbytes = sum(p.record_count * p.elem_bytes()[f] for f in plan.remaps[0][1])
+    assert nbytes == e["remap_bytes"]
+    bf = P.brute_force_plan(P.Program(p.name, p.record_count, p.fields, p.sections[:6], p.order[:6]), a, pr)
+    sp = P.shortest_plan(P.Program(p.name, p.record_count, p.fields, p.sections[:6], p.order[:6]), a, pr)
+    assert sp.total_ns == pytest.approx(bf.total_ns, rel=1e-12)
+
+
+def test_medical_same_device_moved_set():
+    # AoSV -> SoA on one device, all nine fields common -> moved {V1,V2,V3}, 3*N*4 bytes
+    p, a, _ = load("medical_program.json", "medical_arch.json")
+    decl = p.decl()
+    aosv = P.parse_layout("{V1,V2,V3},U1,U2,U3,S,T,interpT", decl)
+    soa = P.parse_layout("V1,V2,V3,U1,U2,U3,S,T,interpT", decl)
+    allf = frozenset(decl)
+    cost, moved = P.remap_cost(aosv, "gpu", soa, "gpu", allf, p, a)
+    assert moved == ["V1", "V2", "V3"]
+    assert cost == pytest.approx(3 * p.record_count * 4 / a.same_device_remap_bandwidth_bytes_per_ns
+                                 + a.remap_fixed_overhead_ns, rel=1e-15)
+    assert P.remap_cost(aosv, "gpu", aosv, "gpu", allf, p, a)[0] == 0.0         # identical -> 0
+    c_rev, _ = P.remap_cost(soa, "gpu", aosv, "gpu", allf, p, a)
+    assert c_rev == cost                                                         # symmetry
+    c_dev, moved_dev = P.remap_cost(aosv, "cpu", aosv, "gpu", allf, p, a)
+    assert moved_dev == sorted(allf)                                             # device change
+
+
+def test_kmeans_plan_table4(expected):
+    e = expected["kmeans_plan"]
+    p, a, pr = load("kmeans_program.json", "kmeans_arch.json", "kmeans_profile.json")
+    plan = P.shortest_plan(p, a, pr)
+    got = [[p.order[r.begin:r.end + 1], r.device, P.layout_string(r.layout)] for r in plan.runs]
+    assert got == e["runs"] and len(plan.remaps) == e["n_remaps"]
+
+
+# ---------------------------------------------------------------- cost model structure
+
+def test_exec_cost_examples_and_profile_precedence():
+    # irregular {U1,U2,U3}, trip 1000, freq 1: SoA touches 3 clusters, AoSU 1
+    names = ["V1", "V2", "V3", "U1", "U2", "U3", "S", "T", "interpT"]
+    p = P.Program("m", 10, [P.Field(n, 4, i) for i, n in enumerate(names)],
+                  [P.Section("x", 1000, (P.AccessGroup(("U1", "U2", "U3"), 1.0, "irregular"),), ("cpu",))],
+                  ["x"])
+    decl = p.decl()
+    soa = P.parse_layout(",".join(names), decl)
+    aosu = P.parse_layout("V1,V2,V3,{U1,U2,U3},S,T,interpT", decl)
+    s = p.sections[0]
+    assert P.exec_cost(s, soa, CPU, p)[0] == 3000 * CPU.line_time_ns
+    assert P.exec_cost(s, aosu, CPU, p)[0] == 1000 * CPU.line_time_ns
+    # linearity in trip count
+    s2 = P.Section("x", 2000, s.groups, s.allowed_devices)
+    assert P.exec_cost(s2, soa, CPU, p)[2] == 2 * P.exec_cost(s, soa, CPU, p)[2]
+    # profile precedence (SPEC acceptance 8)
+    prof = {("x", "cpu", P.layout_string(soa)): 123.5}
+    assert P.exec_cost(s, soa, CPU, p, prof)[2:] == (123.5, "profile")
+    assert P.exec_cost(s, soa, CPU, p, {})[3] == "model"
+
+
+def test_streaming_all_fields_partition_invariant_bytes():
+    # a streaming group over all fields costs the same bytes under SoA and AoS
+    # on a non-coalescing device
+    names = [f"f{i}" for i in range(32)]
+    p = P.Program("k", 10, [P.Field(n, 4, i) for i, n in enumerate(names)],
+                  [P.Section("k", 5, (P.AccessGroup(tuple(names), 1.0, "streaming"),), ("cpu",))], ["k"])
+    decl = p.decl()
+    soa = P.parse_layout(",".join(names), decl)
+    aos = P.parse_layout("{" + ",".join(names) + "}", decl)
+    dev = P.Device("cpu", 128, 1.0, 1.0, False, 2.0, 128)
+    assert P.exec_cost(p.sections[0], soa, dev, p)[0] == pytest.approx(
+        P.exec_cost(p.sections[0], aos, dev, p)[0], rel=1e-15)
+
+
+def test_combine_loss_trivial_cases():
+    p = simple_program([P.AccessGroup(("A", "B"), 1.0, "irregular")])
+    s = p.sections[0]
+    assert P.combine_loss(s, s, CPU, p) == 0.0
+    p2 = P.Program("t", 100, [P.Field(n, 4, i) for i, n in enumerate("ABCD")],
+                   [P.Section("a", 10, (P.AccessGroup(("A", "B"), 1.0, "irregular"),), ("cpu",)),
+                    P.Section("b", 10, (P.AccessGroup(("C", "D"), 1.0, "irregular"),), ("cpu",))],
+                   ["a", "b"])
+    assert P.combine_loss(p2.sections[0], p2.sections[1], CPU, p2) == 0.0
+
+
+# ---------------------------------------------------------------- random instances
+
+def random_program(rng, k_max=5, f_max=8):
+    F = rng.randint(2, f_max)
+    names = [f"x{i}" for i in range(F)]
+    fields = [P.Field(n, rng.choice([4, 8, 4, 2]), i) for i, n in enumerate(names)]
+    devs = ["cpu", "gpu"]
+    secs = []
+    k = rng.randint(1, k_max)
+    for j in range(k):
+        groups = []
+        for _ in range(rng.randint(1, 4)):
+            sz = rng.randint(1, min(4, F))
+            groups.append(P.AccessGroup(tuple(rng.sample(names, sz)), float(rng.randint(1, 4)),
+                                        rng.choice(["streaming", "irregular"]), float(rng.randint(0, 3))))
+        allowed = tuple(d for d in devs if rng.random() < 0.8) or ("cpu",)
+        secs.append(P.Section(f"s{j}", float(rng.randint(1, 1000)), tuple(groups), allowed))
+    return P.Program("r", rng.randint(1, 10 ** 6), fields, secs, [s.id for s in secs])
+
+
+def random_arch(rng):
+    return P.Architecture(
+        [P.Device("cpu", 64, rng.uniform(0.5, 2), rng.uniform(1, 4), False, 2.0, rng.choice([8, 16, 32, 64])),
+         P.Device("gpu", 128, rng.uniform(0.1, 1), rng.uniform(4, 40), True, rng.uniform(1, 3),
+                  rng.choice([8, 16, 32, 128]))],
+        [P.Link("cpu", "gpu", rng.uniform(1, 16), rng.uniform(0, 1e4))],
+        rng.uniform(10, 100), rng.uniform(0, 1e3))
+
+
+def test_pdl_equals_brute_force_200_random():
+    rng = random.Random(1407)
+    for _ in range(200):
+        p, a = random_program(rng), random_arch(rng)
+        sp = P.shortest_plan(p, a)
+        bf = P.brute_force_plan(p, a)
+        assert sp.total_ns == pytest.approx(bf.total_ns, rel=1e-12, abs=0)
+        # cover / contiguity
+        assert sp.runs[0].begin == 0 and sp.runs[-1].end == len(p.order) - 1
+        for r1, r2 in zip(sp.runs, sp.runs[1:]):
+            assert r2.begin == r1.end + 1
+        assert sp.total_ns == pytest.approx(sum(r.exec_ns for r in sp.runs) + sum(c for _, _, c in sp.remaps),
+                                            rel=1e-12)
+
+
+def test_greedy_vs_brute_force_ods_ratio():
+    rng = random.Random(4859)
+    for _ in range(200):
+        p = random_program(rng, k_max=1, f_max=7)
+        a = random_arch(rng)
+        s = p.sections[0]
+        d = a.device(s.allowed_devices[0])
+        try:
+            g = P.ods(s, d, p)
+        except P.PlannerError:
+            continue                                   # a field wider than the capacity
+        bl, bc = P.brute_force_ods(s, d, p)
+        gc = P.exec_cost(s, g, d, p)[2]
+        assert gc >= bc * (1 - 1e-12)
+
+
+def test_ods_invariants_1000_random():
+    rng = random.Random(99)
+    for _ in range(1000):
+        p = random_program(rng, k_max=2, f_max=8)
+        d = random_arch(rng).devices[rng.randrange(2)]
+        s = p.sections[0]
+        if d.name not in s.allowed_devices:
+            continue
+        eb, decl = p.elem_bytes(), p.decl()
+        try:
+            l = P.ods(s, d, p)
+        except P.PlannerError:
+            assert any(eb[n] > d.cluster_capacity_bytes for n in s.fields())
+            continue
+        flat = [x for c in l for x in c]
+        assert sorted(flat) == sorted(eb) and len(flat) == len(set(flat))        # partition
+        _, w = P.build_affinity_graph(s, d, decl)
+        for c in l:
+            assert P.cluster_bytes(c, eb) <= d.cluster_capacity_bytes              # capacity
+            if len(c) >= 2:                                                        # positive merge
+                assert any(w.get(tuple(sorted((x, y), key=decl.get)), 0) > 0
+                           for i, x in enumerate(c) for y in c[i + 1:])
+        assert P.ods(s, d, p) == l                                                 # determinism
+        scaled = P.Section(s.id, s.trip_count, tuple(P.AccessGroup(g.fields, g.freq * 3.0, g.pattern, g.ops)
+                                                     for g in s.groups), s.allowed_devices)
+        assert P.ods(scaled, d, p) == l                                            # scale invariance
+        if len(p.sections) > 1 and d.name in p.sections[1].allowed_devices:       # affinity sums
+            m = P.merge_sections(p.sections[:2])
+            _, wm = P.build_affinity_graph(m, d, decl)
+            _, w1 = P.build_affinity_graph(p.sections[0], d, decl)
+            _, w2 = P.build_affinity_graph(p.sections[1], d, decl)
+            for key in set(wm) | set(w1) | set(w2):
+                assert wm.get(key, 0.0) == pytest.approx(w1.get(key, 0.0) + w2.get(key, 0.0), rel=1e-12)
