@@ -1,0 +1,404 @@
+#!/usr/bin/env python
+"""bench.py -- ADHA layout remap on B200: remap GB/s (read+write), bit-exact path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl adha|reference]
+
+One step = one pass of the hot path over the configuration's records (SURVEY.md
+8(d)): for C2 one AoS->SoA remap of 10M 80-byte records.  Multi-GPU (torchrun,
+one process per GPU): the record array is sharded by contiguous index range
+(adha_shard_range) with no collective on the data path; each rank remaps its
+own shard ("weak" for C2: 10M records per rank; "strong" for C5: 8 GiB total).
+Timing: CUDA events on the launching stream, barrier + synchronize on both
+sides, max over ranks.  Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FALLBACK_HBM_GBS = 6650.0      # /opt/skills/guides/B200_PROFILING.md fallback, used only without MEASURED_PEAKS.json
+
+CONFIGS = {
+    # name: (description, widths, src labels, dst labels chain, n_records, scaling)
+    "C1": ("3-field float record (x,y,z), 1024 records, AoS->SoA->AoS", "xyz", 1024, "weak"),
+    "C2": ("16-field mixed 4/8-byte record, 10M records, AoS->SoA", "c2", 10_000_000, "weak"),
+    "C3": ("64-field record, SoA->ODS hybrid (128-byte cluster cap), 50M records", "c3", 50_000_000, "weak"),
+    "C4": ("Medical 9x fp32, PDL chain AoS->AoSV->SoA->AoS over 2 GiB of records", "c4", (2 ** 31) // 36, "weak"),
+    "C5": ("8 GiB mixed-width record array AoS->SoA, sharded across GPUs", "c2", (2 ** 33) // 80, "strong"),
+    "P1": ("Medical 256^3 voxels x 9 fp32: AoS->AoSV->SoA", "p1", 256 ** 3, "weak"),
+    "P2": ("K-Means 2^23 points x 32 fp32: SoA->4xAoS8->AoS", "p2", 2 ** 23, "weak"),
+}
+
+
+def c3_labels():
+    from tests.conftest import golden  # fixture file only (the planner's expected output, cited)
+    import paper_1407_4859_b200 as A
+    layout = A.plan_ods(golden("c3_program.json"), golden("b200_arch.json"), "c3", "b200")
+    names = [f"f{i}" for i in range(64)]
+    from adha_inputs import config_widths
+    return A.Layout.from_string(layout, names, config_widths(64)).cluster_of, layout
+
+
+def chain_for(kind):
+    """(widths, [label lists along the chain]) of a workload."""
+    from adha_inputs import config_widths
+    if kind == "xyz":
+        return [4, 4, 4], [[0, 0, 0], [0, 1, 2], [0, 0, 0]]
+    if kind == "c2":
+        w = config_widths(16)
+        return w, [[0] * 16, list(range(16))]
+    if kind == "c3":
+        w = config_widths(64)
+        return w, [list(range(64)), c3_labels()[0]]
+    if kind == "c4":
+        return [4] * 9, [[0] * 9, [0, 0, 0, 1, 2, 3, 4, 5, 6], list(range(9)), [0] * 9]
+    if kind == "p1":
+        return [4] * 9, [[0] * 9, [0, 0, 0, 1, 2, 3, 4, 5, 6], list(range(9))]
+    if kind == "p2":
+        return [4] * 32, [list(range(32)), [i // 8 for i in range(32)], [0] * 32]
+    raise ValueError(kind)
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, torch copy_ read+write)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(config):
+    """dram read+write bytes per launch of the dominant kernel from a committed ncu --set full capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as fh:
+            d = json.load(fh)
+        e = d.get(config)
+        return None if e is None else float(e["dram_bytes_per_launch"])
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 100 ms while running."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index):
+        self.dev = device_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "100", "-i", str(self.dev)],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def oracle_rate(widths, chain, sample_records, seconds, threads):
+    """Oracle GB/s (read+write payload) on a sample of the workload, as it stands."""
+    import numpy as np
+    from adha_inputs import random_bytes
+    from oracle import remap as O
+    bufs = []
+    for k, lab in enumerate(chain):
+        nb = O.layout_bytes(widths, lab, sample_records)
+        bufs.append(random_bytes(1407 + k, nb) if k == 0 else np.zeros(nb, np.uint8))
+    R = sum(widths)
+    done = 0
+    t0 = time.perf_counter()
+    while True:
+        for k in range(len(chain) - 1):
+            O.remap(bufs[k], chain[k], bufs[k + 1], chain[k + 1], widths, sample_records, threads=threads)
+            done += 2 * sample_records * R
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            break
+    return done / el / 1e9, el
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# ----------------------------------------------------------------------------------------- reference arm
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    name = args.config
+    desc, kind, n_total, scaling = CONFIGS[name]
+    widths, chain = chain_for(kind)
+    R = sum(widths)
+    n = n_total if scaling == "weak" else n_total // max(world, 1)
+    sample = min(n, 1 << 20)
+    cores = host_cores()
+    from oracle import remap as O
+    import numpy as np
+    from adha_inputs import random_bytes
+    bufs = [random_bytes(1407, O.layout_bytes(widths, chain[0], sample))] + \
+           [np.zeros(O.layout_bytes(widths, lab, sample), np.uint8) for lab in chain[1:]]
+
+    def step():
+        for k in range(len(chain) - 1):
+            O.remap(bufs[k], chain[k], bufs[k + 1], chain[k + 1], widths, sample, threads=cores)
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    el = time.perf_counter() - t0
+    bytes_step = 2 * sample * R * (len(chain) - 1)
+    gbs = bytes_step * args.steps / el / 1e9
+    line = {
+        "impl": "reference", "metric": "remap GB/s (read+write)", "value": gbs, "unit": "GB/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
+        "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic (seeded random bytes)",
+        "config": {"workload": f"{name}: {desc}", "records_per_step": sample, "record_bytes": R,
+                   "note": "CPU oracle (oracle/remap_oracle.c, plain per-record per-field memcpy) on a bounded "
+                           "sample of the workload; no GPU involved"},
+        "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": cores, "kind": "oracle",
+                         "sample": f"first {sample} records of {name} per step"},
+        "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------------------- adha arm
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="adha", choices=["adha", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--soak-s", type=float, default=1.5, help="untimed load before the timed region (clock sampling)")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    import paper_1407_4859_b200 as A
+    from adha_inputs import fill_random_device, SEED_BASE
+
+    name = args.config
+    desc, kind, n_cfg, scaling = CONFIGS[name]
+    widths, chain = chain_for(kind)
+    R = sum(widths)
+    # shard by contiguous record range: weak -> world * n_cfg records in total, strong -> n_cfg in total
+    n_total = n_cfg * world if scaling == "weak" else n_cfg
+    lo, hi = A.shard_range(n_total, world, rank)
+    n = hi - lo
+    layouts = [A.Layout(widths, lab) for lab in chain]
+    bufs = [torch.empty(max(l.nbytes(n), 1), dtype=torch.uint8, device=dev) for l in layouts]
+    fill_random_device(bufs[0], SEED_BASE + 1 + rank)
+    for b in bufs[1:]:
+        b.fill_(0xA5)
+    stream = torch.cuda.current_stream(dev)
+    n_remaps = len(chain) - 1
+    bytes_step_rank = 2 * n * R * n_remaps
+    plan = A.plan_describe(layouts[0], layouts[1])
+
+    def step():
+        for k in range(n_remaps):
+            A.remap(bufs[k], layouts[k], bufs[k + 1], layouts[k + 1], n, stream=stream)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize(dev)
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    t_end = time.perf_counter() + args.soak_s
+    while time.perf_counter() < t_end:              # untimed soak so the sampler sees the load
+        for _ in range(10):
+            step()
+        torch.cuda.synchronize(dev)
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    barrier()
+    torch.cuda.synchronize(dev)
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for i in range(args.steps):
+        starts[i].record(stream)
+        step()
+        ends[i].record(stream)
+    t1.record(stream)
+    torch.cuda.synchronize(dev)
+    barrier()
+    clk = clocks.stop()
+    ms_total = t0.elapsed_time(t1)
+    launch_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    total_bytes = 2 * n_total * R * n_remaps * args.steps
+    value = total_bytes / (ms_max * 1e-3) / 1e9
+
+    # roofline of the dominant kernel (the remap kernel is the only kernel in the step)
+    peak, peak_src = measured_peak()
+    avg_launch_ms = statistics.mean(launch_ms) / n_remaps
+    achieved = 2 * n * R / (avg_launch_ms * 1e-3) / 1e9
+    traffic = ncu_traffic(name)
+
+    # end-to-end through the public API with host buffers (pinned), H2D + D2H inside the timed region
+    e2e = None
+    if not args.no_e2e and n > 0:
+        h_src = torch.empty(layouts[0].nbytes(n), dtype=torch.uint8).pin_memory()
+        h_src.copy_(bufs[0].cpu())
+        h_out = torch.empty(layouts[-1].nbytes(n), dtype=torch.uint8).pin_memory()
+        scratch = torch.empty(min(1 << 30, max(64 << 20, 2 * (layouts[0].nbytes(n) + layouts[-1].nbytes(n)))),
+                              dtype=torch.uint8, device=dev)
+        if n_remaps == 1:
+            def e2e_step():
+                A.remap_host(h_src, layouts[0], h_out, layouts[1], n, scratch, stream=stream)
+        else:       # a chain: host in -> device chain -> host out
+            def e2e_step():
+                bufs[0].copy_(h_src, non_blocking=True)
+                step()
+                h_out.copy_(bufs[-1], non_blocking=True)
+        e2e_steps = max(3, min(args.steps, 10))
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize(dev)
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(e2e_steps):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        barrier()
+        et = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e_ms = float(et.item())
+        e2e = {"value": 2 * n_total * R * n_remaps * e2e_steps / (e_ms * 1e-3) / 1e9, "unit": "GB/s",
+               "h2d_bytes_per_step": n * R, "d2h_bytes_per_step": n * R,
+               "api": "adha_remap_host" if n_remaps == 1 else "H2D copy + adha_remap x%d + D2H copy" % n_remaps,
+               "ms_per_step": e_ms / e2e_steps}
+        del h_src, h_out, scratch
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cores = host_cores()
+        sample = min(n, 1 << 20)
+        v_all, s_all = oracle_rate(widths, chain, sample, 6.0, cores)
+        v_1, s_1 = oracle_rate(widths, chain, sample, 4.0, 1)
+        cpu = {"value": v_all, "unit": "GB/s", "cores": cores, "kind": "oracle",
+               "sample": f"first {sample} records of {name}, repeated for {s_all:.1f} s "
+                         f"(oracle/remap_oracle.c, record-range split over {cores} threads)",
+               "single_thread_value": v_1}
+
+    if rank == 0:
+        line = {
+            "metric": "remap GB/s (read+write)", "value": value, "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic (seeded random bytes generated on the device)",
+            "config": {
+                "workload": f"{name}: {desc}", "n_records_total": n_total, "n_records_per_rank": n,
+                "record_bytes": R, "remaps_per_step": n_remaps,
+                "layouts": [l.to_string() for l in layouts],
+                "bytes_per_step_total": 2 * n_total * R * n_remaps,
+                "l2": f"inputs larger than L2 ({2 * n * R / 1e9:.2f} GB moved per remap per GPU vs 126 MB L2); no flush",
+                "parallelism": f"shard by contiguous record range over {world} GPU(s), no data-path collective",
+                "kernel": {k: plan[k] for k in ("tiled", "unit", "T", "s_in", "s_out", "smem_bytes", "matched")},
+            },
+            "records_per_s": n_total * n_remaps * args.steps / (ms_max * 1e-3) / max(n_remaps, 1),
+            "pct_of_spec_8000": value / world / 8000.0 * 100.0,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "peak_source": peak_src, "kernel": "remap_tiled_kernel",
+                         "algorithmic_bytes_per_launch": 2 * n * R,
+                         "avg_launch_ms": avg_launch_ms},
+            "gpu_launches": args.steps * n_remaps,
+            "clocks": clk,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

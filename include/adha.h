@@ -1,0 +1,246 @@
+/*
+ * adha.h -- C ABI of the B200-native ADHA data-layout remap library (libadha.so).
+ *
+ * ADHA (arXiv 1407.4859, PAPER.md) chooses a data layout per program section:
+ * ODS clusters fields by affinity and PDL places REMAP edges
+ * between sections whose layouts differ.  At a remap edge the
+ * records move from the parent section's layout to the child's ("a remap
+ * operation is performed to SOA layout").  This library is that
+ * remap on B200 (hand-written sm_100a kernels), the layout descriptor it is
+ * addressed by, and the host planner that produces the layouts.
+ *
+ * Conventions (all functions):
+ *   - Plain C types only: sizes are int32_t / int64_t / uint64_t, buffers are
+ *     void pointers, a CUDA stream is passed as `void*` holding a
+ *     cudaStream_t (NULL = the legacy default stream of the current device).
+ *   - Every function returns an adha_status; ADHA_OK = 0.  On failure a
+ *     thread-local message is available from adha_last_error().  Nothing is
+ *     partially written on a validation error.
+ *   - Ownership: layouts are created and destroyed by the caller; device and
+ *     host buffers and streams belong to the caller; strings the library
+ *     returns through `char**` are freed with adha_free().
+ *   - Layout handles are immutable after creation and may be shared between
+ *     threads ("immutable after construction").
+ */
+#ifndef ADHA_H_
+#define ADHA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define ADHA_API __attribute__((visibility("default")))
+#else
+#define ADHA_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum adha_status {
+    ADHA_OK = 0,
+    ADHA_ERR_INVALID_ARG = 1,      /* null pointer, negative count, bad index          */
+    ADHA_ERR_PARSE = 2,            /* malformed layout string or planner JSON          */
+    ADHA_ERR_LAYOUT_MISMATCH = 3,  /* src/dst layouts differ in field count or widths  */
+    ADHA_ERR_CAPACITY = 4,         /* planner: a field wider than the cluster capacity */
+    ADHA_ERR_ALIGNMENT = 5,        /* a device buffer not 256-byte aligned             */
+    ADHA_ERR_OVERLAP = 6,          /* src and dst byte ranges overlap                  */
+    ADHA_ERR_TOO_LARGE = 7,        /* N * record bytes overflows 2^63                  */
+    ADHA_ERR_CUDA = 8,             /* a CUDA runtime call or kernel launch failed      */
+    ADHA_ERR_OOM = 9,              /* host allocation failed                           */
+    ADHA_ERR_UNSUPPORTED = 10,     /* outside the library's limits (see below)         */
+    ADHA_ERR_PLANNER = 11          /* planner rejected the program (no plan/device)    */
+} adha_status;
+
+/* Limits. */
+#define ADHA_MAX_FIELDS 4096       /* fields per layout                                 */
+#define ADHA_MAX_FIELD_BYTES 65536 /* bytes per field                                   */
+
+/* Opaque layout descriptor. */
+typedef struct adha_layout adha_layout;
+
+/* ------------------------------------------------------------------ version / errors */
+
+/* Library version as MAJOR*10000 + MINOR*100 + PATCH. */
+ADHA_API int32_t adha_version(void);
+
+/* Static name of a status code ("ADHA_OK", ...). Never NULL. */
+ADHA_API const char* adha_status_string(adha_status s);
+
+/* Detail of the last failure on the calling thread ("" if none).  Valid until the
+ * next adha_* call on this thread. */
+ADHA_API const char* adha_last_error(void);
+
+/* Free a string returned by the library through a char** out-parameter. NULL is ok. */
+ADHA_API void adha_free(void* p);
+
+/* ------------------------------------------------------------------ layout descriptor
+ *
+ * A layout is a partition of the record's fields into clusters (SPEC.md:55-58,
+ * [TYPE] Layout; Table 2: a cluster of >= 2 fields is an
+ * AoS group, a singleton is an SoA array).  Fields are identified by their
+ * declaration index 0..n_fields-1 and have a byte width each.
+ *
+ * Canonical form: clusters ordered by their minimum field index,
+ * fields inside a cluster by index.  A cluster record is the packed
+ * concatenation of its fields in that order (reading Q2: no padding):
+ *     stride(c) = sum of widths in c,  offset(f) = prefix sum inside c.
+ * One buffer holds one region per cluster, in canonical order, each region
+ * base aligned up to 256 bytes from the buffer start (reading Q3):
+ *     base(0) = 0,  base(c) = align256(base(c-1) + N * stride(c-1)),
+ *     bytes(L, N) = base(last) + N * stride(last).
+ * The element address of field f of record i is
+ *     addr(f, i) = base(cluster(f)) + i * stride(cluster(f)) + offset(f).
+ * Bytes between regions are never read for meaning nor written by a remap.
+ * A handle carries no record count (reading Q4): one handle serves any N.
+ */
+
+/* Create a layout from field widths and a cluster label per field.
+ *   field_widths[n_fields]      bytes per field, 1..ADHA_MAX_FIELD_BYTES
+ *   cluster_of_field[n_fields]  any int32 labels; equal labels = same cluster
+ *   out                         receives the new handle (caller destroys it)
+ * Errors: INVALID_ARG (null, n_fields outside 1..ADHA_MAX_FIELDS, width 0 or too big). */
+ADHA_API adha_status adha_layout_create(const uint32_t* field_widths, int32_t n_fields,
+                               const int32_t* cluster_of_field, adha_layout** out);
+
+/* Create a layout from its string form.  Accepts the canonical form of
+ * SPEC.md:79 "{f,g,h}|{x}|{y}" and the paper's Table-2 notation
+ * "V1,V2,V3,{U1,U2,U3},S" where a bare name is a singleton.
+ * Whitespace is ignored.  field_names[n_fields] give the names in declaration
+ * order; every name must appear exactly once.
+ * Errors: INVALID_ARG (null/bad sizes), PARSE (syntax, unknown or repeated name,
+ * missing field). */
+ADHA_API adha_status adha_layout_from_string(const char* text, const char* const* field_names,
+                                    const uint32_t* field_widths, int32_t n_fields,
+                                    adha_layout** out);
+
+/* Write the canonical string into buf (always NUL-terminated when cap > 0,
+ * truncated if needed).  field_names may be NULL: names are then "f0", "f1", ...
+ * *needed receives the full length excluding the NUL.
+ * Errors: INVALID_ARG (null layout or needed). */
+ADHA_API adha_status adha_layout_to_string(const adha_layout* layout, const char* const* field_names,
+                                  char* buf, size_t cap, size_t* needed);
+
+/* Number of fields / clusters, and R = bytes per record (sum of widths). */
+ADHA_API adha_status adha_layout_info(const adha_layout* layout, int32_t* n_fields, int32_t* n_clusters,
+                             uint64_t* record_bytes);
+
+/* Canonical cluster index of every field (out[n_fields]). */
+ADHA_API adha_status adha_layout_clusters(const adha_layout* layout, int32_t* cluster_of_field);
+
+/* bytes(L, N) as defined above.  Errors: INVALID_ARG (N < 0), TOO_LARGE. */
+ADHA_API adha_status adha_layout_bytes(const adha_layout* layout, int64_t n_records, uint64_t* out_bytes);
+
+/* Address terms of one field for an N-record instance:
+ * region_offset = base(cluster(f)), stride = stride(cluster(f)), offset = offset(f). */
+ADHA_API adha_status adha_layout_field_address(const adha_layout* layout, int32_t field, int64_t n_records,
+                                      uint64_t* region_offset, uint32_t* stride, uint32_t* offset);
+
+/* Destroy a handle.  NULL is ok. */
+ADHA_API void adha_layout_destroy(adha_layout* layout);
+
+/* ------------------------------------------------------------------ the remap (hot path)
+ *
+ * adha_remap computes, for every record i in [0, N) and every field f
+ * (PAPER.md:56-57 remap edge, PAPER.md:146 remap operation):
+ *     dst[addr_Ld(f, i) .. + w_f) = src[addr_Ls(f, i) .. + w_f)
+ * as a type-blind byte copy (NaN payloads, -0, denormals preserved bit for bit,
+ * reading Q6).  Bytes of dst outside its regions are not written.
+ *
+ *   src, dst     DEVICE pointers on the current CUDA device, each 256-byte
+ *                aligned, holding bytes(Ls, N) and bytes(Ld, N) bytes; the two
+ *                ranges must not overlap (reading Q5: out of place only)
+ *   src_layout, dst_layout   same n_fields and the same width per field (Q8)
+ *   n_records    N >= 0; N = 0 is a no-op returning ADHA_OK
+ *   stream       cudaStream_t (as void*) the kernel is enqueued on
+ *
+ * Asynchronous: the call enqueues one kernel launch on `stream` and returns;
+ * it allocates no device memory (the remap plan travels as kernel parameters).
+ * Launch errors return ADHA_ERR_CUDA; faults during execution surface at the
+ * caller's next synchronisation.
+ * Errors: INVALID_ARG, LAYOUT_MISMATCH, ALIGNMENT, OVERLAP, TOO_LARGE, CUDA. */
+ADHA_API adha_status adha_remap(const void* src, const adha_layout* src_layout,
+                       void* dst, const adha_layout* dst_layout,
+                       int64_t n_records, void* stream);
+
+/* A chain of remaps on one stream (a PDL plan with several remap edges,
+ * PAPER.md:146): buffers[k] holds the records in layouts[k];
+ * for k = 0..n_layouts-2: remap buffers[k] (layouts[k]) -> buffers[k+1]
+ * (layouts[k+1]).  Every intermediate is materialised.  Same rules as adha_remap. */
+ADHA_API adha_status adha_remap_chain(void* const* buffers, const adha_layout* const* layouts,
+                             int32_t n_layouts, int64_t n_records, void* stream);
+
+/* Contiguous shard of N records for shard g of G (reading Q10):
+ *     lo = floor(g * N / G),  hi = floor((g + 1) * N / G).
+ * Errors: INVALID_ARG (N < 0, G < 1, g outside [0, G)). */
+ADHA_API adha_status adha_shard_range(int64_t n_total, int32_t n_shards, int32_t shard,
+                             int64_t* lo, int64_t* hi);
+
+/* Single-process multi-device remap.  Shard g holds records [lo_g, hi_g) of an
+ * N-record array as its own layout instance of n_g = hi_g - lo_g records
+ * (src_shards[g] in src_layout, dst_shards[g] in dst_layout, on device
+ * device_ids[g]).  Launches adha_remap for every shard on streams[g] (as void*)
+ * and restores the caller's current device.  No data crosses devices: record i
+ * of the output depends only on record i of the input (record locality), so
+ * the shards need no exchange.  Errors: as adha_remap, per shard. */
+ADHA_API adha_status adha_remap_sharded(const void* const* src_shards, const adha_layout* src_layout,
+                               void* const* dst_shards, const adha_layout* dst_layout,
+                               int64_t n_records_total, int32_t n_shards,
+                               const int32_t* device_ids, void* const* streams);
+
+/* End-to-end remap of HOST buffers through the current device: src_host holds
+ * bytes(Ls, N), dst_host receives bytes(Ld, N) (only payload bytes written).
+ * The records are streamed in chunks through `scratch` (a DEVICE buffer of
+ * scratch_bytes, 256-byte aligned): host->device copy of a chunk, adha_remap of
+ * it, device->host copy of the result, with two chunks in flight on internal
+ * streams so both copy directions overlap the kernels.  Ordered after prior
+ * work on `stream`; later work on `stream` waits for completion.  Use pinned
+ * host memory for asynchrony.  Errors: as adha_remap; INVALID_ARG if the
+ * scratch cannot hold two chunks of at least 1 record. */
+ADHA_API adha_status adha_remap_host(const void* src_host, const adha_layout* src_layout,
+                            void* dst_host, const adha_layout* dst_layout,
+                            int64_t n_records, void* scratch, uint64_t scratch_bytes,
+                            void* stream);
+
+/* JSON description of the compiled remap plan for a layout pair (tile records,
+ * pipeline stages, unit size, per-instruction table, kernel choice) -- for
+ * tests and tooling; the hot path never calls it.  Free with adha_free. */
+ADHA_API adha_status adha_remap_plan_describe(const adha_layout* src_layout, const adha_layout* dst_layout,
+                                     char** json_out);
+
+/* ------------------------------------------------------------------ planner (host)
+ *
+ * Inputs are UTF-8 JSON documents in the SPEC.md schemas (schema_version 1):
+ *   program  {"record_count", "fields":[{"name","elem_bytes"}], "sections":[{"id",
+ *             "trip_count", "allowed_devices", "groups":[{"fields","freq","pattern","ops"}]}],
+ *             "order"}
+ *   arch     {"devices":[{"name","line_bytes","line_time_ns","throughput_ops_per_ns",
+ *             "coalescing","stream_cluster_penalty","cluster_capacity_bytes"}],
+ *             "links":[{"from","to","bandwidth_bytes_per_ns","latency_ns"}],
+ *             "same_device_remap_bandwidth_bytes_per_ns","remap_fixed_overhead_ns"}
+ *   profile  [{"section","device","layout","time_ns"}] or {"entries":[...]}
+ */
+
+/* ODS of one section on one device: affinity graph, Kruskal
+ * greedy clustering under the device's cluster capacity, untouched fields as
+ * singletons.  *layout_out = canonical string (adha_free).
+ * Errors: PARSE, PLANNER (unknown section/device, device not allowed),
+ * CAPACITY (a field wider than the capacity). */
+ADHA_API adha_status adha_plan_ods(const char* program_json, const char* arch_json,
+                          const char* section_id, const char* device, char** layout_out);
+
+/* PDL: run graph over contiguous section runs x devices, run
+ * layouts from ODS of the merged run, remap edges = moved bytes / bandwidth +
+ * overhead, shortest path.  *plan_out = JSON
+ * {"runs":[{"sections","device","layout","exec_ns"}],
+ *  "remaps":[{"boundary","after","moved","cost_ns"}], "total_ns"}.
+ * profile_json may be NULL.  Errors: PARSE, PLANNER, CAPACITY. */
+ADHA_API adha_status adha_plan_pdl(const char* program_json, const char* arch_json,
+                          const char* profile_json, char** plan_out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ADHA_H_ */

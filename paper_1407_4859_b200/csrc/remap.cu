@@ -1,0 +1,532 @@
+// remap.cu -- the ADHA remap on B200 (sm_100a): kernels, launch, and the
+// remap entry points of the C ABI.
+//
+// What it computes (adha.h): for all records i and fields f
+//     dst[addr_Ld(f,i) .. +w_f) = src[addr_Ls(f,i) .. +w_f)
+// as a type-blind copy: integer loads/stores only, never an FP instruction
+// (NaN payloads must survive, reading Q6).
+//
+// remap_tiled_kernel (the hot path):
+//   persistent CTAs, one per SM (1 CTA/SM: ~200 KB of shared memory), 9 warps:
+//   * warp 8 (producer): per tile, one TMA bulk copy (cp.async.bulk, SASS
+//     UBLKCP) per src cluster chunk into an input stage, completion counted as
+//     transaction bytes on the stage's mbarrier; s_in stages in flight;
+//   * warps 0-7 (consumers): permute the staged tile into an output buffer with
+//     32-bit (or 16/8-bit) shared loads/stores driven by a per-lane table held
+//     in registers -- conflict-free by construction for 4-byte units -- then
+//     warp 0 writes every dst cluster chunk back with one TMA bulk store each
+//     (cp.async.bulk.global.shared::cta) from a double-buffered output stage;
+//   * the last CTA finishes the N mod T tail records with plain loads/stores.
+// remap_naive_kernel: one thread per (record, field) unit copy; used only for
+//   layouts beyond the tiled kernel's limits (more than 256 fields, ...).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <set>
+#include <string>
+#include <tuple>
+
+#include "internal.h"
+#include "ptx.cuh"
+#include "remap_plan.h"
+
+namespace adha {
+namespace dev {
+
+using namespace adha::ptx;
+
+template <typename U, int NENT, int EMAX>
+__global__ void __launch_bounds__(NTHREADS, 1)
+    remap_tiled_kernel(const __grid_constant__ TiledParams p, const __grid_constant__ EntryTable<NENT> et) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const uint32_t warp = threadIdx.x >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t sbase = smem_u32(smem);
+    const uint32_t full0 = sbase;                      // s_in mbarriers: tile landed
+    const uint32_t empty0 = sbase + 8 * MAX_S_IN;      // s_in mbarriers: stage consumed
+    const uint32_t in0 = sbase + HDR_BYTES;
+    const uint32_t out0 = in0 + p.s_in * p.stage_bytes;
+
+    if (threadIdx.x == 0) {
+        for (uint32_t s = 0; s < p.s_in; ++s) {
+            mbar_init(full0 + 8 * s, 1);
+            mbar_init(empty0 + 8 * s, NCONS);
+        }
+        fence_mbarrier_init();
+    }
+    __syncthreads();
+
+    if (warp == NCONS) {
+        // ------------------------------------------------------------ TMA producer
+        uint32_t stage = 0, phase = 0;
+        for (int64_t t = blockIdx.x; t < p.n_tiles; t += gridDim.x) {
+            mbar_wait(empty0 + 8 * stage, phase ^ 1);
+            if (lane == 0) mbar_arrive_expect_tx(full0 + 8 * stage, p.tile_bytes);
+            __syncwarp();
+            const uint32_t ib = in0 + stage * p.stage_bytes;
+            for (uint32_t c = lane; c < p.n_src; c += 32) {
+                const uint32_t bytes = p.T * p.srcc[c].stride;
+                bulk_load(ib + p.srcc[c].smem, p.src + p.srcc[c].region + (uint64_t)t * bytes, bytes,
+                          full0 + 8 * stage);
+            }
+            if (++stage == p.s_in) { stage = 0; phase ^= 1; }
+        }
+        return;
+    }
+
+    // ---------------------------------------------------------------- consumers
+    // this warp's instructions i = warp + NCONS*e; lane's unit = entry i*32 + lane
+    const uint32_t ne = p.n_instr > warp ? (p.n_instr - warp + NCONS - 1) / NCONS : 0;
+    uint32_t ioff[EMAX], ooff[EMAX], din[EMAX], dout[EMAX];
+#pragma unroll
+    for (int e = 0; e < EMAX; ++e) {
+        ioff[e] = ooff[e] = din[e] = dout[e] = 0;
+        if ((uint32_t)e < ne) {
+            const uint32_t idx = (warp + NCONS * e) * 32 + lane;
+            const uint32_t v = et.off[idx];
+            ioff[e] = (v & 0xFFFFu) * (uint32_t)sizeof(U);
+            ooff[e] = (v >> 16) * (uint32_t)sizeof(U);
+            din[e] = 32u * p.srcc[et.sc[idx]].stride;
+            dout[e] = 32u * p.dstc[et.dc[idx]].stride;
+        }
+    }
+
+    uint32_t stage = 0, phase = 0, oslot = 0;
+    const uint32_t periods = p.periods;
+    for (int64_t t = blockIdx.x; t < p.n_tiles; t += gridDim.x) {
+        mbar_wait(full0 + 8 * stage, phase);
+        if (warp == 0) bulk_wait_read<S_OUT - 1>();     // output slot's previous stores have read smem
+        named_bar_sync(1, NCONS * 32);
+        const uint32_t ib = in0 + stage * p.stage_bytes;
+        const uint32_t ob = out0 + oslot * p.stage_bytes;
+#pragma unroll
+        for (int e = 0; e < EMAX; ++e) {
+            if ((uint32_t)e < ne) {
+                const uint32_t ia = ib + ioff[e], oa = ob + ooff[e];
+                const uint32_t di = din[e], dO = dout[e];
+                uint32_t q = 0;
+                for (; q + 4 <= periods; q += 4) {
+                    const U v0 = lds<U>(ia + (q + 0) * di);
+                    const U v1 = lds<U>(ia + (q + 1) * di);
+                    const U v2 = lds<U>(ia + (q + 2) * di);
+                    const U v3 = lds<U>(ia + (q + 3) * di);
+                    sts(oa + (q + 0) * dO, v0);
+                    sts(oa + (q + 1) * dO, v1);
+                    sts(oa + (q + 2) * dO, v2);
+                    sts(oa + (q + 3) * dO, v3);
+                }
+                for (; q < periods; ++q) sts(oa + q * dO, lds<U>(ia + q * di));
+            }
+        }
+        fence_proxy_async_smem();                       // STS -> visible to the TMA store
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty0 + 8 * stage); // input stage free for the producer
+        named_bar_sync(1, NCONS * 32);
+        if (warp == 0) {
+            for (uint32_t c = lane; c < p.n_dst; c += 32) {
+                const uint32_t bytes = p.T * p.dstc[c].stride;
+                bulk_store(p.dst + p.dstc[c].region + (uint64_t)t * bytes, ob + p.dstc[c].smem, bytes);
+            }
+            bulk_commit();
+        }
+        if (++stage == p.s_in) { stage = 0; phase ^= 1; }
+        oslot ^= 1;
+    }
+    if (warp == 0) bulk_wait_all();
+
+    // ---------------------------------------------------------------- tail: records [tail_lo, N)
+    if (blockIdx.x == gridDim.x - 1 && p.tail_lo < p.n_records) {
+        const int64_t n_tail = p.n_records - p.tail_lo;
+        const int64_t total = n_tail * (int64_t)p.n_fields;
+        for (int64_t k = threadIdx.x; k < total; k += NCONS * 32) {
+            const uint32_t f = (uint32_t)(k / n_tail);
+            const int64_t r = p.tail_lo + (k - (int64_t)f * n_tail);
+            const FieldDesc fd = p.fields[f];
+            const uint8_t* s = p.src + p.srcc[fd.sc].region + (uint64_t)r * p.srcc[fd.sc].stride + fd.soff;
+            uint8_t* d = p.dst + p.dstc[fd.dc].region + (uint64_t)r * p.dstc[fd.dc].stride + fd.doff;
+            for (uint32_t j = 0; j < fd.width; j += sizeof(U))
+                *reinterpret_cast<U*>(d + j) = *reinterpret_cast<const U*>(s + j);
+        }
+    }
+}
+
+__global__ void remap_naive_kernel(const __grid_constant__ NaiveParams p) {
+    const int64_t n = p.n_records;
+    const int64_t total = n * (int64_t)p.n_fields;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total; k += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t f = (uint32_t)(k / n);
+        const int64_t r = p.lo + (k - (int64_t)f * n);
+        const NaiveField& fd = p.f[f];
+        const uint8_t* s = p.src + fd.sbase + (uint64_t)r * fd.sstride + fd.soff;
+        uint8_t* d = p.dst + fd.dbase + (uint64_t)r * fd.dstride + fd.doff;
+        const uintptr_t a = (uintptr_t)s | (uintptr_t)d | fd.width;
+        uint32_t j = 0;
+        if ((a & 3) == 0) {
+            for (; j < fd.width; j += 4) *reinterpret_cast<uint32_t*>(d + j) = *reinterpret_cast<const uint32_t*>(s + j);
+        } else {
+            for (; j < fd.width; ++j) d[j] = s[j];
+        }
+    }
+}
+
+}  // namespace dev
+
+// ============================================================================ host side
+
+using namespace dev;
+
+namespace {
+
+typedef void (*TiledLauncher)(dim3, dim3, size_t, cudaStream_t, const TiledParams&, const void* table);
+
+template <typename U, int CLS>
+void launch_tiled(dim3 grid, dim3 block, size_t smem, cudaStream_t st, const TiledParams& p, const void* table) {
+    constexpr int NENT = CLASS_NENT[CLS];
+    constexpr int EMAX = CLASS_EMAX[CLS];
+    remap_tiled_kernel<U, NENT, EMAX><<<grid, block, smem, st>>>(p, *static_cast<const EntryTable<NENT>*>(table));
+}
+
+template <typename U, int CLS>
+const void* tiled_fn() {
+    constexpr int NENT = CLASS_NENT[CLS];
+    constexpr int EMAX = CLASS_EMAX[CLS];
+    return (const void*)&remap_tiled_kernel<U, NENT, EMAX>;
+}
+
+template <typename U>
+TiledLauncher pick_cls(int cls, const void** fn) {
+    switch (cls) {
+        case 0: *fn = tiled_fn<U, 0>(); return &launch_tiled<U, 0>;
+        case 1: *fn = tiled_fn<U, 1>(); return &launch_tiled<U, 1>;
+        case 2: *fn = tiled_fn<U, 2>(); return &launch_tiled<U, 2>;
+        default: *fn = tiled_fn<U, 3>(); return &launch_tiled<U, 3>;
+    }
+}
+
+TiledLauncher pick(uint32_t unit, int cls, const void** fn) {
+    if (unit == 4) return pick_cls<uint32_t>(cls, fn);
+    if (unit == 2) return pick_cls<uint16_t>(cls, fn);
+    return pick_cls<uint8_t>(cls, fn);
+}
+
+struct PlanCache {
+    std::mutex mu;
+    std::map<std::pair<uint64_t, uint64_t>, std::shared_ptr<const RemapPlan>> plans;
+    std::set<std::tuple<int, const void*>> attr_done;
+    std::map<int, int> sm_count;
+};
+PlanCache& cache() {
+    static PlanCache c;
+    return c;
+}
+
+std::shared_ptr<const RemapPlan> get_plan(const Layout& ls, const Layout& ld) {
+    PlanCache& c = cache();
+    std::lock_guard<std::mutex> g(c.mu);
+    auto key = std::make_pair(ls.id, ld.id);
+    auto it = c.plans.find(key);
+    if (it != c.plans.end()) return it->second;
+    if (c.plans.size() > 4096) c.plans.clear();
+    auto p = std::make_shared<const RemapPlan>(compile_plan(ls, ld));
+    c.plans.emplace(key, p);
+    return p;
+}
+
+adha_status cuda_fail(cudaError_t e, const char* what) {
+    return fail(ADHA_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// per-device setup: SM count and the kernel's dynamic shared memory opt-in
+adha_status device_setup(const void* fn, int* n_sm) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    PlanCache& c = cache();
+    std::lock_guard<std::mutex> g(c.mu);
+    auto it = c.sm_count.find(dev);
+    if (it == c.sm_count.end()) {
+        int sms = 0;
+        e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
+        it = c.sm_count.emplace(dev, sms).first;
+    }
+    *n_sm = it->second;
+    if (fn && !c.attr_done.count({dev, fn})) {
+        e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+        c.attr_done.insert({dev, fn});
+    }
+    return ADHA_OK;
+}
+
+adha_status launch_naive(const uint8_t* src, const Layout& ls, const std::vector<uint64_t>& bs, uint8_t* dst,
+                         const Layout& ld, const std::vector<uint64_t>& bd, int64_t lo, int64_t hi,
+                         cudaStream_t st) {
+    int n_sm = 0;
+    adha_status s = device_setup(nullptr, &n_sm);
+    if (s != ADHA_OK) return s;
+    auto P = std::make_unique<NaiveParams>();
+    for (int f0 = 0; f0 < ls.n_fields; f0 += MAXF) {
+        std::memset(P.get(), 0, sizeof(NaiveParams));
+        P->src = src;
+        P->dst = dst;
+        P->n_records = hi - lo;
+        P->lo = lo;
+        const int nf = std::min(MAXF, ls.n_fields - f0);
+        P->n_fields = (uint32_t)nf;
+        for (int k = 0; k < nf; ++k) {
+            const int f = f0 + k;
+            const int cs = ls.cluster[f], cd = ld.cluster[f];
+            P->f[k] = {bs[cs], bd[cd], (uint32_t)ls.stride[cs], (uint32_t)ld.stride[cd], ls.offset[f], ld.offset[f],
+                       ls.width[f], 0};
+        }
+        const int64_t total = (hi - lo) * (int64_t)nf;
+        const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, (int64_t)n_sm * 16));
+        remap_naive_kernel<<<(unsigned)blocks, 256, 0, st>>>(*P);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return cuda_fail(e, "remap_naive_kernel launch");
+    }
+    return ADHA_OK;
+}
+
+struct Checked {
+    uint64_t bytes_s = 0, bytes_d = 0;
+    std::vector<uint64_t> bs, bd;
+};
+
+adha_status validate(const void* src, const adha_layout* hs, const void* dst, const adha_layout* hd, int64_t n,
+                     Checked* out, bool device_buffers) {
+    if (!hs || !hd) return fail(ADHA_ERR_INVALID_ARG, "null layout");
+    if (n < 0) return fail(ADHA_ERR_INVALID_ARG, "n_records < 0");
+    const Layout& ls = hs->L;
+    const Layout& ld = hd->L;
+    if (ls.n_fields != ld.n_fields) return fail(ADHA_ERR_LAYOUT_MISMATCH, "layouts differ in field count");
+    for (int f = 0; f < ls.n_fields; ++f)
+        if (ls.width[f] != ld.width[f])
+            return fail(ADHA_ERR_LAYOUT_MISMATCH, "field " + std::to_string(f) + " differs in width");
+    if (!ls.region_bases(n, out->bs, &out->bytes_s) || !ld.region_bases(n, out->bd, &out->bytes_d))
+        return fail(ADHA_ERR_TOO_LARGE, "N * record bytes overflows");
+    if (n == 0) return ADHA_OK;
+    if (!src || !dst) return fail(ADHA_ERR_INVALID_ARG, "null buffer");
+    if (device_buffers && (((uintptr_t)src & 255) || ((uintptr_t)dst & 255)))
+        return fail(ADHA_ERR_ALIGNMENT, "src and dst must be 256-byte aligned");
+    const uintptr_t s0 = (uintptr_t)src, s1 = s0 + out->bytes_s, d0 = (uintptr_t)dst, d1 = d0 + out->bytes_d;
+    if (s0 < d1 && d0 < s1) return fail(ADHA_ERR_OVERLAP, "src and dst ranges overlap");
+    return ADHA_OK;
+}
+
+adha_status remap_checked(const uint8_t* src, const Layout& ls, uint8_t* dst, const Layout& ld, int64_t n,
+                          const Checked& ck, cudaStream_t st) {
+    if (n == 0) return ADHA_OK;
+    auto plan = get_plan(ls, ld);
+    if (!plan->tiled) return launch_naive(src, ls, ck.bs, dst, ld, ck.bd, 0, n, st);
+
+    const void* fn = nullptr;
+    TiledLauncher launch = pick(plan->unit, plan->table_class, &fn);
+    int n_sm = 0;
+    adha_status s = device_setup(fn, &n_sm);
+    if (s != ADHA_OK) return s;
+
+    auto P = std::make_unique<TiledParams>();
+    std::memset(P.get(), 0, sizeof(TiledParams));
+    P->src = src;
+    P->dst = dst;
+    P->n_records = n;
+    P->T = plan->T;
+    P->n_tiles = n / plan->T;
+    P->tail_lo = P->n_tiles * plan->T;
+    P->periods = plan->T / 32;
+    P->tile_bytes = plan->tile_bytes;
+    P->stage_bytes = plan->stage_bytes;
+    P->n_src = (uint32_t)ls.n_clusters();
+    P->n_dst = (uint32_t)ld.n_clusters();
+    P->n_fields = (uint32_t)ls.n_fields;
+    P->s_in = plan->s_in;
+    P->n_instr = plan->n_instr;
+    P->unit = plan->unit;
+    for (int c = 0; c < ls.n_clusters(); ++c) P->srcc[c] = {ck.bs[c], (uint32_t)ls.stride[c], plan->src_chunk[c]};
+    for (int c = 0; c < ld.n_clusters(); ++c) P->dstc[c] = {ck.bd[c], (uint32_t)ld.stride[c], plan->dst_chunk[c]};
+    for (int f = 0; f < ls.n_fields; ++f)
+        P->fields[f] = {(uint16_t)ls.cluster[f], (uint16_t)ld.cluster[f], ls.offset[f], ld.offset[f], ls.width[f]};
+
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(P->n_tiles, n_sm));
+    launch(dim3((unsigned)grid), dim3(NTHREADS), plan->smem_bytes, st, *P, plan->table.data());
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "remap_tiled_kernel launch");
+    return ADHA_OK;
+}
+
+}  // namespace
+}  // namespace adha
+
+using namespace adha;
+
+extern "C" adha_status adha_remap(const void* src, const adha_layout* hs, void* dst, const adha_layout* hd,
+                                  int64_t n, void* stream) {
+    clear_error();
+    Checked ck;
+    adha_status s = validate(src, hs, dst, hd, n, &ck, true);
+    if (s != ADHA_OK) return s;
+    return remap_checked((const uint8_t*)src, hs->L, (uint8_t*)dst, hd->L, n, ck, (cudaStream_t)stream);
+}
+
+extern "C" adha_status adha_remap_chain(void* const* buffers, const adha_layout* const* layouts, int32_t n_layouts,
+                                        int64_t n, void* stream) {
+    clear_error();
+    if (!buffers || !layouts || n_layouts < 2) return fail(ADHA_ERR_INVALID_ARG, "need at least two layouts");
+    for (int32_t k = 0; k + 1 < n_layouts; ++k) {
+        adha_status s = adha_remap(buffers[k], layouts[k], buffers[k + 1], layouts[k + 1], n, stream);
+        if (s != ADHA_OK) return s;
+    }
+    return ADHA_OK;
+}
+
+extern "C" adha_status adha_remap_sharded(const void* const* src_shards, const adha_layout* hs,
+                                          void* const* dst_shards, const adha_layout* hd, int64_t n_total,
+                                          int32_t n_shards, const int32_t* device_ids, void* const* streams) {
+    clear_error();
+    if (!src_shards || !dst_shards || !device_ids || !streams || n_shards < 1)
+        return fail(ADHA_ERR_INVALID_ARG, "null argument or n_shards < 1");
+    if (n_total < 0) return fail(ADHA_ERR_INVALID_ARG, "n_records_total < 0");
+    int prev = 0;
+    cudaError_t e = cudaGetDevice(&prev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    adha_status out = ADHA_OK;
+    for (int32_t g = 0; g < n_shards && out == ADHA_OK; ++g) {
+        int64_t lo = 0, hi = 0;
+        adha_shard_range(n_total, n_shards, g, &lo, &hi);
+        e = cudaSetDevice(device_ids[g]);
+        if (e != cudaSuccess) { out = cuda_fail(e, "cudaSetDevice"); break; }
+        out = adha_remap(src_shards[g], hs, dst_shards[g], hd, hi - lo, streams[g]);
+        if (out != ADHA_OK) set_error("shard " + std::to_string(g) + ": " + adha_last_error());
+    }
+    std::string msg = adha_last_error();
+    cudaSetDevice(prev);
+    if (out != ADHA_OK) set_error(msg);
+    return out;
+}
+
+// ---------------------------------------------------------------------------- host end-to-end
+namespace adha {
+namespace {
+struct HostPipe {
+    cudaStream_t s[2] = {nullptr, nullptr};
+    cudaEvent_t start = nullptr, done[2] = {nullptr, nullptr};
+};
+std::mutex g_pipe_mu;
+std::map<int, HostPipe> g_pipes;
+
+adha_status get_pipe(HostPipe** out) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    std::lock_guard<std::mutex> g(g_pipe_mu);
+    auto it = g_pipes.find(dev);
+    if (it == g_pipes.end()) {
+        HostPipe hp;
+        for (int i = 0; i < 2; ++i) {
+            if ((e = cudaStreamCreateWithFlags(&hp.s[i], cudaStreamNonBlocking)) != cudaSuccess)
+                return cuda_fail(e, "cudaStreamCreate");
+            if ((e = cudaEventCreateWithFlags(&hp.done[i], cudaEventDisableTiming)) != cudaSuccess)
+                return cuda_fail(e, "cudaEventCreate");
+        }
+        if ((e = cudaEventCreateWithFlags(&hp.start, cudaEventDisableTiming)) != cudaSuccess)
+            return cuda_fail(e, "cudaEventCreate");
+        it = g_pipes.emplace(dev, hp).first;
+    }
+    *out = &it->second;
+    return ADHA_OK;
+}
+}  // namespace
+}  // namespace adha
+
+extern "C" adha_status adha_remap_host(const void* src_host, const adha_layout* hs, void* dst_host,
+                                       const adha_layout* hd, int64_t n, void* scratch, uint64_t scratch_bytes,
+                                       void* stream) {
+    clear_error();
+    Checked ck;
+    adha_status s = validate(src_host, hs, dst_host, hd, n, &ck, false);
+    if (s != ADHA_OK) return s;
+    if (n == 0) return ADHA_OK;
+    if (!scratch || ((uintptr_t)scratch & 255)) return fail(ADHA_ERR_ALIGNMENT, "scratch must be 256-byte aligned");
+    const Layout& ls = hs->L;
+    const Layout& ld = hd->L;
+    // chunk records: two slots, each holding a src and a dst instance of `nc` records
+    const uint64_t slot = (scratch_bytes / 2) & ~uint64_t(255);
+    const uint64_t pad = 256ull * (ls.n_clusters() + ld.n_clusters() + 2);
+    const uint64_t R = ls.record_bytes;
+    if (slot <= pad + 2 * R) return fail(ADHA_ERR_INVALID_ARG, "scratch too small for two chunks");
+    int64_t nc = (int64_t)((slot - pad) / (2 * R));
+    if (nc > 4096) nc = nc / 4096 * 4096;
+    nc = std::min<int64_t>(nc, n);
+    // keep at least 4 chunks in flight for large N so copies overlap kernels
+    if (n > 4 * 4096 && nc > n / 4) nc = std::max<int64_t>(4096, (n / 4) / 4096 * 4096);
+    std::vector<uint64_t> cbs, cbd;
+    uint64_t cbytes_s = 0, cbytes_d = 0;
+    ls.region_bases(nc, cbs, &cbytes_s);
+    ld.region_bases(nc, cbd, &cbytes_d);
+    const uint64_t off_d = align256(cbytes_s);
+    if (off_d + cbytes_d > slot) return fail(ADHA_ERR_INVALID_ARG, "scratch too small");
+
+    HostPipe* hp = nullptr;
+    if ((s = get_pipe(&hp)) != ADHA_OK) return s;
+    cudaStream_t user = (cudaStream_t)stream;
+    cudaError_t e = cudaEventRecord(hp->start, user);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
+    for (int i = 0; i < 2; ++i)
+        if ((e = cudaStreamWaitEvent(hp->s[i], hp->start, 0)) != cudaSuccess) return cuda_fail(e, "cudaStreamWaitEvent");
+
+    const uint8_t* hsrc = (const uint8_t*)src_host;
+    uint8_t* hdst = (uint8_t*)dst_host;
+    int64_t k = 0;
+    for (int64_t lo = 0; lo < n; lo += nc, ++k) {
+        const int64_t m = std::min<int64_t>(nc, n - lo);
+        const int i = (int)(k & 1);
+        cudaStream_t st = hp->s[i];
+        uint8_t* dsrc = (uint8_t*)scratch + (uint64_t)i * slot;
+        uint8_t* ddst = dsrc + off_d;
+        std::vector<uint64_t> ms, md;
+        uint64_t mbs = 0, mbd = 0;
+        ls.region_bases(m, ms, &mbs);
+        ld.region_bases(m, md, &mbd);
+        for (int c = 0; c < ls.n_clusters(); ++c) {
+            e = cudaMemcpyAsync(dsrc + ms[c], hsrc + ck.bs[c] + (uint64_t)lo * ls.stride[c], (uint64_t)m * ls.stride[c],
+                                cudaMemcpyHostToDevice, st);
+            if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync H2D");
+        }
+        Checked cm;
+        cm.bs = ms;
+        cm.bd = md;
+        cm.bytes_s = mbs;
+        cm.bytes_d = mbd;
+        if ((s = remap_checked(dsrc, ls, ddst, ld, m, cm, st)) != ADHA_OK) return s;
+        for (int c = 0; c < ld.n_clusters(); ++c) {
+            e = cudaMemcpyAsync(hdst + ck.bd[c] + (uint64_t)lo * ld.stride[c], ddst + md[c], (uint64_t)m * ld.stride[c],
+                                cudaMemcpyDeviceToHost, st);
+            if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync D2H");
+        }
+    }
+    for (int i = 0; i < 2; ++i) {
+        if ((e = cudaEventRecord(hp->done[i], hp->s[i])) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
+        if ((e = cudaStreamWaitEvent(user, hp->done[i], 0)) != cudaSuccess) return cuda_fail(e, "cudaStreamWaitEvent");
+    }
+    return ADHA_OK;
+}
+
+extern "C" adha_status adha_remap_plan_describe(const adha_layout* hs, const adha_layout* hd, char** json_out) {
+    clear_error();
+    if (!hs || !hd || !json_out) return fail(ADHA_ERR_INVALID_ARG, "null argument");
+    if (hs->L.n_fields != hd->L.n_fields) return fail(ADHA_ERR_LAYOUT_MISMATCH, "layouts differ in field count");
+    for (int f = 0; f < hs->L.n_fields; ++f)
+        if (hs->L.width[f] != hd->L.width[f]) return fail(ADHA_ERR_LAYOUT_MISMATCH, "widths differ");
+    auto plan = get_plan(hs->L, hd->L);
+    std::string s = describe_plan(*plan, hs->L, hd->L);
+    *json_out = (char*)std::malloc(s.size() + 1);
+    if (!*json_out) return fail(ADHA_ERR_OOM, "out of host memory");
+    std::memcpy(*json_out, s.c_str(), s.size() + 1);
+    return ADHA_OK;
+}

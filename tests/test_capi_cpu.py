@@ -1,0 +1,283 @@
+"""CPU-side tests of the C ABI (no GPU): exported symbols, the layout descriptor
+against the oracle's address model, shard ranges, error codes, the C++ planner
+against the Python planner oracle and the paper pins, and the remap-plan
+compiler's permutation table (coverage and bank-conflict freedom)."""
+import json
+import os
+import random
+import re
+import ctypes
+
+import numpy as np
+import pytest
+
+import paper_1407_4859_b200 as A
+from oracle import planner as P
+from oracle import remap as O
+from tests.conftest import ROOT, golden
+
+
+def header_symbols():
+    text = open(os.path.join(ROOT, "include", "adha.h")).read()
+    return sorted(set(re.findall(r"ADHA_API\s+[\w\s\*]*?\b(adha_\w+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    syms = header_symbols()
+    assert len(syms) >= 20
+    lib = ctypes.CDLL(A.LIB_PATH)
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert A.version() >= 100
+
+
+def rand_layout(rng, F):
+    widths = [rng.choice([1, 2, 3, 4, 8, 12]) for _ in range(F)]
+    labels = [rng.randrange(F) for _ in range(F)]
+    return widths, labels
+
+
+def test_layout_descriptor_matches_oracle_addresses():
+    rng = random.Random(3)
+    for _ in range(300):
+        F = rng.randint(1, 12)
+        widths, labels = rand_layout(rng, F)
+        L = A.Layout(widths, labels)
+        for n in (0, 1, 5, 1000, 123457):
+            base, stride, offset, total = O.field_addresses(widths, labels, n)
+            assert L.nbytes(n) == total == O.layout_bytes(widths, labels, n)
+            for f in range(F):
+                assert L.field_address(f, n) == (base[f], stride[f], offset[f])
+        assert L.record_bytes == sum(widths)
+
+
+def test_layout_strings_and_paper_notation(expected):
+    names = ["V1", "V2", "V3", "U1", "U2", "U3", "S", "T", "interpT"]
+    w = [4] * 9
+    l = A.Layout.from_string("V1,V2,V3,{U1,U2,U3},S,T,interpT", names, w)
+    assert l.to_string() == expected["medical_aosu"]["value"]
+    l2 = A.Layout.from_string(expected["medical_aosv"]["value"], names, w)
+    assert l2.to_string() == expected["medical_aosv"]["value"]
+    assert l2.n_clusters == 7 and l2.cluster_of == [0, 0, 0, 1, 2, 3, 4, 5, 6]
+    decl = {n: i for i, n in enumerate(names)}
+    rng = random.Random(8)
+    for _ in range(100):
+        labels = [rng.randrange(9) for _ in names]
+        L = A.Layout(w, labels, names)
+        groups = {}
+        for n, lab in zip(names, labels):
+            groups.setdefault(lab, []).append(n)
+        assert L.to_string() == P.layout_string(P.canonical(list(groups.values()), decl))
+        assert A.Layout.from_string(L.to_string(), names, w).to_string() == L.to_string()
+    for bad in ["{V1,V2}", "V1,V1,V2,V3,U1,U2,U3,S,T,interpT", "{V1,{V2}},V3,U1,U2,U3,S,T,interpT", "X"]:
+        with pytest.raises(A.AdhaError) as e:
+            A.Layout.from_string(bad, names, w)
+        assert e.value.name == "ADHA_ERR_PARSE"
+
+
+def test_invalid_layouts_rejected():
+    with pytest.raises(A.AdhaError):
+        A.Layout([], [])
+    with pytest.raises(A.AdhaError):
+        A.Layout([0, 4], [0, 1])
+    with pytest.raises(A.AdhaError):
+        A.Layout.aos([4]).nbytes(-1)
+    with pytest.raises(A.AdhaError) as e:
+        A.Layout.aos([1 << 16]).nbytes(2 ** 62)
+    assert e.value.name == "ADHA_ERR_TOO_LARGE"
+
+
+def test_shard_range_floor_formula():
+    for N in (0, 1, 7, 1000, 107374182, 2 ** 40 + 3):
+        for G in (1, 2, 3, 4, 8):
+            prev = 0
+            for g in range(G):
+                lo, hi = A.shard_range(N, G, g)
+                assert lo == g * N // G and hi == (g + 1) * N // G and lo == prev
+                prev = hi
+            assert prev == N
+    with pytest.raises(A.AdhaError):
+        A.shard_range(10, 0, 0)
+    with pytest.raises(A.AdhaError):
+        A.shard_range(10, 2, 2)
+
+
+def test_remap_validation_errors_without_gpu():
+    # validation happens before any CUDA call
+    a, s = A.Layout.aos([4, 4]), A.Layout.soa([4, 4])
+    with pytest.raises(A.AdhaError) as e:
+        A.remap(256, a, 1 << 20, A.Layout.aos([4, 8]), 10, stream=0)
+    assert e.value.name == "ADHA_ERR_LAYOUT_MISMATCH"
+    with pytest.raises(A.AdhaError) as e:
+        A.remap(256 + 16, a, 1 << 20, s, 10, stream=0)
+    assert e.value.name == "ADHA_ERR_ALIGNMENT"
+    with pytest.raises(A.AdhaError) as e:
+        A.remap(4096, a, 4096 + 256, s, 100, stream=0)
+    assert e.value.name == "ADHA_ERR_OVERLAP"
+    with pytest.raises(A.AdhaError) as e:
+        A.remap(4096, a, 1 << 20, s, -1, stream=0)
+    assert e.value.name == "ADHA_ERR_INVALID_ARG"
+    A.remap(0, a, 0, s, 0, stream=0)          # N = 0 is a no-op
+
+
+# ---------------------------------------------------------------- C++ planner vs Python oracle
+
+def _prog_json(p: P.Program) -> str:
+    return json.dumps({
+        "schema_version": 1, "name": p.name, "record_count": p.record_count,
+        "fields": [{"name": f.name, "elem_bytes": f.elem_bytes} for f in p.fields],
+        "sections": [{"id": s.id, "trip_count": s.trip_count, "allowed_devices": list(s.allowed_devices),
+                      "groups": [{"fields": list(g.fields), "freq": g.freq, "pattern": g.pattern, "ops": g.ops}
+                                 for g in s.groups]} for s in p.sections],
+        "order": p.order})
+
+
+def _arch_json(a: P.Architecture) -> str:
+    return json.dumps({
+        "schema_version": 1,
+        "devices": [{"name": d.name, "line_bytes": d.line_bytes, "line_time_ns": d.line_time_ns,
+                     "throughput_ops_per_ns": d.throughput_ops_per_ns, "coalescing": d.coalescing,
+                     "stream_cluster_penalty": d.stream_cluster_penalty,
+                     "cluster_capacity_bytes": d.cluster_capacity_bytes} for d in a.devices],
+        "links": [{"from": l.src, "to": l.dst, "bandwidth_bytes_per_ns": l.bandwidth_bytes_per_ns,
+                   "latency_ns": l.latency_ns} for l in a.links],
+        "same_device_remap_bandwidth_bytes_per_ns": a.same_device_remap_bandwidth_bytes_per_ns,
+        "remap_fixed_overhead_ns": a.remap_fixed_overhead_ns})
+
+
+def test_cpp_ods_fixtures(expected):
+    prog, arch = golden("medical_aosu_program.json"), golden("medical_arch.json")
+    assert A.plan_ods(prog, arch, "aosu", "cpu") == expected["medical_aosu"]["value"]
+    km, t3 = golden("kmeans_program.json"), golden("kmeans_table3_arch.json")
+    assert A.plan_ods(km, t3, "k1", "cpu") == expected["kmeans_cap32_noncoalescing"]["value"]
+    assert A.plan_ods(km, t3, "k1", "gpu") == expected["kmeans_coalescing_soa"]["value"]
+    assert A.plan_ods(golden("c3_program.json"), golden("b200_arch.json"), "c3", "b200") == \
+        expected["c3_hybrid"]["value"]
+
+
+def test_cpp_pdl_fixtures(expected):
+    plan = A.plan_pdl(golden("medical_program.json"), golden("medical_arch.json"), golden("medical_profile.json"))
+    assert [[r["sections"], r["device"], r["layout"]] for r in plan["runs"]] == expected["medical_plan"]["runs"]
+    assert len(plan["remaps"]) == 1 and plan["remaps"][0]["moved"] == expected["medical_plan"]["remap_moved"]
+    plan = A.plan_pdl(golden("kmeans_program.json"), golden("kmeans_arch.json"), golden("kmeans_profile.json"))
+    assert [[r["sections"], r["device"], r["layout"]] for r in plan["runs"]] == expected["kmeans_plan"]["runs"]
+    assert plan["remaps"] == []
+
+
+def test_cpp_planner_errors():
+    prog, arch = golden("medical_aosu_program.json"), golden("medical_arch.json")
+    with pytest.raises(A.AdhaError) as e:
+        A.plan_ods(prog, arch, "aosu", "gpu")                 # device not allowed for the section
+    assert e.value.name == "ADHA_ERR_PLANNER"
+    with pytest.raises(A.AdhaError) as e:
+        A.plan_ods("{not json", arch, "aosu", "cpu")
+    assert e.value.name == "ADHA_ERR_PARSE"
+    bad = json.loads(json.dumps(prog))
+    bad["sections"][0]["groups"][0]["fields"].append("X")
+    with pytest.raises(A.AdhaError) as e:
+        A.plan_ods(bad, arch, "aosu", "cpu")
+    assert e.value.name == "ADHA_ERR_PLANNER"
+    narrow = json.loads(json.dumps(arch))
+    narrow["devices"][0]["cluster_capacity_bytes"] = 2
+    with pytest.raises(A.AdhaError) as e:
+        A.plan_ods(prog, narrow, "aosu", "cpu")
+    assert e.value.name == "ADHA_ERR_CAPACITY"
+
+
+def test_cpp_planner_equals_oracle_random():
+    from tests.test_oracle_planner import random_program, random_arch
+    rng = random.Random(2024)
+    for _ in range(150):
+        p, a = random_program(rng), random_arch(rng)
+        pj, aj = _prog_json(p), _arch_json(a)
+        for s in p.sections:
+            for d in s.allowed_devices:
+                try:
+                    exp = P.layout_string(P.ods(s, a.device(d), p))
+                except P.PlannerError:
+                    with pytest.raises(A.AdhaError):
+                        A.plan_ods(pj, aj, s.id, d)
+                    continue
+                assert A.plan_ods(pj, aj, s.id, d) == exp
+        try:
+            exp_plan = P.plan_to_json(P.shortest_plan(p, a), p)
+        except P.PlannerError:
+            with pytest.raises(A.AdhaError):
+                A.plan_pdl(pj, aj)
+            continue
+        got = A.plan_pdl(pj, aj)
+        assert got["total_ns"] == pytest.approx(exp_plan["total_ns"], rel=1e-12)
+        assert [[r["sections"], r["device"], r["layout"]] for r in got["runs"]] == \
+            [[r["sections"], r["device"], r["layout"]] for r in exp_plan["runs"]]
+        assert [[m["boundary"], m["moved"]] for m in got["remaps"]] == \
+            [[m["boundary"], m["moved"]] for m in exp_plan["remaps"]]
+
+
+# ---------------------------------------------------------------- remap-plan compiler (host)
+
+def _plan_checks(widths, ls, ld):
+    Ls, Ld = A.Layout(widths, ls), A.Layout(widths, ld)
+    d = A.plan_describe(Ls, Ld)
+    assert d["tiled"], d["why_naive"]
+    g = d["unit"]
+    W = sum(widths) // g
+    assert d["n_instr"] == W and d["T"] % 32 == 0
+    ent_in, ent_out = np.array(d["ent_in"]), np.array(d["ent_out"])
+    assert ent_in.size == 32 * W
+    # chunks are packed in canonical cluster order, T*stride bytes each
+    from tests.test_oracle_remap import clusters_in_order
+    T = d["T"]
+    cs, cd = clusters_in_order(ls), clusters_in_order(ld)
+    def packed(cl):
+        offs, o = [], 0
+        for c in cl:
+            offs.append(o)
+            o += T * sum(widths[f] for f in c)
+        return offs
+    assert d["src_chunk"] == packed(cs) and d["dst_chunk"] == packed(cd)
+    # every unit of the 32-record period moved exactly once, to the place the oracle's
+    # record model gives (chunk + r*stride + offset + j*g)
+    _, ss, os_, _ = O.field_addresses(widths, ls, T)
+    _, sd, od, _ = O.field_addresses(widths, ld, T)
+    chunk_s = {f: d["src_chunk"][k] for k, c in enumerate(cs) for f in c}
+    chunk_d = {f: d["dst_chunk"][k] for k, c in enumerate(cd) for f in c}
+    exp = set()
+    for r in range(32):
+        for f, w in enumerate(widths):
+            for j in range(0, w, g):
+                exp.add((int(chunk_s[f] + r * ss[f] + os_[f] + j) // g, int(chunk_d[f] + r * sd[f] + od[f] + j) // g))
+    got = set(zip(ent_in.tolist(), ent_out.tolist()))
+    assert got == exp and len(got) == ent_in.size
+    if g == 4:
+        assert d["matched"]
+        for i in range(W):                    # conflict-free: 32 distinct banks on both sides
+            assert len(set((ent_in[32 * i: 32 * i + 32] % 32).tolist())) == 32
+            assert len(set((ent_out[32 * i: 32 * i + 32] % 32).tolist())) == 32
+    return d
+
+
+def test_plan_compiler_tables():
+    w16 = [8 if i % 4 == 3 else 4 for i in range(16)]
+    d = _plan_checks(w16, [0] * 16, list(range(16)))                    # C2 AoS -> SoA
+    assert d["unit"] == 4
+    w64 = [8 if i % 4 == 3 else 4 for i in range(64)]
+    hyb = P.parse_layout(golden("expected.json")["c3_hybrid"]["value"], {f"f{i}": i for i in range(64)})
+    lab = [0] * 64
+    for c, cl in enumerate(hyb):
+        for n in cl:
+            lab[int(n[1:])] = c
+    _plan_checks(w64, list(range(64)), lab)                             # C3 SoA -> hybrid
+    med = [4] * 9
+    _plan_checks(med, [0] * 9, [0, 0, 0, 1, 2, 3, 4, 5, 6])            # C4 AoS -> AoSV
+    _plan_checks([4, 4, 4], [0, 0, 0], [0, 1, 2])                       # C1
+    rng = random.Random(11)
+    for _ in range(40):
+        F = rng.randint(1, 10)
+        widths = [rng.choice([1, 2, 3, 4, 8]) for _ in range(F)]
+        _plan_checks(widths, [rng.randrange(F) for _ in range(F)], [rng.randrange(F) for _ in range(F)])
+
+
+def test_plan_falls_back_beyond_limits():
+    widths = [4] * 300
+    d = A.plan_describe(A.Layout.aos(widths), A.Layout.soa(widths))
+    assert not d["tiled"] and "fields" in d["why_naive"]

@@ -1,0 +1,258 @@
+"""GPU parity: the CUDA remap (through the C ABI) against the CPU oracle.
+
+Bit-exact is the bar (integer/byte work; SURVEY.md 8(c) c1 -- the result is
+unique).  Small N: element by element over the whole dst buffer, including the
+sentinel-filled gaps between regions.  Full BASELINE sizes: every byte at C2,
+sampled records (one output at a time from the oracle's address model) at C3,
+C4, C5, in the launch configuration bench.py times.
+"""
+import os
+
+import numpy as np
+import pytest
+
+from adha_inputs import config_widths, field_columns, tagged_columns, fill_random_device, SEED_BASE
+from oracle import remap as O
+from tests.gpu_util import SENT, run_remap, sample_records, gather_fields_dev, sentinel_dev, to_dev
+from tests.test_oracle_remap import set_partitions
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1407_4859_b200 as A  # noqa: E402
+
+
+def oracle_dst(src, ls, ld, widths, n):
+    dst = np.full(O.layout_bytes(widths, ld, n), SENT, np.uint8)
+    O.remap(src, ls, dst, ld, widths, n, threads=min(8, os.cpu_count() or 1))
+    return dst
+
+
+def check_pair(widths, ls, ld, n, cols=None, seed=0):
+    cols = cols if cols is not None else field_columns(seed, n, widths)
+    src = O.pack(cols, widths, ls, n, fill=0x3C)
+    got = run_remap(A, src, A.Layout(widths, ls), A.Layout(widths, ld), n)
+    exp = oracle_dst(src, ls, ld, widths, n)
+    assert got.shape == exp.shape
+    if not np.array_equal(got, exp):
+        bad = np.nonzero(got != exp)[0]
+        raise AssertionError(f"mismatch at {bad.size} bytes, first {bad[:8]} (widths={widths} ls={ls} ld={ld} n={n})")
+
+
+def plan_T(widths, ls, ld):
+    return A.plan_describe(A.Layout(widths, ls), A.Layout(widths, ld))["T"]
+
+
+# ----------------------------------------------------------------------------- C1
+
+def test_c1_xyz_aos_soa_and_back():
+    widths, n = [4, 4, 4], 1024
+    cols = field_columns(SEED_BASE + 0, n, widths)
+    aos, soa = [0, 0, 0], [0, 1, 2]
+    src = O.pack(cols, widths, aos, n)
+    La, Ls = A.Layout(widths, aos), A.Layout(widths, soa)
+    mid = run_remap(A, src, La, Ls, n)
+    assert np.array_equal(mid, oracle_dst(src, aos, soa, widths, n))
+    back = run_remap(A, mid, Ls, La, n)
+    assert np.array_equal(back, src)
+
+
+# ----------------------------------------------------------------------------- brute force
+
+@pytest.mark.parametrize("widths", [[1, 2, 3, 4, 8], [4, 4, 4, 8, 4], [2, 2, 6, 4, 2]])
+def test_all_layout_pairs_5_fields(widths):
+    parts = set_partitions(5)
+    rng = np.random.default_rng(sum(widths))
+    for ls in parts:
+        for ld in parts:
+            T = plan_T(widths, ls, ld)
+            n = 3 * T + 5
+            check_pair(widths, ls, ld, n, cols=tagged_columns(n, widths))
+    for _ in range(60):                                   # edge record counts on random pairs
+        ls, ld = parts[rng.integers(52)], parts[rng.integers(52)]
+        T = plan_T(widths, ls, ld)
+        for n in (0, 1, 15, 16, 17, 31, 32, 33, T - 1, T, T + 1):
+            check_pair(widths, ls, ld, n, seed=n)
+
+
+# ----------------------------------------------------------------------------- config shapes, small N
+
+def c3_labels():
+    from oracle import planner as P
+    from tests.conftest import golden
+    hyb = P.parse_layout(golden("expected.json")["c3_hybrid"]["value"], {f"f{i}": i for i in range(64)})
+    lab = [0] * 64
+    for c, cl in enumerate(hyb):
+        for nm in cl:
+            lab[int(nm[1:])] = c
+    return lab
+
+
+AOSV = [0, 0, 0, 1, 2, 3, 4, 5, 6]
+
+
+@pytest.mark.parametrize("name,widths,ls,ld", [
+    ("C2", config_widths(16), [0] * 16, list(range(16))),
+    ("C2-back", config_widths(16), list(range(16)), [0] * 16),
+    ("C3", config_widths(64), list(range(64)), c3_labels()),
+    ("C3-back", config_widths(64), c3_labels(), list(range(64))),
+    ("C4-aos-aosv", [4] * 9, [0] * 9, AOSV),
+    ("C4-aosv-soa", [4] * 9, AOSV, list(range(9))),
+    ("C4-soa-aos", [4] * 9, list(range(9)), [0] * 9),
+    ("P2-soa-4x8", [4] * 32, list(range(32)), [i // 8 for i in range(32)]),
+    ("identity-hybrid", [4] * 9, AOSV, AOSV),
+])
+def test_config_shapes_small(name, widths, ls, ld):
+    T = plan_T(widths, ls, ld)
+    for n in (1, 33, T + 7, 5 * T + 31, 151 * T + 3):
+        check_pair(widths, ls, ld, n, seed=n)
+
+
+def test_nan_payloads_bit_exact():
+    widths = [4, 8, 4, 8, 4, 4, 4, 8]
+    n = 50_000
+    cols = field_columns(7, n, widths)
+    f32 = cols[0].view(np.uint32).ravel()
+    assert np.any(((f32 >> 23) & 0xFF) == 0xFF)
+    check_pair(widths, [0] * 8, list(range(8)), n, cols=cols)
+    check_pair(widths, list(range(8)), [0, 0, 1, 1, 1, 2, 3, 3], n, cols=cols)
+
+
+def test_naive_fallback_many_fields():
+    widths = [4, 2, 1, 8] * 75                              # 300 fields > tiled limit
+    d = A.plan_describe(A.Layout.aos(widths), A.Layout.soa(widths))
+    assert not d["tiled"]
+    check_pair(widths, [0] * 300, list(range(300)), 777)
+
+
+# ----------------------------------------------------------------------------- errors on device pointers
+
+def test_device_pointer_errors():
+    a, s = A.Layout.aos([4, 4]), A.Layout.soa([4, 4])
+    buf = torch.zeros(1 << 20, dtype=torch.uint8, device="cuda")
+    with pytest.raises(A.AdhaError) as e:
+        A.remap(buf[16:], a, buf[4096:], s, 10)
+    assert e.value.name == "ADHA_ERR_ALIGNMENT"
+    with pytest.raises(A.AdhaError) as e:
+        A.remap(buf, a, buf[256:], s, 1000)
+    assert e.value.name == "ADHA_ERR_OVERLAP"
+
+
+def test_side_stream():
+    widths = config_widths(16)
+    n = 100_000
+    cols = field_columns(1, n, widths)
+    src = O.pack(cols, widths, [0] * 16, n)
+    La, Ls = A.Layout.aos(widths), A.Layout.soa(widths)
+    s = torch.cuda.Stream()
+    d_src = to_dev(src)
+    d_dst = sentinel_dev(Ls.nbytes(n))
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s):
+        A.remap(d_src, La, d_dst, Ls, n, stream=s)
+    s.synchronize()
+    assert np.array_equal(d_dst.cpu().numpy(), oracle_dst(src, [0] * 16, list(range(16)), widths, n))
+
+
+# ----------------------------------------------------------------------------- full BASELINE sizes
+
+def test_c2_full_size_every_byte():
+    widths, n = config_widths(16), 10_000_000
+    aos, soa = [0] * 16, list(range(16))
+    La, Ls = A.Layout(widths, aos), A.Layout(widths, soa)
+    src = torch.empty(La.nbytes(n), dtype=torch.uint8, device="cuda")
+    fill_random_device(src, SEED_BASE + 1)
+    dst = sentinel_dev(Ls.nbytes(n))
+    A.remap(src, La, dst, Ls, n)
+    torch.cuda.synchronize()
+    h_src = src.cpu().numpy()
+    exp = oracle_dst(h_src, aos, soa, widths, n)
+    assert np.array_equal(dst.cpu().numpy(), exp)
+
+
+def sampled_check(src, Ls_lab, dst, Ld_lab, widths, n, T, seed=0):
+    recs = sample_records(n, T, seed=seed)
+    bs, ss, os_, _ = O.field_addresses(widths, Ls_lab, n)
+    bd, sd, od, tot = O.field_addresses(widths, Ld_lab, n)
+    a = gather_fields_dev(src, widths, bs, ss, os_, recs)
+    b = gather_fields_dev(dst, widths, bd, sd, od, recs)
+    assert np.array_equal(a, b), f"{np.count_nonzero((a != b).any(1))} sampled records differ"
+    # gap bytes (between regions) still hold the sentinel
+    regions = sorted({(int(bd[f]), int(sd[f])) for f in range(len(widths))})
+    for (b0, s0), (b1, _) in zip(regions, regions[1:]):
+        gap = dst[b0 + n * s0: b1]
+        if gap.numel():
+            assert bool((gap == SENT).all())
+
+
+@pytest.mark.parametrize("cfg", ["C3", "C5"])
+def test_full_size_sampled(cfg):
+    if cfg == "C3":
+        widths, n, ls, ld = config_widths(64), 50_000_000, list(range(64)), c3_labels()
+    else:
+        widths, n, ls, ld = config_widths(16), 107_374_182, [0] * 16, list(range(16))
+    Ls, Ld = A.Layout(widths, ls), A.Layout(widths, ld)
+    src = torch.empty(Ls.nbytes(n), dtype=torch.uint8, device="cuda")
+    fill_random_device(src, SEED_BASE + (2 if cfg == "C3" else 4))
+    dst = sentinel_dev(Ld.nbytes(n))
+    A.remap(src, Ls, dst, Ld, n)
+    torch.cuda.synchronize()
+    sampled_check(src, ls, dst, ld, widths, n, plan_T(widths, ls, ld))
+    del src, dst
+    torch.cuda.empty_cache()
+
+
+def test_c4_pdl_chain_full_size():
+    widths, n = [4] * 9, (2 ** 31) // 36
+    labs = [[0] * 9, AOSV, list(range(9)), [0] * 9]
+    lays = [A.Layout(widths, l) for l in labs]
+    bufs = [torch.empty(l.nbytes(n), dtype=torch.uint8, device="cuda") for l in lays]
+    fill_random_device(bufs[0], SEED_BASE + 3)
+    for b in bufs[1:]:
+        b.fill_(SENT)
+    A.remap_chain(bufs, lays, n)
+    torch.cuda.synchronize()
+    for k in range(3):
+        sampled_check(bufs[k], labs[k], bufs[k + 1], labs[k + 1], widths, n, plan_T(widths, labs[k], labs[k + 1]),
+                      seed=k)
+    assert torch.equal(bufs[3], bufs[0])                    # AoS -> AoSV -> SoA -> AoS is the identity
+
+
+def test_sharded_on_one_device():
+    widths, n, G = config_widths(16), 3_000_001, 4
+    aos, soa = [0] * 16, list(range(16))
+    La, Ls = A.Layout(widths, aos), A.Layout(widths, soa)
+    cols = field_columns(9, n, widths)
+    srcs, dsts, exp_cols = [], [], []
+    for g in range(G):
+        lo, hi = A.shard_range(n, G, g)
+        sub = [c[lo:hi] for c in cols]
+        srcs.append(to_dev(O.pack(sub, widths, aos, hi - lo)))
+        dsts.append(sentinel_dev(Ls.nbytes(hi - lo)))
+    streams = [torch.cuda.Stream() for _ in range(G)]
+    torch.cuda.synchronize()
+    A.remap_sharded(srcs, La, dsts, Ls, n, [0] * G, streams)
+    torch.cuda.synchronize()
+    got = [[] for _ in widths]
+    for g in range(G):
+        lo, hi = A.shard_range(n, G, g)
+        for f, c in enumerate(O.unpack(dsts[g].cpu().numpy(), widths, soa, hi - lo)):
+            got[f].append(c)
+    for f in range(16):                                      # shard union == the 1-GPU result
+        assert np.array_equal(np.concatenate(got[f]), cols[f])
+
+
+def test_remap_host_end_to_end():
+    widths, n = config_widths(16), 2_000_003
+    aos, soa = [0] * 16, list(range(16))
+    La, Ls = A.Layout(widths, aos), A.Layout(widths, soa)
+    h_src = torch.empty(La.nbytes(n), dtype=torch.uint8).pin_memory()
+    h_src.copy_(torch.from_numpy(O.pack(field_columns(5, n, widths), widths, aos, n)))
+    h_dst = torch.full((Ls.nbytes(n),), SENT, dtype=torch.uint8).pin_memory()
+    scratch = torch.empty(64 << 20, dtype=torch.uint8, device="cuda")
+    A.remap_host(h_src, La, h_dst, Ls, n, scratch)
+    torch.cuda.synchronize()
+    assert np.array_equal(h_dst.numpy(), oracle_dst(h_src.numpy(), aos, soa, widths, n))
