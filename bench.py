@@ -230,6 +230,7 @@ def main():
     ap.add_argument("--impl", default="adha", choices=["adha", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-copy-ref", action="store_true")
     ap.add_argument("--soak-s", type=float, default=1.5, help="untimed load before the timed region (clock sampling)")
     args = ap.parse_args()
 
@@ -311,6 +312,23 @@ def main():
     total_bytes = 2 * n_total * R * n_remaps * args.steps
     value = total_bytes / (ms_max * 1e-3) / 1e9
 
+    # same-run torch copy_ of the same traffic (N*R bytes read + N*R written): the box's copy ceiling now
+    copy_gbs = None
+    if n > 0 and not args.no_copy_ref:
+        ca = torch.empty(n * R, dtype=torch.uint8, device=dev)
+        cb = torch.empty_like(ca)
+        for _ in range(3):
+            cb.copy_(ca)
+        c0 = torch.cuda.Event(enable_timing=True)
+        c1 = torch.cuda.Event(enable_timing=True)
+        c0.record(stream)
+        for _ in range(args.steps):
+            cb.copy_(ca)
+        c1.record(stream)
+        torch.cuda.synchronize(dev)
+        copy_gbs = 2 * n * R * args.steps / (c0.elapsed_time(c1) * 1e-3) / 1e9
+        del ca, cb
+
     # roofline of the dominant kernel (the remap kernel is the only kernel in the step)
     peak, peak_src = measured_peak()
     avg_launch_ms = statistics.mean(launch_ms) / n_remaps
@@ -384,11 +402,14 @@ def main():
             },
             "records_per_s": n_total * n_remaps * args.steps / (ms_max * 1e-3) / max(n_remaps, 1),
             "pct_of_spec_8000": value / world / 8000.0 * 100.0,
+            "same_run_copy_gbs_per_gpu": copy_gbs,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "peak_source": peak_src, "kernel": "remap_tiled_kernel",
                          "algorithmic_bytes_per_launch": 2 * n * R,
-                         "avg_launch_ms": avg_launch_ms},
+                         "avg_launch_ms": avg_launch_ms,
+                         "launch_ms_min": min(launch_ms) / n_remaps,
+                         "launch_ms_max": max(launch_ms) / n_remaps},
             "gpu_launches": args.steps * n_remaps,
             "clocks": clk,
             "e2e": e2e,

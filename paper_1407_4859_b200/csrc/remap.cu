@@ -39,13 +39,62 @@ namespace dev {
 
 using namespace adha::ptx;
 
+// Copy-out plan of one consumer thread for the current component: the thread writes the
+// 16-byte vectors b = tid*16 + u*NT*16 (u < nv) of a staged tile (dst chunks packed in
+// cluster order).  Vector u lands at dst + gofs[u] + lt * gstep[u] for local tile lt.
+// The mapping is the same for every tile of the component, so it is computed once per
+// component switch and kept in registers.
+constexpr uint32_t VMAX = 14;                  // 14 * 16 B * 256 threads = 57344 B >= stage_bytes
+
+__device__ __forceinline__ uint32_t copy_plan(const TiledParams& p, uint32_t c_lo, uint32_t T, uint32_t total,
+                                              uint32_t tid, uint64_t (&gofs)[VMAX], uint32_t (&gstep)[VMAX]) {
+    constexpr uint32_t NT = NCONS * 32;
+    uint32_t c = c_lo, cbeg = 0, cend = T * p.dstc[c].stride;
+    uint32_t nv = 0;
+#pragma unroll
+    for (uint32_t u = 0; u < VMAX; ++u) {
+        const uint32_t b = tid * 16 + u * NT * 16;
+        gofs[u] = 0;
+        gstep[u] = 0;
+        if (b < total) {
+            while (b >= cend) {
+                ++c;
+                cbeg = cend;
+                cend = cbeg + T * p.dstc[c].stride;
+            }
+            gofs[u] = p.dstc[c].region + (b - cbeg);
+            gstep[u] = cend - cbeg;
+            nv = u + 1;
+        }
+    }
+    return nv;
+}
+
+// LDS.128 -> STG.128 of one staged tile, four vectors in flight per step
+__device__ __forceinline__ void copy_out(uint8_t* dst, uint32_t sm_base, uint32_t tid, int64_t lt, uint32_t nv,
+                                         const uint64_t (&gofs)[VMAX], const uint32_t (&gstep)[VMAX]) {
+    constexpr uint32_t NT = NCONS * 32;
+#pragma unroll
+    for (uint32_t u0 = 0; u0 < VMAX; u0 += 4) {
+        if (u0 < nv) {
+            uint4 val[4];
+#pragma unroll
+            for (uint32_t u = u0; u < u0 + 4 && u < VMAX; ++u)
+                if (u < nv) val[u - u0] = lds128(sm_base + tid * 16 + u * NT * 16);
+#pragma unroll
+            for (uint32_t u = u0; u < u0 + 4 && u < VMAX; ++u)
+                if (u < nv) stg128(dst + gofs[u] + (uint64_t)lt * gstep[u], val[u - u0]);
+        }
+    }
+}
+
 template <typename U, int NENT, int EMAX>
 __global__ void __launch_bounds__(NTHREADS, 1)
     remap_tiled_kernel(const __grid_constant__ TiledParams p, const __grid_constant__ EntryTable<NENT> et) {
     extern __shared__ __align__(1024) uint8_t smem[];
     const uint32_t warp = threadIdx.x >> 5;
     const uint32_t lane = threadIdx.x & 31;
-    const uint32_t sbase = smem_u32(smem);
+    const uint32_t sbase = (smem_u32(smem) + 127u) & ~127u;
     const uint32_t full0 = sbase;                      // s_in mbarriers: tile landed
     const uint32_t empty0 = sbase + 8 * MAX_S_IN;      // s_in mbarriers: stage consumed
     const uint32_t in0 = sbase + HDR_BYTES;
@@ -62,15 +111,18 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
     if (warp == NCONS) {
         // ------------------------------------------------------------ TMA producer
-        uint32_t stage = 0, phase = 0;
-        for (int64_t t = blockIdx.x; t < p.n_tiles; t += gridDim.x) {
+        uint32_t stage = 0, phase = 0, k = 0;
+        for (int64_t t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
+            while (t >= p.comp[k].tile_base + p.comp[k].n_tiles) ++k;
+            const int64_t lt = t - p.comp[k].tile_base;
+            const uint32_t T = p.comp[k].T;
             mbar_wait(empty0 + 8 * stage, phase ^ 1);
-            if (lane == 0) mbar_arrive_expect_tx(full0 + 8 * stage, p.tile_bytes);
+            if (lane == 0) mbar_arrive_expect_tx(full0 + 8 * stage, p.comp[k].tile_bytes);
             __syncwarp();
             const uint32_t ib = in0 + stage * p.stage_bytes;
-            for (uint32_t c = lane; c < p.n_src; c += 32) {
-                const uint32_t bytes = p.T * p.srcc[c].stride;
-                bulk_load(ib + p.srcc[c].smem, p.src + p.srcc[c].region + (uint64_t)t * bytes, bytes,
+            for (uint32_t c = p.comp[k].sc_lo + lane; c < p.comp[k].sc_hi; c += 32) {
+                const uint32_t bytes = T * p.srcc[c].stride;
+                bulk_load(ib + p.srcc[c].smem, p.src + p.srcc[c].region + (uint64_t)lt * bytes, bytes,
                           full0 + 8 * stage);
             }
             if (++stage == p.s_in) { stage = 0; phase ^= 1; }
@@ -79,73 +131,87 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
 
     // ---------------------------------------------------------------- consumers
-    // this warp's instructions i = warp + NCONS*e; lane's unit = entry i*32 + lane
-    const uint32_t ne = p.n_instr > warp ? (p.n_instr - warp + NCONS - 1) / NCONS : 0;
+    const uint32_t tid = threadIdx.x;
     uint32_t ioff[EMAX], ooff[EMAX], din[EMAX], dout[EMAX];
+    uint64_t gofs[VMAX];
+    uint32_t gstep[VMAX];
+    uint32_t ne = 0, nv = 0;
+    int k_cur = -1;
+    uint32_t stage = 0, phase = 0, oslot = 0, k = 0;
+    for (int64_t t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
+        while (t >= p.comp[k].tile_base + p.comp[k].n_tiles) ++k;
+        const int64_t lt = t - p.comp[k].tile_base;
+        const uint32_t T = p.comp[k].T;
+        if ((int)k != k_cur) {
+            // this warp's instructions of component k: i = warp + NCONS*e; lane's unit = entry i*32 + lane
+            k_cur = (int)k;
+            nv = copy_plan(p, p.comp[k].dc_lo, T, p.comp[k].tile_bytes, tid, gofs, gstep);
+            const uint32_t W = p.comp[k].n_instr;
+            ne = W > warp ? (W - warp + NCONS - 1) / NCONS : 0;
 #pragma unroll
-    for (int e = 0; e < EMAX; ++e) {
-        ioff[e] = ooff[e] = din[e] = dout[e] = 0;
-        if ((uint32_t)e < ne) {
-            const uint32_t idx = (warp + NCONS * e) * 32 + lane;
-            const uint32_t v = et.off[idx];
-            ioff[e] = (v & 0xFFFFu) * (uint32_t)sizeof(U);
-            ooff[e] = (v >> 16) * (uint32_t)sizeof(U);
-            din[e] = 32u * p.srcc[et.sc[idx]].stride;
-            dout[e] = 32u * p.dstc[et.dc[idx]].stride;
-        }
-    }
-
-    uint32_t stage = 0, phase = 0, oslot = 0;
-    const uint32_t periods = p.periods;
-    for (int64_t t = blockIdx.x; t < p.n_tiles; t += gridDim.x) {
-        mbar_wait(full0 + 8 * stage, phase);
-        if (warp == 0) bulk_wait_read<S_OUT - 1>();     // output slot's previous stores have read smem
-        named_bar_sync(1, NCONS * 32);
-        const uint32_t ib = in0 + stage * p.stage_bytes;
-        const uint32_t ob = out0 + oslot * p.stage_bytes;
-#pragma unroll
-        for (int e = 0; e < EMAX; ++e) {
-            if ((uint32_t)e < ne) {
-                const uint32_t ia = ib + ioff[e], oa = ob + ooff[e];
-                const uint32_t di = din[e], dO = dout[e];
-                uint32_t q = 0;
-                for (; q + 4 <= periods; q += 4) {
-                    const U v0 = lds<U>(ia + (q + 0) * di);
-                    const U v1 = lds<U>(ia + (q + 1) * di);
-                    const U v2 = lds<U>(ia + (q + 2) * di);
-                    const U v3 = lds<U>(ia + (q + 3) * di);
-                    sts(oa + (q + 0) * dO, v0);
-                    sts(oa + (q + 1) * dO, v1);
-                    sts(oa + (q + 2) * dO, v2);
-                    sts(oa + (q + 3) * dO, v3);
+            for (int e = 0; e < EMAX; ++e) {
+                ioff[e] = ooff[e] = din[e] = dout[e] = 0;
+                if ((uint32_t)e < ne) {
+                    const uint32_t idx = (p.comp[k].instr_base + warp + NCONS * e) * 32 + lane;
+                    const uint32_t v = et.off[idx];
+                    const ClusterDesc& cs = p.srcc[et.sc[idx]];
+                    const ClusterDesc& cd = p.dstc[et.dc[idx]];
+                    ioff[e] = cs.smem + (v & 0xFFFFu) * (uint32_t)sizeof(U);
+                    ooff[e] = cd.smem + (v >> 16) * (uint32_t)sizeof(U);
+                    din[e] = 32u * cs.stride;
+                    dout[e] = 32u * cd.stride;
                 }
-                for (; q < periods; ++q) sts(oa + q * dO, lds<U>(ia + q * di));
             }
         }
-        fence_proxy_async_smem();                       // STS -> visible to the TMA store
-        __syncwarp();
-        if (lane == 0) mbar_arrive(empty0 + 8 * stage); // input stage free for the producer
-        named_bar_sync(1, NCONS * 32);
-        if (warp == 0) {
-            for (uint32_t c = lane; c < p.n_dst; c += 32) {
-                const uint32_t bytes = p.T * p.dstc[c].stride;
-                bulk_store(p.dst + p.dstc[c].region + (uint64_t)t * bytes, ob + p.dstc[c].smem, bytes);
+        mbar_wait(full0 + 8 * stage, phase);
+        const uint32_t ib = in0 + stage * p.stage_bytes;
+        if (p.comp[k].identity) {
+            copy_out(p.dst, ib, tid, lt, nv, gofs, gstep);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty0 + 8 * stage);
+        } else {
+            const uint32_t ob = out0 + oslot * p.stage_bytes;
+            const uint32_t periods = T / 32;
+#pragma unroll
+            for (int e = 0; e < EMAX; ++e) {
+                if ((uint32_t)e < ne) {
+                    const uint32_t ia = ib + ioff[e], oa = ob + ooff[e];
+                    const uint32_t di = din[e], dO = dout[e];
+                    uint32_t q = 0;
+                    for (; q + 4 <= periods; q += 4) {
+                        const U v0 = lds<U>(ia + (q + 0) * di);
+                        const U v1 = lds<U>(ia + (q + 1) * di);
+                        const U v2 = lds<U>(ia + (q + 2) * di);
+                        const U v3 = lds<U>(ia + (q + 3) * di);
+                        sts(oa + (q + 0) * dO, v0);
+                        sts(oa + (q + 1) * dO, v1);
+                        sts(oa + (q + 2) * dO, v2);
+                        sts(oa + (q + 3) * dO, v3);
+                    }
+                    for (; q < periods; ++q) sts(oa + q * dO, lds<U>(ia + q * di));
+                }
             }
-            bulk_commit();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty0 + 8 * stage);    // input stage free for the producer
+            named_bar_sync(1, NCONS * 32);                      // output tile complete
+            copy_out(p.dst, ob, tid, lt, nv, gofs, gstep);
+            oslot ^= 1;
         }
         if (++stage == p.s_in) { stage = 0; phase ^= 1; }
-        oslot ^= 1;
     }
-    if (warp == 0) bulk_wait_all();
 
-    // ---------------------------------------------------------------- tail: records [tail_lo, N)
-    if (blockIdx.x == gridDim.x - 1 && p.tail_lo < p.n_records) {
-        const int64_t n_tail = p.n_records - p.tail_lo;
-        const int64_t total = n_tail * (int64_t)p.n_fields;
-        for (int64_t k = threadIdx.x; k < total; k += NCONS * 32) {
-            const uint32_t f = (uint32_t)(k / n_tail);
-            const int64_t r = p.tail_lo + (k - (int64_t)f * n_tail);
-            const FieldDesc fd = p.fields[f];
+    // ---------------------------------------------------------------- tails: records [n_tiles*T, N)
+    for (uint32_t kk = 0; kk < p.n_comp; ++kk) {
+        if (gridDim.x - 1 - (kk % gridDim.x) != blockIdx.x) continue;
+        const CompDesc& K = p.comp[kk];
+        const int64_t lo = K.n_tiles * (int64_t)K.T;
+        const int64_t n_tail = p.n_records - lo;
+        if (n_tail <= 0) continue;
+        const int64_t total = n_tail * (int64_t)(K.f_hi - K.f_lo);
+        for (int64_t x = tid; x < total; x += NCONS * 32) {
+            const uint32_t f = K.f_lo + (uint32_t)(x / n_tail);
+            const int64_t r = lo + (x % n_tail);
+            const FieldDesc fd = et.fields[f];
             const uint8_t* s = p.src + p.srcc[fd.sc].region + (uint64_t)r * p.srcc[fd.sc].stride + fd.soff;
             uint8_t* d = p.dst + p.dstc[fd.dc].region + (uint64_t)r * p.dstc[fd.dc].stride + fd.doff;
             for (uint32_t j = 0; j < fd.width; j += sizeof(U))
@@ -177,7 +243,12 @@ __global__ void remap_naive_kernel(const __grid_constant__ NaiveParams p) {
 
 // ============================================================================ host side
 
+
 using namespace dev;
+
+static_assert(sizeof(dev::TiledParams) + sizeof(dev::EntryTable<dev::CLASS_NENT[3]>) <= 32764,
+              "tiled kernel parameters exceed the 32764-byte kernel parameter limit");
+static_assert(sizeof(dev::NaiveParams) <= 32764, "naive kernel parameters too large");
 
 namespace {
 
@@ -336,25 +407,46 @@ adha_status remap_checked(const uint8_t* src, const Layout& ls, uint8_t* dst, co
     P->src = src;
     P->dst = dst;
     P->n_records = n;
-    P->T = plan->T;
-    P->n_tiles = n / plan->T;
-    P->tail_lo = P->n_tiles * plan->T;
-    P->periods = plan->T / 32;
-    P->tile_bytes = plan->tile_bytes;
     P->stage_bytes = plan->stage_bytes;
-    P->n_src = (uint32_t)ls.n_clusters();
-    P->n_dst = (uint32_t)ld.n_clusters();
-    P->n_fields = (uint32_t)ls.n_fields;
     P->s_in = plan->s_in;
-    P->n_instr = plan->n_instr;
+    P->n_comp = (uint32_t)plan->comps.size();
     P->unit = plan->unit;
-    for (int c = 0; c < ls.n_clusters(); ++c) P->srcc[c] = {ck.bs[c], (uint32_t)ls.stride[c], plan->src_chunk[c]};
-    for (int c = 0; c < ld.n_clusters(); ++c) P->dstc[c] = {ck.bd[c], (uint32_t)ld.stride[c], plan->dst_chunk[c]};
-    for (int f = 0; f < ls.n_fields; ++f)
-        P->fields[f] = {(uint16_t)ls.cluster[f], (uint16_t)ld.cluster[f], ls.offset[f], ld.offset[f], ls.width[f]};
-
-    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(P->n_tiles, n_sm));
-    launch(dim3((unsigned)grid), dim3(NTHREADS), plan->smem_bytes, st, *P, plan->table.data());
+    int64_t tiles = 0;
+    uint32_t sc = 0, dc = 0, fi = 0;
+    for (size_t k = 0; k < plan->comps.size(); ++k) {
+        const RemapPlan::Comp& K = plan->comps[k];
+        CompDesc& D = P->comp[k];
+        D.T = call_tile(*plan, (int)k, n, n_sm);
+        D.tile_bytes = D.T * K.R;
+        D.n_tiles = n / D.T;
+        D.tile_base = tiles;
+        tiles += D.n_tiles;
+        D.identity = K.identity ? 1 : 0;
+        D.instr_base = K.instr_base;
+        D.n_instr = K.n_instr;
+        D.sc_lo = (uint16_t)sc;
+        uint32_t off = 0;
+        for (int c : K.src_clusters) {
+            P->srcc[sc++] = {ck.bs[c], (uint32_t)ls.stride[c], off};
+            off += D.T * (uint32_t)ls.stride[c];
+        }
+        D.sc_hi = (uint16_t)sc;
+        D.dc_lo = (uint16_t)dc;
+        off = 0;
+        for (int c : K.dst_clusters) {
+            P->dstc[dc++] = {ck.bd[c], (uint32_t)ld.stride[c], off};
+            off += D.T * (uint32_t)ld.stride[c];
+        }
+        D.dc_hi = (uint16_t)dc;
+        D.f_lo = (uint16_t)fi;
+        fi += (uint32_t)K.fields.size();
+        D.f_hi = (uint16_t)fi;
+    }
+    P->total_tiles = tiles;
+    // a tail-only call still needs one CTA per component tail
+    const int64_t grid = std::max<int64_t>(std::min<int64_t>((int64_t)plan->comps.size(), n_sm),
+                                           std::min<int64_t>(tiles, n_sm));
+    launch(dim3((unsigned)std::max<int64_t>(grid, 1)), dim3(NTHREADS), plan->smem_bytes, st, *P, plan->table.data());
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "remap_tiled_kernel launch");
     return ADHA_OK;

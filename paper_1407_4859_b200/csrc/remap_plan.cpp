@@ -1,14 +1,15 @@
 // remap_plan.cpp -- compiles a (src layout, dst layout) pair into the tiled
-// kernel's plan: unit size, tile records T, pipeline
-// stages, chunk placement in shared memory and the per-lane permutation table.
+// kernel's plan: unit size, components, tile records T_k,
+// pipeline stages and the per-lane permutation table (remap_plan.h).
 //
-// Everything here is N-independent; adha_remap fills the N-dependent region
-// bases (adha.h "layout descriptor") into the kernel parameters per call.
+// Everything here is N-independent; adha_remap picks T_k for the call and fills
+// the N-dependent region bases (adha.h "layout descriptor") into the parameters.
 #include "remap_plan.h"
 
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <numeric>
 #include <string>
 
@@ -39,10 +40,59 @@ static bool augment(int u, const uint32_t cnt[32][32], int match_r[32], bool see
     return false;
 }
 
+namespace {
+struct Unit {
+    uint32_t in, out;   // local unit offsets inside period 0 of the src / dst chunk
+    uint8_t sc, dc;     // kernel cluster slots
+};
+
+// Order the 32*W units of one period into W instructions of 32 lanes.  g = 4: every
+// instruction is a perfect matching of src banks to dst banks.  Returns false if the
+// decomposition failed (then destination order is used).
+bool matched_order(const std::vector<Unit>& units, std::vector<uint32_t>& order) {
+    std::vector<uint32_t> bucket[32][32];
+    uint32_t cnt[32][32] = {};
+    for (uint32_t u = 0; u < units.size(); ++u) {
+        const int bi = units[u].in % 32, bo = units[u].out % 32;
+        bucket[bi][bo].push_back(u);
+        ++cnt[bi][bo];
+    }
+    while (order.size() < units.size()) {
+        int match_r[32];
+        std::fill(match_r, match_r + 32, -1);
+        for (int u = 0; u < 32; ++u) {
+            bool seen[32] = {};
+            if (!augment(u, cnt, match_r, seen)) return false;
+        }
+        int sigma[32];
+        for (int v = 0; v < 32; ++v) sigma[match_r[v]] = v;
+        uint32_t m = UINT32_MAX;
+        for (int u = 0; u < 32; ++u) m = std::min(m, cnt[u][sigma[u]]);
+        for (uint32_t rep = 0; rep < m; ++rep)
+            for (int u = 0; u < 32; ++u) {
+                order.push_back(bucket[u][sigma[u]].back());
+                bucket[u][sigma[u]].pop_back();
+            }
+        for (int u = 0; u < 32; ++u) cnt[u][sigma[u]] -= m;
+    }
+    return true;
+}
+}  // namespace
+
+uint32_t call_tile(const RemapPlan& p, int k, int64_t n, int n_sm) {
+    const uint32_t T = p.comps[k].T_max;
+    if (n_sm > 0 && n < (int64_t)T * n_sm) {
+        int64_t t = (n + n_sm - 1) / n_sm;
+        t = (t + 31) / 32 * 32;
+        return (uint32_t)std::max<int64_t>(32, std::min<int64_t>(t, T));
+    }
+    return T;
+}
+
 RemapPlan compile_plan(const Layout& ls, const Layout& ld) {
     RemapPlan P;
     const int F = ls.n_fields;
-    const uint64_t R = ls.record_bytes;
+    const int Cs = ls.n_clusters(), Cd = ld.n_clusters();
 
     // unit g: largest of 4, 2, 1 dividing every width and every offset in both layouts
     uint64_t gall = 0;
@@ -60,110 +110,144 @@ RemapPlan compile_plan(const Layout& ls, const Layout& ld) {
         return P;
     };
     if (F > MAXF) return naive("more than " + std::to_string(MAXF) + " fields");
-    if (ls.n_clusters() > MAXC || ld.n_clusters() > MAXC)
-        return naive("more than " + std::to_string(MAXC) + " clusters");
-    const uint64_t W = R / g;
+    if (Cs > MAXC || Cd > MAXC) return naive("more than " + std::to_string(MAXC) + " clusters");
+
+    // components: union-find over src clusters [0, Cs) and dst clusters [Cs, Cs + Cd)
+    std::vector<int> parent(Cs + Cd);
+    std::iota(parent.begin(), parent.end(), 0);
+    auto find = [&](int x) {
+        while (parent[x] != x) x = parent[x] = parent[parent[x]];
+        return x;
+    };
+    for (int f = 0; f < F; ++f) {
+        int a = find(ls.cluster[f]), b = find(Cs + ld.cluster[f]);
+        if (a != b) parent[std::max(a, b)] = std::min(a, b);
+    }
+    std::map<int, int> comp_of_root;   // ordered by root = min src cluster of the component
+    for (int c = 0; c < Cs; ++c) {
+        int r = find(c);
+        if (!comp_of_root.count(r)) {
+            int k = (int)comp_of_root.size();
+            comp_of_root[r] = k;
+            P.comps.emplace_back();
+        }
+        P.comps[comp_of_root[r]].src_clusters.push_back(c);
+    }
+    for (int c = 0; c < Cd; ++c) P.comps[comp_of_root.at(find(Cs + c))].dst_clusters.push_back(c);
+    for (int f = 0; f < F; ++f) {
+        auto& K = P.comps[comp_of_root.at(find(ls.cluster[f]))];
+        K.fields.push_back(f);
+        K.R += ls.width[f];
+    }
+    if ((int)P.comps.size() > MAXK) return naive("more than " + std::to_string(MAXK) + " components");
+
+    // kernel cluster numbering: clusters grouped by component
+    P.src_slot.assign(Cs, -1);
+    P.dst_slot.assign(Cd, -1);
+    for (auto& K : P.comps) {
+        for (int c : K.src_clusters) { P.src_slot[c] = (int)P.src_order.size(); P.src_order.push_back(c); }
+        for (int c : K.dst_clusters) { P.dst_slot[c] = (int)P.dst_order.size(); P.dst_order.push_back(c); }
+        K.identity = K.src_clusters.size() == 1 && K.dst_clusters.size() == 1 &&
+                     ls.members[K.src_clusters[0]] == ld.members[K.dst_clusters[0]];
+    }
+
+    // tile sizes and stages
+    const uint32_t budget = 232448 - HDR_BYTES - 128;   // sm_100 opt-in dynamic smem per block
+    const uint32_t target = env_u32("ADHA_STAGE_BYTES", 49152);
+    const uint32_t t_cap = env_u32("ADHA_TILE_CAP", 16384);
+    uint32_t s_in = std::min<uint32_t>(env_u32("ADHA_STAGES", 4), MAX_S_IN);
+    auto round128 = [](uint64_t x) { return (x + 127) / 128 * 128; };
+    uint64_t stage = 0;
+    for (auto& K : P.comps) {
+        uint64_t T = std::max<uint64_t>(32, (target / (32ull * K.R)) * 32);
+        T = std::min<uint64_t>(T, std::max<uint32_t>(32, t_cap / 32 * 32));
+        K.T_max = (uint32_t)T;
+        stage = std::max<uint64_t>(stage, round128(T * K.R));
+    }
+    while (s_in > 2 && (s_in + S_OUT) * stage > budget) --s_in;
+    if ((s_in + S_OUT) * stage > budget || stage > STAGE_MAX) {
+        // shrink the largest tiles until four buffers fit and a tile is at most STAGE_MAX bytes
+        const uint64_t cap = std::min<uint64_t>(budget / (s_in + S_OUT) / 128 * 128, STAGE_MAX);
+        stage = 0;
+        for (auto& K : P.comps) {
+            uint64_t T = (cap / K.R) / 32 * 32;
+            if (T < 32) return naive("a 32-record tile does not fit in shared memory");
+            K.T_max = (uint32_t)std::min<uint64_t>(K.T_max, T);
+            stage = std::max<uint64_t>(stage, round128((uint64_t)K.T_max * K.R));
+        }
+    }
+    P.s_in = s_in;
+    P.stage_bytes = (uint32_t)stage;
+    P.smem_bytes = HDR_BYTES + 128 + (s_in + S_OUT) * P.stage_bytes;
+
+    // instructions: 32 * W_k units per non-identity component
+    uint64_t total_w = 0, max_w = 0;
+    for (auto& K : P.comps) {
+        if (K.identity) continue;
+        total_w += K.R / g;
+        max_w = std::max<uint64_t>(max_w, K.R / g);
+    }
     int cls = -1;
     for (int c = 0; c < 4; ++c)
-        if (32 * W <= (uint64_t)CLASS_NENT[c] && W <= (uint64_t)NCONS * CLASS_EMAX[c]) { cls = c; break; }
-    if (cls < 0) return naive("record of " + std::to_string(W) + " units exceeds the instruction table");
+        if (32 * total_w <= (uint64_t)CLASS_NENT[c] && max_w <= (uint64_t)NCONS * CLASS_EMAX[c]) { cls = c; break; }
+    if (cls < 0) return naive("record of " + std::to_string(total_w) + " units exceeds the instruction table");
     P.table_class = cls;
-    P.n_instr = (uint32_t)W;
 
-    // tile size and stages
-    const uint32_t budget = 232448 - HDR_BYTES;  // sm_100 opt-in dynamic shared memory per block
-    const uint32_t target = env_u32("ADHA_STAGE_BYTES", 32768);
-    uint32_t s_in = std::min<uint32_t>(env_u32("ADHA_STAGES", 4), MAX_S_IN);
-    uint64_t T = std::max<uint64_t>(32, (target / (32 * R)) * 32);
-    while (T > 32 && T * W > 65536) T -= 32;                       // 16-bit unit offsets
-    auto stage_of = [&](uint64_t t) { return ((t * R) + 127) / 128 * 128; };
-    while (s_in > 2 && (s_in + S_OUT) * stage_of(T) > budget) --s_in;
-    while (T > 32 && (s_in + S_OUT) * stage_of(T) > budget) T -= 32;
-    if ((s_in + S_OUT) * stage_of(T) > budget || T * W > 65536)
-        return naive("a 32-record tile does not fit in shared memory");
-    P.T = (uint32_t)T;
-    P.s_in = s_in;
-    P.tile_bytes = (uint32_t)(T * R);
-    P.stage_bytes = (uint32_t)stage_of(T);
-    P.smem_bytes = HDR_BYTES + (s_in + S_OUT) * P.stage_bytes;
-
-    // chunk placement: clusters in canonical order, each T*stride bytes (a multiple of 32)
-    uint32_t off = 0;
-    for (int c = 0; c < ls.n_clusters(); ++c) { P.src_chunk.push_back(off); off += (uint32_t)(T * ls.stride[c]); }
-    off = 0;
-    for (int c = 0; c < ld.n_clusters(); ++c) { P.dst_chunk.push_back(off); off += (uint32_t)(T * ld.stride[c]); }
-
-    // the 32*W units of period 0
-    struct Unit { uint32_t in, out; uint8_t sc, dc; };
-    std::vector<Unit> units;
-    units.reserve(32 * W);
-    for (uint32_t r = 0; r < 32; ++r)
-        for (int f = 0; f < F; ++f) {
-            const int cs = ls.cluster[f], cd = ld.cluster[f];
-            for (uint32_t j = 0; j < ls.width[f] / g; ++j) {
-                uint64_t ib = P.src_chunk[cs] + r * ls.stride[cs] + ls.offset[f] + j * g;
-                uint64_t ob = P.dst_chunk[cd] + r * ld.stride[cd] + ld.offset[f] + j * g;
-                units.push_back({(uint32_t)(ib / g), (uint32_t)(ob / g), (uint8_t)cs, (uint8_t)cd});
-            }
-        }
-
-    std::vector<uint32_t> order;   // unit index per (instruction, lane)
-    order.reserve(units.size());
-    if (g == 4) {
-        // decompose the bank multigraph (src bank -> dst bank) into perfect matchings
-        std::vector<uint32_t> bucket[32][32];
-        uint32_t cnt[32][32] = {};
-        for (uint32_t u = 0; u < units.size(); ++u) {
-            int bi = units[u].in % 32, bo = units[u].out % 32;
-            bucket[bi][bo].push_back(u);
-            ++cnt[bi][bo];
-        }
-        bool ok = true;
-        while (order.size() < units.size()) {
-            int match_r[32];
-            std::fill(match_r, match_r + 32, -1);
-            for (int u = 0; u < 32 && ok; ++u) {
-                bool seen[32] = {};
-                if (!augment(u, cnt, match_r, seen)) ok = false;
-            }
-            if (!ok) break;
-            int sigma[32];
-            for (int v = 0; v < 32; ++v) sigma[match_r[v]] = v;
-            uint32_t m = UINT32_MAX;
-            for (int u = 0; u < 32; ++u) m = std::min(m, cnt[u][sigma[u]]);
-            for (uint32_t rep = 0; rep < m; ++rep)
-                for (int u = 0; u < 32; ++u) {
-                    order.push_back(bucket[u][sigma[u]].back());
-                    bucket[u][sigma[u]].pop_back();
+    P.matched = (g == 4);
+    uint32_t instr = 0;
+    for (auto& K : P.comps) {
+        K.instr_base = instr;
+        K.n_instr = 0;
+        if (K.identity) continue;
+        std::vector<Unit> units;
+        for (uint32_t r = 0; r < 32; ++r)
+            for (int f : K.fields) {
+                const int cs = ls.cluster[f], cd = ld.cluster[f];
+                for (uint32_t j = 0; j < ls.width[f] / g; ++j) {
+                    const uint64_t ib = r * ls.stride[cs] + ls.offset[f] + j * g;
+                    const uint64_t ob = r * ld.stride[cd] + ld.offset[f] + j * g;
+                    units.push_back({(uint32_t)(ib / g), (uint32_t)(ob / g), (uint8_t)P.src_slot[cs],
+                                     (uint8_t)P.dst_slot[cd]});
                 }
-            for (int u = 0; u < 32; ++u) cnt[u][sigma[u]] -= m;
+            }
+        std::vector<uint32_t> order;
+        if (g == 4 && !matched_order(units, order)) {
+            P.matched = false;
+            order.clear();
         }
-        P.matched = ok;
-        if (!ok) order.clear();
+        if (order.empty()) {
+            // destination order (by dst cluster, then unit): lanes write consecutive units
+            order.resize(units.size());
+            std::iota(order.begin(), order.end(), 0u);
+            std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
+                if (units[a].dc != units[b].dc) return units[a].dc < units[b].dc;
+                return units[a].out < units[b].out;
+            });
+        }
+        for (uint32_t idx : order) {
+            const Unit& u = units[idx];
+            P.ent_off.push_back(u.in | (u.out << 16));
+            P.ent_sc.push_back(u.sc);
+            P.ent_dc.push_back(u.dc);
+        }
+        K.n_instr = K.R / g;
+        instr += K.n_instr;
     }
-    if (order.empty()) {
-        // destination order: lanes write consecutive units
-        std::vector<uint32_t> idx(units.size());
-        std::iota(idx.begin(), idx.end(), 0u);
-        std::sort(idx.begin(), idx.end(), [&](uint32_t a, uint32_t b) { return units[a].out < units[b].out; });
-        order = idx;
-    }
-    P.ent_off.resize(order.size());
-    P.ent_sc.resize(order.size());
-    P.ent_dc.resize(order.size());
-    for (size_t k = 0; k < order.size(); ++k) {
-        const Unit& u = units[order[k]];
-        P.ent_off[k] = u.in | (u.out << 16);
-        P.ent_sc[k] = u.sc;
-        P.ent_dc[k] = u.dc;
-    }
-    // kernel-parameter image of EntryTable<NENT>: off[NENT] | sc[NENT] | dc[NENT]
+
+    // kernel-parameter image of EntryTable<NENT>: off[NENT] | sc[NENT] | dc[NENT] | fields[MAXF]
     const uint32_t nent = (uint32_t)CLASS_NENT[cls];
-    P.table.assign((nent * 6 + 3) / 4, 0u);
+    const size_t bytes = 6ull * nent + sizeof(FieldDesc) * MAXF;
+    P.table.assign((bytes + 3) / 4, 0u);
     uint8_t* img = reinterpret_cast<uint8_t*>(P.table.data());
     std::memcpy(img, P.ent_off.data(), P.ent_off.size() * 4);
     std::memcpy(img + 4 * nent, P.ent_sc.data(), P.ent_sc.size());
     std::memcpy(img + 5 * nent, P.ent_dc.data(), P.ent_dc.size());
+    FieldDesc* fd = reinterpret_cast<FieldDesc*>(img + 6 * nent);
+    int fi = 0;
+    for (auto& K : P.comps)
+        for (int f : K.fields)
+            fd[fi++] = {(uint16_t)P.src_slot[ls.cluster[f]], (uint16_t)P.dst_slot[ld.cluster[f]], ls.offset[f],
+                        ld.offset[f], ls.width[f]};
     P.tiled = true;
     return P;
 }
@@ -173,24 +257,36 @@ std::string describe_plan(const RemapPlan& p, const Layout& ls, const Layout& ld
     o += "\"tiled\":" + std::string(p.tiled ? "true" : "false");
     o += ",\"why_naive\":" + json::quote(p.why_naive);
     o += ",\"unit\":" + std::to_string(p.unit);
-    o += ",\"T\":" + std::to_string(p.T);
     o += ",\"s_in\":" + std::to_string(p.s_in);
     o += ",\"s_out\":" + std::to_string(dev::S_OUT);
     o += ",\"stage_bytes\":" + std::to_string(p.stage_bytes);
-    o += ",\"tile_bytes\":" + std::to_string(p.tile_bytes);
     o += ",\"smem_bytes\":" + std::to_string(p.smem_bytes);
-    o += ",\"n_instr\":" + std::to_string(p.n_instr);
     o += ",\"n_consumer_warps\":" + std::to_string(dev::NCONS);
     o += ",\"table_class\":" + std::to_string(p.table_class);
     o += ",\"table_entries\":" + std::to_string(dev::CLASS_NENT[p.table_class]);
     o += ",\"matched\":" + std::string(p.matched ? "true" : "false");
-    auto arr = [&](const char* name, const std::vector<uint32_t>& v) {
-        o += ",\"" + std::string(name) + "\":[";
-        for (size_t i = 0; i < v.size(); ++i) o += (i ? "," : "") + std::to_string(v[i]);
-        o += "]";
+    auto arr = [](const std::vector<uint32_t>& v) {
+        std::string s = "[";
+        for (size_t i = 0; i < v.size(); ++i) s += (i ? "," : "") + std::to_string(v[i]);
+        return s + "]";
     };
-    arr("src_chunk", p.src_chunk);
-    arr("dst_chunk", p.dst_chunk);
+    auto iarr = [](const std::vector<int>& v) {
+        std::string s = "[";
+        for (size_t i = 0; i < v.size(); ++i) s += (i ? "," : "") + std::to_string(v[i]);
+        return s + "]";
+    };
+    o += ",\"T\":" + std::to_string(p.comps.empty() ? 0 : p.comps[0].T_max);
+    o += ",\"components\":[";
+    for (size_t k = 0; k < p.comps.size(); ++k) {
+        const auto& K = p.comps[k];
+        o += (k ? ",{" : "{");
+        o += "\"src_clusters\":" + iarr(K.src_clusters) + ",\"dst_clusters\":" + iarr(K.dst_clusters) +
+             ",\"fields\":" + iarr(K.fields) + ",\"R\":" + std::to_string(K.R) + ",\"T\":" + std::to_string(K.T_max) +
+             ",\"identity\":" + (K.identity ? "true" : "false") + ",\"instr_base\":" + std::to_string(K.instr_base) +
+             ",\"n_instr\":" + std::to_string(K.n_instr) + "}";
+    }
+    o += "]";
+    o += ",\"src_order\":" + iarr(p.src_order) + ",\"dst_order\":" + iarr(p.dst_order);
     std::vector<uint32_t> sst, dst, ein, eout, esc, edc;
     for (auto s : ls.stride) sst.push_back((uint32_t)s);
     for (auto s : ld.stride) dst.push_back((uint32_t)s);
@@ -200,12 +296,8 @@ std::string describe_plan(const RemapPlan& p, const Layout& ls, const Layout& ld
         esc.push_back(p.ent_sc[k]);
         edc.push_back(p.ent_dc[k]);
     }
-    arr("src_stride", sst);
-    arr("dst_stride", dst);
-    arr("ent_in", ein);
-    arr("ent_out", eout);
-    arr("ent_sc", esc);
-    arr("ent_dc", edc);
+    o += ",\"src_stride\":" + arr(sst) + ",\"dst_stride\":" + arr(dst);
+    o += ",\"ent_in\":" + arr(ein) + ",\"ent_out\":" + arr(eout) + ",\"ent_sc\":" + arr(esc) + ",\"ent_dc\":" + arr(edc);
     o += "}";
     return o;
 }

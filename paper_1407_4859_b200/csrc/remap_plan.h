@@ -2,19 +2,29 @@
 // and the kernel-parameter structs it fills.
 //
 // Tiled kernel model:
-//   * a tile is T consecutive records (T a multiple of 32); for every src
-//     cluster c the tile's records form ONE contiguous chunk of T*stride(c)
-//     bytes in region c (element address), so a tile arrives in
-//     shared memory as n_src TMA bulk copies and leaves as n_dst bulk copies;
+//   * components: the fields split into the connected components of the
+//     bipartite graph "src cluster -- dst cluster sharing a field".  Each
+//     component is an independent remap of its own clusters (record i of a
+//     dst cluster depends only on record i of the src clusters of its
+//     component), so each gets its own tile size T_k = records per tile;
+//   * a tile of component k is T_k consecutive records (T_k a multiple of 32);
+//     for every src cluster c of k the tile's records form ONE contiguous chunk
+//     of T_k*stride(c) bytes in region c (element address): a tile
+//     arrives in shared memory as one TMA bulk copy per src cluster;
 //   * in shared memory the tile is permuted by "units" of g bytes (g = 4, 2 or
-//     1: the largest of those dividing every width and offset of both layouts);
-//   * a period is 32 records: every chunk advances by 32*stride bytes per
-//     period, a multiple of 128 bytes, so the 4-byte bank of every unit
-//     repeats from period to period;  the 32*W units of one period
-//     (W = R/g) are split into W warp instructions of 32 lanes.  For g = 4 the
-//     split is a decomposition of the 32x32 bank multigraph into perfect
-//     matchings (every instruction reads 32 distinct banks and writes 32
-//     distinct banks: conflict-free LDS and STS by construction).
+//     1: the largest of those dividing every width and offset of both layouts)
+//     into an output buffer holding one contiguous chunk per dst cluster, which
+//     the consumer warps write back with coalesced 16-byte stores;
+//   * a period is 32 records: a chunk advances by 32*stride bytes per period,
+//     and chunk starts are multiples of 32*stride, so with g = 4 the 4-byte
+//     bank of a unit depends only on its offset inside period 0 of its chunk.
+//     The 32*W_k units of one period (W_k = R_k/g) are split into W_k warp
+//     instructions of 32 lanes: for g = 4 by decomposing the 32x32 bank
+//     multigraph into perfect matchings, so every instruction reads 32
+//     distinct banks and writes 32 distinct banks (conflict-free LDS and STS by
+//     construction, independent of T_k);
+//   * identity components (one src cluster == one dst cluster, same fields)
+//     skip the permutation: the staged chunk is written straight back.
 #pragma once
 
 #include <cstdint>
@@ -28,51 +38,62 @@ constexpr int NCONS = 8;                       // consumer warps per CTA
 constexpr int NTHREADS = (NCONS + 1) * 32;     // + one TMA producer warp
 constexpr int MAXC = 128;                      // clusters per side (tiled kernel)
 constexpr int MAXF = 256;                      // fields (tiled kernel tail table, naive chunk)
+constexpr int MAXK = 64;                       // components
 constexpr int S_OUT = 2;                       // output staging buffers
 constexpr int HDR_BYTES = 1024;                // barrier header at the start of dynamic smem
 constexpr int MAX_S_IN = 8;
+constexpr uint32_t STAGE_MAX = 14 * 16 * NCONS * 32;   // copy-out covers 14 16-byte vectors per thread
 
 struct ClusterDesc {
     uint64_t region;    // region base in the buffer for this N (bytes)
     uint32_t stride;    // bytes per cluster record
-    uint32_t smem;      // chunk offset inside a staged tile (bytes)
+    uint32_t smem;      // chunk offset inside its component's staged tile (bytes), for this call's T
 };
 
 struct FieldDesc {
-    uint16_t sc, dc;    // src / dst cluster
+    uint16_t sc, dc;      // src / dst cluster (indices into srcc / dstc)
     uint32_t soff, doff;  // byte offset in the src / dst cluster record
     uint32_t width;
+};
+
+struct CompDesc {
+    int64_t tile_base;    // first global tile index of the component
+    int64_t n_tiles;      // floor(N / T)
+    uint32_t T;           // records per tile (multiple of 32)
+    uint32_t tile_bytes;  // T * R_k: TMA transaction bytes per tile
+    uint16_t sc_lo, sc_hi, dc_lo, dc_hi;   // cluster ranges (clusters are numbered by component)
+    uint16_t f_lo, f_hi;                   // field range in the field table
+    uint16_t identity, pad;
+    uint32_t instr_base;  // first instruction of the component in the entry table
+    uint32_t n_instr;     // W_k = R_k / g
 };
 
 struct TiledParams {
     const uint8_t* src;
     uint8_t* dst;
     int64_t n_records;
-    int64_t n_tiles;      // full tiles: floor(N / T)
-    int64_t tail_lo;      // n_tiles * T
-    uint32_t T;
-    uint32_t periods;     // T / 32
-    uint32_t tile_bytes;  // T * R: TMA transaction bytes per tile
-    uint32_t stage_bytes; // tile_bytes rounded up to 128
-    uint32_t n_src, n_dst, n_fields;
+    int64_t total_tiles;  // sum of the components' n_tiles
+    uint32_t stage_bytes; // bytes per staging buffer (max tile bytes, rounded to 128)
     uint32_t s_in;        // input pipeline stages
-    uint32_t n_instr;     // W = R / g instructions per period
+    uint32_t n_comp;
     uint32_t unit;        // g
+    CompDesc comp[MAXK];
     ClusterDesc srcc[MAXC];
     ClusterDesc dstc[MAXC];
-    FieldDesc fields[MAXF];
 };
 
-// per-(instruction, lane) table: entry i*32+lane of instruction i
+// per-(instruction, lane) table: entry i*32+lane of instruction i (instructions of all
+// components concatenated); offsets are units inside period 0 of the unit's chunk
 template <int NENT>
 struct EntryTable {
-    uint32_t off[NENT];   // src unit offset (low 16 bits) | dst unit offset (high 16 bits), period 0
-    uint8_t sc[NENT];     // src cluster of the unit (its period stride is 32*stride)
+    uint32_t off[NENT];   // src local unit offset (low 16 bits) | dst local unit offset (high 16 bits)
+    uint8_t sc[NENT];     // src cluster of the unit
     uint8_t dc[NENT];     // dst cluster of the unit
+    FieldDesc fields[MAXF];   // tail table, fields grouped by component
 };
 
-// Table size classes (entries per warp EMAX = instructions per warp).
-constexpr int CLASS_NENT[4] = {512, 1024, 2048, 3584};
+// Table size classes (entries per warp EMAX = instructions per warp per component).
+constexpr int CLASS_NENT[4] = {512, 1024, 2048, 3552};
 constexpr int CLASS_EMAX[4] = {2, 4, 8, 14};
 
 struct NaiveField {
@@ -90,23 +111,34 @@ struct NaiveParams {
 
 }  // namespace dev
 
-// Host-side compiled plan (N-independent; region bases are filled per call).
+// Host-side compiled plan (N-independent; T per call, region bases per call).
 struct RemapPlan {
+    struct Comp {
+        std::vector<int> src_clusters, dst_clusters, fields;   // original (canonical) indices
+        uint32_t R = 0;               // bytes per record of the component
+        uint32_t T_max = 0;           // records per tile at full size
+        bool identity = false;
+        uint32_t instr_base = 0, n_instr = 0;
+    };
     bool tiled = false;
-    std::string why_naive;        // reason when not tiled
-    uint32_t unit = 1;            // g
-    uint32_t T = 0, s_in = 0, stage_bytes = 0, tile_bytes = 0, n_instr = 0;
+    std::string why_naive;            // reason when not tiled
+    uint32_t unit = 1;                // g
+    uint32_t s_in = 0, stage_bytes = 0;
     uint32_t smem_bytes = 0;
     int table_class = 0;
-    bool matched = false;         // conflict-free matching used (g = 4)
-    std::vector<uint32_t> src_chunk, dst_chunk;     // per cluster chunk offsets in a staged tile
-    std::vector<uint32_t> ent_off;                  // 32 * n_instr entries
-    std::vector<uint8_t> ent_sc, ent_dc;
-    std::vector<uint32_t> table;                    // EntryTable<CLASS_NENT[table_class]> image
+    bool matched = false;             // conflict-free matching used (g = 4)
+    std::vector<Comp> comps;
+    std::vector<int> src_order, dst_order;   // kernel cluster index -> canonical cluster
+    std::vector<int> src_slot, dst_slot;     // canonical cluster -> kernel cluster index
+    std::vector<uint32_t> ent_off;           // 32 * sum(W_k) entries (local offsets)
+    std::vector<uint8_t> ent_sc, ent_dc;     // kernel cluster indices
+    std::vector<uint32_t> table;             // EntryTable<CLASS_NENT[table_class]> image (fields filled)
 };
 
 struct Layout;
 RemapPlan compile_plan(const Layout& ls, const Layout& ld);
 std::string describe_plan(const RemapPlan& p, const Layout& ls, const Layout& ld);
+// records per tile of component k for an N-record call on n_sm SMs
+uint32_t call_tile(const RemapPlan& p, int k, int64_t n, int n_sm);
 
 }  // namespace adha

@@ -216,43 +216,58 @@ def test_cpp_planner_equals_oracle_random():
 # ---------------------------------------------------------------- remap-plan compiler (host)
 
 def _plan_checks(widths, ls, ld):
+    from tests.test_oracle_remap import clusters_in_order
     Ls, Ld = A.Layout(widths, ls), A.Layout(widths, ld)
     d = A.plan_describe(Ls, Ld)
     assert d["tiled"], d["why_naive"]
     g = d["unit"]
-    W = sum(widths) // g
-    assert d["n_instr"] == W and d["T"] % 32 == 0
+    cs, cd = clusters_in_order(ls), clusters_in_order(ld)          # canonical clusters (field lists)
+    csrc = {f: k for k, c in enumerate(cs) for f in c}
+    cdst = {f: k for k, c in enumerate(cd) for f in c}
+    comps = d["components"]
+    # components partition the fields and are closed under "shares a src or dst cluster"
+    allf = sorted(f for K in comps for f in K["fields"])
+    assert allf == list(range(len(widths)))
+    for K in comps:
+        fs = set(K["fields"])
+        assert sorted(K["src_clusters"]) == sorted({csrc[f] for f in fs})
+        assert sorted(K["dst_clusters"]) == sorted({cdst[f] for f in fs})
+        for c in K["src_clusters"]:
+            assert set(cs[c]) <= fs
+        for c in K["dst_clusters"]:
+            assert set(cd[c]) <= fs
+        assert K["R"] == sum(widths[f] for f in fs) and K["T"] % 32 == 0
+        assert K["identity"] == (len(K["src_clusters"]) == 1 and len(K["dst_clusters"]) == 1
+                                 and cs[K["src_clusters"][0]] == cd[K["dst_clusters"][0]])
     ent_in, ent_out = np.array(d["ent_in"]), np.array(d["ent_out"])
-    assert ent_in.size == 32 * W
-    # chunks are packed in canonical cluster order, T*stride bytes each
-    from tests.test_oracle_remap import clusters_in_order
-    T = d["T"]
-    cs, cd = clusters_in_order(ls), clusters_in_order(ld)
-    def packed(cl):
-        offs, o = [], 0
-        for c in cl:
-            offs.append(o)
-            o += T * sum(widths[f] for f in c)
-        return offs
-    assert d["src_chunk"] == packed(cs) and d["dst_chunk"] == packed(cd)
-    # every unit of the 32-record period moved exactly once, to the place the oracle's
-    # record model gives (chunk + r*stride + offset + j*g)
-    _, ss, os_, _ = O.field_addresses(widths, ls, T)
-    _, sd, od, _ = O.field_addresses(widths, ld, T)
-    chunk_s = {f: d["src_chunk"][k] for k, c in enumerate(cs) for f in c}
-    chunk_d = {f: d["dst_chunk"][k] for k, c in enumerate(cd) for f in c}
-    exp = set()
-    for r in range(32):
-        for f, w in enumerate(widths):
-            for j in range(0, w, g):
-                exp.add((int(chunk_s[f] + r * ss[f] + os_[f] + j) // g, int(chunk_d[f] + r * sd[f] + od[f] + j) // g))
-    got = set(zip(ent_in.tolist(), ent_out.tolist()))
-    assert got == exp and len(got) == ent_in.size
-    if g == 4:
-        assert d["matched"]
-        for i in range(W):                    # conflict-free: 32 distinct banks on both sides
-            assert len(set((ent_in[32 * i: 32 * i + 32] % 32).tolist())) == 32
-            assert len(set((ent_out[32 * i: 32 * i + 32] % 32).tolist())) == 32
+    ent_sc, ent_dc = np.array(d["ent_sc"]), np.array(d["ent_dc"])
+    _, ss, os_, _ = O.field_addresses(widths, ls, 32)
+    _, sd, od, _ = O.field_addresses(widths, ld, 32)
+    total = 0
+    for K in comps:
+        if K["identity"]:
+            assert K["n_instr"] == 0
+            continue
+        W = K["R"] // g
+        assert K["n_instr"] == W
+        lo, hi = 32 * K["instr_base"], 32 * (K["instr_base"] + W)
+        total += hi - lo
+        # every unit of the component's 32-record period moved exactly once, to the place the
+        # oracle's record model gives (r*stride + offset + j, inside the unit's chunk)
+        exp = set()
+        for r in range(32):
+            for f in K["fields"]:
+                for j in range(0, widths[f], g):
+                    exp.add((int(r * ss[f] + os_[f] + j) // g, int(r * sd[f] + od[f] + j) // g, csrc[f], cdst[f]))
+        got = {(int(a), int(b), d["src_order"][c], d["dst_order"][e])
+               for a, b, c, e in zip(ent_in[lo:hi], ent_out[lo:hi], ent_sc[lo:hi], ent_dc[lo:hi])}
+        assert got == exp and len(got) == hi - lo
+        if g == 4:
+            assert d["matched"]
+            for i in range(lo, hi, 32):           # conflict-free: 32 distinct banks on both sides
+                assert len(set((ent_in[i: i + 32] % 32).tolist())) == 32
+                assert len(set((ent_out[i: i + 32] % 32).tolist())) == 32
+    assert total == ent_in.size
     return d
 
 
