@@ -248,6 +248,7 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
 
     import paper_1407_4859_b200 as A
+    from paper_1407_4859_b200.sharding import shard_for, max_over_ranks, aggregate_gbs
     from adha_inputs import fill_random_device, SEED_BASE
 
     name = args.config
@@ -255,8 +256,7 @@ def main():
     widths, chain = chain_for(kind)
     R = sum(widths)
     # shard by contiguous record range: weak -> world * n_cfg records in total, strong -> n_cfg in total
-    n_total = n_cfg * world if scaling == "weak" else n_cfg
-    lo, hi = A.shard_range(n_total, world, rank)
+    n_total, lo, hi = shard_for(n_cfg, world, rank, scaling)
     n = hi - lo
     layouts = [A.Layout(widths, lab) for lab in chain]
     bufs = [torch.empty(max(l.nbytes(n), 1), dtype=torch.uint8, device=dev) for l in layouts]
@@ -305,12 +305,8 @@ def main():
     clk = clocks.stop()
     ms_total = t0.elapsed_time(t1)
     launch_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
-    total_bytes = 2 * n_total * R * n_remaps * args.steps
-    value = total_bytes / (ms_max * 1e-3) / 1e9
+    ms_max = max_over_ranks(ms_total, dev)
+    value = aggregate_gbs(n_total, R, n_remaps, args.steps, ms_max)
 
     # same-run torch copy_ of the same traffic (N*R bytes read + N*R written): the box's copy ceiling now
     copy_gbs = None
@@ -364,11 +360,8 @@ def main():
         e1.record(stream)
         torch.cuda.synchronize(dev)
         barrier()
-        et = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(et, op=dist.ReduceOp.MAX)
-        e_ms = float(et.item())
-        e2e = {"value": 2 * n_total * R * n_remaps * e2e_steps / (e_ms * 1e-3) / 1e9, "unit": "GB/s",
+        e_ms = max_over_ranks(e0.elapsed_time(e1), dev)
+        e2e = {"value": aggregate_gbs(n_total, R, n_remaps, e2e_steps, e_ms), "unit": "GB/s",
                "h2d_bytes_per_step": n * R, "d2h_bytes_per_step": n * R,
                "api": "adha_remap_host" if n_remaps == 1 else "H2D copy + adha_remap x%d + D2H copy" % n_remaps,
                "ms_per_step": e_ms / e2e_steps}

@@ -164,6 +164,22 @@ ADHA_API adha_status adha_remap(const void* src, const adha_layout* src_layout,
                        void* dst, const adha_layout* dst_layout,
                        int64_t n_records, void* stream);
 
+/* The remap between layout instances given REGION BY REGION (SURVEY.md 8(f) N1,
+ * "moved subset"): src_regions[c] is the device address of src cluster c's region
+ * (canonical cluster order, n_records * stride(c) bytes), dst_regions[c] likewise.
+ * Regions need not be parts of one buffer.  A dst region that is the very same
+ * memory as the src region of an IDENTICAL cluster (same fields in the same
+ * order) is left untouched: its records are already in place, so only the fields
+ * whose cluster changes move -- the paper's remap cost "based on the number of
+ * common fields" (Medical AoSV -> SoA moves
+ * only {V1,V2,V3}).  Every region must be 256-byte aligned; dst regions must not
+ * overlap each other or any src region except by that exact aliasing.
+ * Asynchronous on `stream` like adha_remap.
+ * Errors: INVALID_ARG, LAYOUT_MISMATCH, ALIGNMENT, OVERLAP, TOO_LARGE, CUDA. */
+ADHA_API adha_status adha_remap_regions(const void* const* src_regions, const adha_layout* src_layout,
+                                        void* const* dst_regions, const adha_layout* dst_layout,
+                                        int64_t n_records, void* stream);
+
 /* A chain of remaps on one stream (a PDL plan with several remap edges,
  * PAPER.md:146): buffers[k] holds the records in layouts[k];
  * for k = 0..n_layouts-2: remap buffers[k] (layouts[k]) -> buffers[k+1]

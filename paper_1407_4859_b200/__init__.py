@@ -50,6 +50,7 @@ _SIGS = {
                                                  ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_uint32)]),
     "adha_layout_destroy": (None, [_L]),
     "adha_remap": (ctypes.c_int, [_vp, _L, _vp, _L, _i64, _vp]),
+    "adha_remap_regions": (ctypes.c_int, [ctypes.POINTER(_vp), _L, ctypes.POINTER(_vp), _L, _i64, _vp]),
     "adha_remap_chain": (ctypes.c_int, [ctypes.POINTER(_vp), ctypes.POINTER(_L), _i32, _i64, _vp]),
     "adha_shard_range": (ctypes.c_int, [_i64, _i32, _i32, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
     "adha_remap_sharded": (ctypes.c_int, [ctypes.POINTER(_vp), _L, ctypes.POINTER(_vp), _L, _i64, _i32,
@@ -231,6 +232,17 @@ def remap(src, src_layout: Layout, dst, dst_layout: Layout, n_records: int, stre
     _check(_lib.adha_remap(_ptr(src), src_layout.handle, _ptr(dst), dst_layout.handle, n, _stream(stream)))
 
 
+def remap_regions(src_regions: Sequence, src_layout: Layout, dst_regions: Sequence, dst_layout: Layout,
+                  n_records: int, stream=None) -> None:
+    """Remap between per-cluster regions (adha_remap_regions): a dst region that aliases the src
+    region of an identical cluster is left in place, so only the changed fields move."""
+    s = (_vp * len(src_regions))(*[_ptr(x) for x in src_regions])
+    d = (_vp * len(dst_regions))(*[_ptr(x) for x in dst_regions])
+    if len(src_regions) != src_layout.n_clusters or len(dst_regions) != dst_layout.n_clusters:
+        raise ValueError("one region per cluster")
+    _check(_lib.adha_remap_regions(s, src_layout.handle, d, dst_layout.handle, int(n_records), _stream(stream)))
+
+
 def remap_chain(buffers: Sequence, layouts: Sequence[Layout], n_records: int, stream=None) -> None:
     """buffers[k] (layouts[k]) -> buffers[k+1] (layouts[k+1]) for each k, one stream (adha_remap_chain)."""
     if len(buffers) != len(layouts):
@@ -303,5 +315,5 @@ def plan_pdl(program, arch, profile=None) -> dict:
     return json.loads(_take_string(p))
 
 
-__all__ = ["Layout", "AdhaError", "remap", "remap_chain", "shard_range", "remap_sharded", "remap_host",
+__all__ = ["Layout", "AdhaError", "remap", "remap_regions", "remap_chain", "shard_range", "remap_sharded", "remap_host",
            "plan_describe", "plan_ods", "plan_pdl", "version", "LIB_PATH"]

@@ -1,6 +1,8 @@
 """Build libadha.so in-tree: nvcc for sm_100a, static cudart, -lineinfo.
 
-    python -m paper_1407_4859_b200.build [--force]
+    python paper_1407_4859_b200/build.py [--force] [-v]
+
+(Run as a script: importing the package first would need the library it builds.)
 """
 from __future__ import annotations
 

@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             const uint32_t ib = in0 + stage * p.stage_bytes;
             for (uint32_t c = p.comp[k].sc_lo + lane; c < p.comp[k].sc_hi; c += 32) {
                 const uint32_t bytes = T * p.srcc[c].stride;
-                bulk_load(ib + p.srcc[c].smem, p.src + p.srcc[c].region + (uint64_t)lt * bytes, bytes,
+                bulk_load(ib + p.srcc[c].smem, (const void*)(p.src + p.srcc[c].region + (uint64_t)lt * bytes), bytes,
                           full0 + 8 * stage);
             }
             if (++stage == p.s_in) { stage = 0; phase ^= 1; }
@@ -166,12 +166,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         mbar_wait(full0 + 8 * stage, phase);
         const uint32_t ib = in0 + stage * p.stage_bytes;
         if (p.comp[k].identity) {
-            copy_out(p.dst, ib, tid, lt, nv, gofs, gstep);
+            copy_out((uint8_t*)p.dst, ib, tid, lt, nv, gofs, gstep);
             __syncwarp();
             if (lane == 0) mbar_arrive(empty0 + 8 * stage);
         } else {
             const uint32_t ob = out0 + oslot * p.stage_bytes;
             const uint32_t periods = T / 32;
+            if (p.s_out == 1) named_bar_sync(1, NCONS * 32);   // previous copy-out done with the buffer
 #pragma unroll
             for (int e = 0; e < EMAX; ++e) {
                 if ((uint32_t)e < ne) {
@@ -194,8 +195,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(empty0 + 8 * stage);    // input stage free for the producer
             named_bar_sync(1, NCONS * 32);                      // output tile complete
-            copy_out(p.dst, ob, tid, lt, nv, gofs, gstep);
-            oslot ^= 1;
+            copy_out((uint8_t*)p.dst, ob, tid, lt, nv, gofs, gstep);
+            if (p.s_out == 2) oslot ^= 1;
         }
         if (++stage == p.s_in) { stage = 0; phase ^= 1; }
     }
@@ -204,6 +205,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     for (uint32_t kk = 0; kk < p.n_comp; ++kk) {
         if (gridDim.x - 1 - (kk % gridDim.x) != blockIdx.x) continue;
         const CompDesc& K = p.comp[kk];
+        if (K.skip) continue;
         const int64_t lo = K.n_tiles * (int64_t)K.T;
         const int64_t n_tail = p.n_records - lo;
         if (n_tail <= 0) continue;
@@ -212,8 +214,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             const uint32_t f = K.f_lo + (uint32_t)(x / n_tail);
             const int64_t r = lo + (x % n_tail);
             const FieldDesc fd = et.fields[f];
-            const uint8_t* s = p.src + p.srcc[fd.sc].region + (uint64_t)r * p.srcc[fd.sc].stride + fd.soff;
-            uint8_t* d = p.dst + p.dstc[fd.dc].region + (uint64_t)r * p.dstc[fd.dc].stride + fd.doff;
+            const uint8_t* s = (const uint8_t*)(p.src + p.srcc[fd.sc].region + (uint64_t)r * p.srcc[fd.sc].stride + fd.soff);
+            uint8_t* d = (uint8_t*)(p.dst + p.dstc[fd.dc].region + (uint64_t)r * p.dstc[fd.dc].stride + fd.doff);
             for (uint32_t j = 0; j < fd.width; j += sizeof(U))
                 *reinterpret_cast<U*>(d + j) = *reinterpret_cast<const U*>(s + j);
         }
@@ -227,8 +229,8 @@ __global__ void remap_naive_kernel(const __grid_constant__ NaiveParams p) {
         const uint32_t f = (uint32_t)(k / n);
         const int64_t r = p.lo + (k - (int64_t)f * n);
         const NaiveField& fd = p.f[f];
-        const uint8_t* s = p.src + fd.sbase + (uint64_t)r * fd.sstride + fd.soff;
-        uint8_t* d = p.dst + fd.dbase + (uint64_t)r * fd.dstride + fd.doff;
+        const uint8_t* s = (const uint8_t*)(p.src + fd.sbase + (uint64_t)r * fd.sstride + fd.soff);
+        uint8_t* d = (uint8_t*)(p.dst + fd.dbase + (uint64_t)r * fd.dstride + fd.doff);
         const uintptr_t a = (uintptr_t)s | (uintptr_t)d | fd.width;
         uint32_t j = 0;
         if ((a & 3) == 0) {
@@ -343,8 +345,8 @@ adha_status launch_naive(const uint8_t* src, const Layout& ls, const std::vector
     auto P = std::make_unique<NaiveParams>();
     for (int f0 = 0; f0 < ls.n_fields; f0 += MAXF) {
         std::memset(P.get(), 0, sizeof(NaiveParams));
-        P->src = src;
-        P->dst = dst;
+        P->src = (uint64_t)(uintptr_t)src;
+        P->dst = (uint64_t)(uintptr_t)dst;
         P->n_records = hi - lo;
         P->lo = lo;
         const int nf = std::min(MAXF, ls.n_fields - f0);
@@ -404,11 +406,12 @@ adha_status remap_checked(const uint8_t* src, const Layout& ls, uint8_t* dst, co
 
     auto P = std::make_unique<TiledParams>();
     std::memset(P.get(), 0, sizeof(TiledParams));
-    P->src = src;
-    P->dst = dst;
+    P->src = (uint64_t)(uintptr_t)src;
+    P->dst = (uint64_t)(uintptr_t)dst;
     P->n_records = n;
     P->stage_bytes = plan->stage_bytes;
     P->s_in = plan->s_in;
+    P->s_out = plan->s_out;
     P->n_comp = (uint32_t)plan->comps.size();
     P->unit = plan->unit;
     int64_t tiles = 0;
@@ -418,7 +421,9 @@ adha_status remap_checked(const uint8_t* src, const Layout& ls, uint8_t* dst, co
         CompDesc& D = P->comp[k];
         D.T = call_tile(*plan, (int)k, n, n_sm);
         D.tile_bytes = D.T * K.R;
-        D.n_tiles = n / D.T;
+        // an identity component whose dst region is its src region moves nothing (NEXT N1)
+        D.skip = K.identity && P->src + ck.bs[K.src_clusters[0]] == P->dst + ck.bd[K.dst_clusters[0]];
+        D.n_tiles = D.skip ? 0 : n / D.T;
         D.tile_base = tiles;
         tiles += D.n_tiles;
         D.identity = K.identity ? 1 : 0;
@@ -464,6 +469,54 @@ extern "C" adha_status adha_remap(const void* src, const adha_layout* hs, void* 
     adha_status s = validate(src, hs, dst, hd, n, &ck, true);
     if (s != ADHA_OK) return s;
     return remap_checked((const uint8_t*)src, hs->L, (uint8_t*)dst, hd->L, n, ck, (cudaStream_t)stream);
+}
+
+extern "C" adha_status adha_remap_regions(const void* const* src_regions, const adha_layout* hs,
+                                          void* const* dst_regions, const adha_layout* hd, int64_t n,
+                                          void* stream) {
+    clear_error();
+    Checked ck;
+    // layout checks (buffer checks are per region below)
+    adha_status s = validate(nullptr, hs, nullptr, hd, 0, &ck, false);
+    if (s != ADHA_OK) return s;
+    if (n < 0) return fail(ADHA_ERR_INVALID_ARG, "n_records < 0");
+    if (n == 0) return ADHA_OK;
+    if (!src_regions || !dst_regions) return fail(ADHA_ERR_INVALID_ARG, "null region array");
+    const Layout& ls = hs->L;
+    const Layout& ld = hd->L;
+    std::vector<uint64_t> tmp;
+    if (!ls.region_bases(n, tmp, nullptr) || !ld.region_bases(n, tmp, nullptr))
+        return fail(ADHA_ERR_TOO_LARGE, "N * record bytes overflows");
+    struct Span { uint64_t lo, hi; int side, c; };
+    std::vector<Span> spans;
+    ck.bs.assign(ls.n_clusters(), 0);
+    ck.bd.assign(ld.n_clusters(), 0);
+    for (int c = 0; c < ls.n_clusters(); ++c) {
+        const uint64_t a = (uint64_t)(uintptr_t)src_regions[c];
+        if (!a) return fail(ADHA_ERR_INVALID_ARG, "null src region " + std::to_string(c));
+        if (a & 255) return fail(ADHA_ERR_ALIGNMENT, "src region " + std::to_string(c) + " not 256-byte aligned");
+        ck.bs[c] = a;
+        spans.push_back({a, a + (uint64_t)n * ls.stride[c], 0, c});
+    }
+    for (int c = 0; c < ld.n_clusters(); ++c) {
+        const uint64_t a = (uint64_t)(uintptr_t)dst_regions[c];
+        if (!a) return fail(ADHA_ERR_INVALID_ARG, "null dst region " + std::to_string(c));
+        if (a & 255) return fail(ADHA_ERR_ALIGNMENT, "dst region " + std::to_string(c) + " not 256-byte aligned");
+        ck.bd[c] = a;
+        spans.push_back({a, a + (uint64_t)n * ld.stride[c], 1, c});
+    }
+    for (size_t i = 0; i < spans.size(); ++i)
+        for (size_t j = i + 1; j < spans.size(); ++j) {
+            const Span& x = spans[i];
+            const Span& y = spans[j];
+            if (!(x.lo < y.hi && y.lo < x.hi)) continue;
+            if (x.side == 0 && y.side == 0) continue;                  // src regions may share memory
+            // a dst region may BE the src region of an identical cluster: nothing moves there
+            const bool alias = x.side != y.side && x.lo == y.lo &&
+                               ls.members[x.side == 0 ? x.c : y.c] == ld.members[x.side == 0 ? y.c : x.c];
+            if (!alias) return fail(ADHA_ERR_OVERLAP, "regions overlap (only identical clusters may alias)");
+        }
+    return remap_checked(nullptr, ls, nullptr, ld, n, ck, (cudaStream_t)stream);
 }
 
 extern "C" adha_status adha_remap_chain(void* const* buffers, const adha_layout* const* layouts, int32_t n_layouts,

@@ -156,6 +156,7 @@ RemapPlan compile_plan(const Layout& ls, const Layout& ld) {
     const uint32_t target = env_u32("ADHA_STAGE_BYTES", 49152);
     const uint32_t t_cap = env_u32("ADHA_TILE_CAP", 16384);
     uint32_t s_in = std::min<uint32_t>(env_u32("ADHA_STAGES", 4), MAX_S_IN);
+    const uint32_t S_OUT = std::min<uint32_t>(std::max<uint32_t>(env_u32("ADHA_OUT_BUFFERS", 2), 1), S_OUT_MAX);
     auto round128 = [](uint64_t x) { return (x + 127) / 128 * 128; };
     uint64_t stage = 0;
     for (auto& K : P.comps) {
@@ -177,6 +178,7 @@ RemapPlan compile_plan(const Layout& ls, const Layout& ld) {
         }
     }
     P.s_in = s_in;
+    P.s_out = S_OUT;
     P.stage_bytes = (uint32_t)stage;
     P.smem_bytes = HDR_BYTES + 128 + (s_in + S_OUT) * P.stage_bytes;
 
@@ -258,7 +260,7 @@ std::string describe_plan(const RemapPlan& p, const Layout& ls, const Layout& ld
     o += ",\"why_naive\":" + json::quote(p.why_naive);
     o += ",\"unit\":" + std::to_string(p.unit);
     o += ",\"s_in\":" + std::to_string(p.s_in);
-    o += ",\"s_out\":" + std::to_string(dev::S_OUT);
+    o += ",\"s_out\":" + std::to_string(p.s_out);
     o += ",\"stage_bytes\":" + std::to_string(p.stage_bytes);
     o += ",\"smem_bytes\":" + std::to_string(p.smem_bytes);
     o += ",\"n_consumer_warps\":" + std::to_string(dev::NCONS);

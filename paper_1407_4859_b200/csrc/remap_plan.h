@@ -39,7 +39,7 @@ constexpr int NTHREADS = (NCONS + 1) * 32;     // + one TMA producer warp
 constexpr int MAXC = 128;                      // clusters per side (tiled kernel)
 constexpr int MAXF = 256;                      // fields (tiled kernel tail table, naive chunk)
 constexpr int MAXK = 64;                       // components
-constexpr int S_OUT = 2;                       // output staging buffers
+constexpr int S_OUT_MAX = 2;                   // output staging buffers (1 or 2)
 constexpr int HDR_BYTES = 1024;                // barrier header at the start of dynamic smem
 constexpr int MAX_S_IN = 8;
 constexpr uint32_t STAGE_MAX = 14 * 16 * NCONS * 32;   // copy-out covers 14 16-byte vectors per thread
@@ -63,18 +63,20 @@ struct CompDesc {
     uint32_t tile_bytes;  // T * R_k: TMA transaction bytes per tile
     uint16_t sc_lo, sc_hi, dc_lo, dc_hi;   // cluster ranges (clusters are numbered by component)
     uint16_t f_lo, f_hi;                   // field range in the field table
-    uint16_t identity, pad;
+    uint16_t identity;
+    uint16_t skip;        // 1: identity component whose dst region IS its src region (nothing moves)
     uint32_t instr_base;  // first instruction of the component in the entry table
     uint32_t n_instr;     // W_k = R_k / g
 };
 
 struct TiledParams {
-    const uint8_t* src;
-    uint8_t* dst;
+    uint64_t src;         // base address: src region c starts at src + srcc[c].region
+    uint64_t dst;         // base address: dst region c starts at dst + dstc[c].region
     int64_t n_records;
     int64_t total_tiles;  // sum of the components' n_tiles
     uint32_t stage_bytes; // bytes per staging buffer (max tile bytes, rounded to 128)
     uint32_t s_in;        // input pipeline stages
+    uint32_t s_out;       // output buffers: 2 = double-buffered, 1 = one buffer + a barrier before reuse
     uint32_t n_comp;
     uint32_t unit;        // g
     CompDesc comp[MAXK];
@@ -101,8 +103,8 @@ struct NaiveField {
     uint32_t sstride, dstride, soff, doff, width, pad;
 };
 struct NaiveParams {
-    const uint8_t* src;
-    uint8_t* dst;
+    uint64_t src;
+    uint64_t dst;
     int64_t n_records;
     int64_t lo;           // first record
     uint32_t n_fields;
@@ -123,7 +125,7 @@ struct RemapPlan {
     bool tiled = false;
     std::string why_naive;            // reason when not tiled
     uint32_t unit = 1;                // g
-    uint32_t s_in = 0, stage_bytes = 0;
+    uint32_t s_in = 0, s_out = 2, stage_bytes = 0;
     uint32_t smem_bytes = 0;
     int table_class = 0;
     bool matched = false;             // conflict-free matching used (g = 4)

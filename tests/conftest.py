@@ -11,6 +11,19 @@ if ROOT not in sys.path:
 GOLDEN = os.path.join(ROOT, "tests", "golden")
 
 
+def _ensure_built():
+    """Build libadha.so (and the C oracle) in-tree if missing or stale: the package itself
+    refuses to import without its library."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("adha_build", os.path.join(ROOT, "paper_1407_4859_b200", "build.py"))
+    B = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(B)
+    B.build()
+
+
+_ensure_built()
+
+
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA B200 (sm_100a); parity tests through the C-ABI")
     config.addinivalue_line("markers", "slow: long-running CPU test")

@@ -256,3 +256,32 @@ def test_remap_host_end_to_end():
     A.remap_host(h_src, La, h_dst, Ls, n, scratch)
     torch.cuda.synchronize()
     assert np.array_equal(h_dst.numpy(), oracle_dst(h_src.numpy(), aos, soa, widths, n))
+
+
+# ----------------------------------------------------------------------------- moved subset (NEXT N1)
+
+def test_remap_regions_moves_only_changed_fields():
+    """Medical AoSV -> SoA with the six unchanged singleton regions aliased between the two
+    instances: only {V1,V2,V3} move, the aliased regions are untouched, and the
+    result equals the full out-of-place remap."""
+    widths, n = [4] * 9, 1_000_003
+    aosv, soa = [0, 0, 0, 1, 2, 3, 4, 5, 6], list(range(9))
+    Lv, Ls = A.Layout(widths, aosv), A.Layout(widths, soa)
+    cols = field_columns(21, n, widths)
+    src_full = O.pack(cols, widths, aosv, n)
+    exp = oracle_dst(src_full, aosv, soa, widths, n)
+    exp_cols = O.unpack(exp, widths, soa, n)
+    # src instance as separate regions: the {V1,V2,V3} cluster and six singletons
+    v_reg = to_dev(np.ascontiguousarray(np.concatenate([cols[0], cols[1], cols[2]], 1)).reshape(-1))
+    singles = [to_dev(np.ascontiguousarray(cols[f]).reshape(-1)) for f in range(3, 9)]
+    dst_v = [sentinel_dev(4 * n) for _ in range(3)]
+    A.remap_regions([v_reg] + singles, Lv, dst_v + singles, Ls, n)
+    torch.cuda.synchronize()
+    for f in range(3):
+        assert np.array_equal(dst_v[f].cpu().numpy().reshape(n, 4), exp_cols[f])
+    for k, f in enumerate(range(3, 9)):
+        assert np.array_equal(singles[k].cpu().numpy().reshape(n, 4), exp_cols[f])
+    # a non-identical alias is rejected
+    with pytest.raises(A.AdhaError) as e:
+        A.remap_regions([v_reg] + singles, Lv, [v_reg] + dst_v[1:] + singles, Ls, n)
+    assert e.value.name == "ADHA_ERR_OVERLAP"
