@@ -207,13 +207,17 @@ ADHA_API adha_status adha_remap_sharded(const void* const* src_shards, const adh
 
 /* End-to-end remap of HOST buffers through the current device: src_host holds
  * bytes(Ls, N), dst_host receives bytes(Ld, N) (only payload bytes written).
- * The records are streamed in chunks through `scratch` (a DEVICE buffer of
- * scratch_bytes, 256-byte aligned): host->device copy of a chunk, adha_remap of
- * it, device->host copy of the result, with two chunks in flight on internal
- * streams so both copy directions overlap the kernels.  Ordered after prior
- * work on `stream`; later work on `stream` waits for completion.  Use pinned
- * host memory for asynchrony.  Errors: as adha_remap; INVALID_ARG if the
- * scratch cannot hold two chunks of at least 1 record. */
+ * Strategy (ADHA_HOST_MODE = auto | hybrid | zero | staged; auto = hybrid when dst_host
+ * is pinned, 256-byte aligned host memory and a scratch is given, else staged):
+ *   hybrid  record chunks (~16 MB) are copied host->device into `scratch` (one copy per
+ *           src region, copy engine) and each chunk's remap kernel stores its records
+ *           straight into dst_host over PCIe: H2D of chunk k+1 overlaps the kernel of k;
+ *   zero    one remap kernel reads src_host and writes dst_host directly (both pinned);
+ *   staged  H2D per src region, remap in `scratch`, D2H per dst region (pageable memory).
+ * `scratch` is a DEVICE buffer of scratch_bytes, 256-byte aligned (may be NULL only
+ * in zero mode).  Work is enqueued on internal streams ordered after prior work on
+ * `stream`; later work on `stream` waits for completion.  Errors: as adha_remap;
+ * INVALID_ARG if the scratch cannot hold a chunk of 4096 records. */
 ADHA_API adha_status adha_remap_host(const void* src_host, const adha_layout* src_layout,
                             void* dst_host, const adha_layout* dst_layout,
                             int64_t n_records, void* scratch, uint64_t scratch_bytes,

@@ -132,8 +132,11 @@ class Layout:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value:
-            _lib.adha_layout_destroy(h)
+        if h is not None and h.value and _lib is not None:
+            try:
+                _lib.adha_layout_destroy(h)
+            except Exception:       # interpreter shutdown: the library may already be gone
+                pass
             self._h = None
 
     @property
@@ -173,9 +176,15 @@ class Layout:
         return buf.value.decode()
 
     def nbytes(self, n_records: int) -> int:
-        out = _u64()
-        _check(_lib.adha_layout_bytes(self._h, int(n_records), ctypes.byref(out)))
-        return out.value
+        n = int(n_records)
+        cache = self.__dict__.setdefault("_nbytes", {})
+        if n not in cache:
+            out = _u64()
+            _check(_lib.adha_layout_bytes(self._h, n, ctypes.byref(out)))
+            if len(cache) > 64:
+                cache.clear()
+            cache[n] = out.value
+        return cache[n]
 
     def field_address(self, field: int, n_records: int):
         """(region_offset, stride, offset) of a field for an n_records instance."""
@@ -315,5 +324,24 @@ def plan_pdl(program, arch, profile=None) -> dict:
     return json.loads(_take_string(p))
 
 
-__all__ = ["Layout", "AdhaError", "remap", "remap_regions", "remap_chain", "shard_range", "remap_sharded", "remap_host",
+def plan_layouts(plan: dict, field_names: Sequence[str], widths: Sequence[int]) -> List[Layout]:
+    """One Layout per run of a PDL plan (adha_plan_pdl output), in execution order.  Consecutive
+    runs with different layouts are the plan's remap edges."""
+    return [Layout.from_string(r["layout"], field_names, widths) for r in plan["runs"]]
+
+
+def run_plan_remaps(plan: dict, field_names: Sequence[str], widths: Sequence[int], buffers: Sequence,
+                    n_records: int, stream=None) -> List[Layout]:
+    """Materialise every run's layout of a PDL plan on the device: buffers[0] holds the records in
+    the first run's layout; buffers[k] receives run k's layout (a chain of adha_remap on one
+    stream).  Returns the layouts."""
+    lays = plan_layouts(plan, field_names, widths)
+    if len(buffers) != len(lays):
+        raise ValueError("one buffer per run")
+    if len(lays) > 1:
+        remap_chain(buffers, lays, n_records, stream)
+    return lays
+
+
+__all__ = ["Layout", "AdhaError", "remap", "remap_regions", "remap_chain", "plan_layouts", "run_plan_remaps", "shard_range", "remap_sharded", "remap_host",
            "plan_describe", "plan_ods", "plan_pdl", "version", "LIB_PATH"]

@@ -21,6 +21,8 @@
 //   layouts beyond the tiled kernel's limits (more than 256 fields, ...).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include <algorithm>
 #include <cstring>
 #include <map>
@@ -71,8 +73,9 @@ __device__ __forceinline__ uint32_t copy_plan(const TiledParams& p, uint32_t c_l
 }
 
 // LDS.128 -> STG.128 of one staged tile, four vectors in flight per step
+template <bool HINT>
 __device__ __forceinline__ void copy_out(uint8_t* dst, uint32_t sm_base, uint32_t tid, int64_t lt, uint32_t nv,
-                                         const uint64_t (&gofs)[VMAX], const uint32_t (&gstep)[VMAX]) {
+                                         const uint64_t (&gofs)[VMAX], const uint32_t (&gstep)[VMAX], uint64_t pol) {
     constexpr uint32_t NT = NCONS * 32;
 #pragma unroll
     for (uint32_t u0 = 0; u0 < VMAX; u0 += 4) {
@@ -83,13 +86,16 @@ __device__ __forceinline__ void copy_out(uint8_t* dst, uint32_t sm_base, uint32_
                 if (u < nv) val[u - u0] = lds128(sm_base + tid * 16 + u * NT * 16);
 #pragma unroll
             for (uint32_t u = u0; u < u0 + 4 && u < VMAX; ++u)
-                if (u < nv) stg128(dst + gofs[u] + (uint64_t)lt * gstep[u], val[u - u0]);
+                if (u < nv) {
+                    if (HINT) stg128_hint(dst + gofs[u] + (uint64_t)lt * gstep[u], val[u - u0], pol);
+                    else stg128(dst + gofs[u] + (uint64_t)lt * gstep[u], val[u - u0]);
+                }
         }
     }
 }
 
 template <typename U, int NENT, int EMAX>
-__global__ void __launch_bounds__(NTHREADS, 1)
+__global__ void __maxnreg__(224)
     remap_tiled_kernel(const __grid_constant__ TiledParams p, const __grid_constant__ EntryTable<NENT> et) {
     extern __shared__ __align__(1024) uint8_t smem[];
     const uint32_t warp = threadIdx.x >> 5;
@@ -111,6 +117,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
     if (warp == NCONS) {
         // ------------------------------------------------------------ TMA producer
+        const uint64_t pol = policy_evict_first();        // src is read once: evict it first from L2
         uint32_t stage = 0, phase = 0, k = 0;
         for (int64_t t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
             while (t >= p.comp[k].tile_base + p.comp[k].n_tiles) ++k;
@@ -122,8 +129,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             const uint32_t ib = in0 + stage * p.stage_bytes;
             for (uint32_t c = p.comp[k].sc_lo + lane; c < p.comp[k].sc_hi; c += 32) {
                 const uint32_t bytes = T * p.srcc[c].stride;
-                bulk_load(ib + p.srcc[c].smem, (const void*)(p.src + p.srcc[c].region + (uint64_t)lt * bytes), bytes,
-                          full0 + 8 * stage);
+                const void* g = (const void*)(p.src + p.srcc[c].region + (uint64_t)lt * bytes);
+                if (p.l2_hints & 1) bulk_load_hint(ib + p.srcc[c].smem, g, bytes, full0 + 8 * stage, pol);
+                else bulk_load(ib + p.srcc[c].smem, g, bytes, full0 + 8 * stage);
             }
             if (++stage == p.s_in) { stage = 0; phase ^= 1; }
         }
@@ -132,6 +140,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
     // ---------------------------------------------------------------- consumers
     const uint32_t tid = threadIdx.x;
+    const uint64_t spol = policy_evict_first();
     uint32_t ioff[EMAX], ooff[EMAX], din[EMAX], dout[EMAX];
     uint64_t gofs[VMAX];
     uint32_t gstep[VMAX];
@@ -166,7 +175,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         mbar_wait(full0 + 8 * stage, phase);
         const uint32_t ib = in0 + stage * p.stage_bytes;
         if (p.comp[k].identity) {
-            copy_out((uint8_t*)p.dst, ib, tid, lt, nv, gofs, gstep);
+            if (p.l2_hints & 2) copy_out<true>((uint8_t*)p.dst, ib, tid, lt, nv, gofs, gstep, spol);
+            else copy_out<false>((uint8_t*)p.dst, ib, tid, lt, nv, gofs, gstep, spol);
             __syncwarp();
             if (lane == 0) mbar_arrive(empty0 + 8 * stage);
         } else {
@@ -195,7 +205,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(empty0 + 8 * stage);    // input stage free for the producer
             named_bar_sync(1, NCONS * 32);                      // output tile complete
-            copy_out((uint8_t*)p.dst, ob, tid, lt, nv, gofs, gstep);
+            if (p.l2_hints & 2) copy_out<true>((uint8_t*)p.dst, ob, tid, lt, nv, gofs, gstep, spol);
+            else copy_out<false>((uint8_t*)p.dst, ob, tid, lt, nv, gofs, gstep, spol);
             if (p.s_out == 2) oslot ^= 1;
         }
         if (++stage == p.s_in) { stage = 0; phase ^= 1; }
@@ -222,7 +233,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
 }
 
-__global__ void remap_naive_kernel(const __grid_constant__ NaiveParams p) {
+template <int NF>
+__global__ void remap_naive_kernel(const __grid_constant__ NaiveParamsT<NF> p) {
     const int64_t n = p.n_records;
     const int64_t total = n * (int64_t)p.n_fields;
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total; k += (int64_t)gridDim.x * blockDim.x) {
@@ -336,20 +348,24 @@ adha_status device_setup(const void* fn, int* n_sm) {
     return ADHA_OK;
 }
 
-adha_status launch_naive(const uint8_t* src, const Layout& ls, const std::vector<uint64_t>& bs, uint8_t* dst,
-                         const Layout& ld, const std::vector<uint64_t>& bd, int64_t lo, int64_t hi,
-                         cudaStream_t st) {
+// Direct global->global kernel: the fallback beyond the tiled kernel's limits, and the
+// latency path for small remaps (a handful of KB, where one launch with small parameters
+// and one load/store per unit beats staging through shared memory).
+template <int NF>
+adha_status launch_naive_t(const uint8_t* src, const Layout& ls, const std::vector<uint64_t>& bs, uint8_t* dst,
+                           const Layout& ld, const std::vector<uint64_t>& bd, int64_t lo, int64_t hi,
+                           cudaStream_t st) {
     int n_sm = 0;
     adha_status s = device_setup(nullptr, &n_sm);
     if (s != ADHA_OK) return s;
-    auto P = std::make_unique<NaiveParams>();
-    for (int f0 = 0; f0 < ls.n_fields; f0 += MAXF) {
-        std::memset(P.get(), 0, sizeof(NaiveParams));
+    auto P = std::make_unique<NaiveParamsT<NF>>();
+    for (int f0 = 0; f0 < ls.n_fields; f0 += NF) {
+        std::memset(P.get(), 0, sizeof(NaiveParamsT<NF>));
         P->src = (uint64_t)(uintptr_t)src;
         P->dst = (uint64_t)(uintptr_t)dst;
         P->n_records = hi - lo;
         P->lo = lo;
-        const int nf = std::min(MAXF, ls.n_fields - f0);
+        const int nf = std::min(NF, ls.n_fields - f0);
         P->n_fields = (uint32_t)nf;
         for (int k = 0; k < nf; ++k) {
             const int f = f0 + k;
@@ -359,11 +375,23 @@ adha_status launch_naive(const uint8_t* src, const Layout& ls, const std::vector
         }
         const int64_t total = (hi - lo) * (int64_t)nf;
         const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, (int64_t)n_sm * 16));
-        remap_naive_kernel<<<(unsigned)blocks, 256, 0, st>>>(*P);
+        remap_naive_kernel<NF><<<(unsigned)blocks, 256, 0, st>>>(*P);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_fail(e, "remap_naive_kernel launch");
     }
     return ADHA_OK;
+}
+
+adha_status launch_naive(const uint8_t* src, const Layout& ls, const std::vector<uint64_t>& bs, uint8_t* dst,
+                         const Layout& ld, const std::vector<uint64_t>& bd, int64_t lo, int64_t hi,
+                         cudaStream_t st) {
+    if (ls.n_fields <= SMALL_NF) return launch_naive_t<SMALL_NF>(src, ls, bs, dst, ld, bd, lo, hi, st);
+    return launch_naive_t<MAXF>(src, ls, bs, dst, ld, bd, lo, hi, st);
+}
+
+uint64_t small_bytes() {
+    const char* e = std::getenv("ADHA_SMALL_BYTES");   // read per call: tests switch the path
+    return e && *e ? (uint64_t)std::strtoull(e, nullptr, 10) : (uint64_t)(64u << 10);
 }
 
 struct Checked {
@@ -396,7 +424,9 @@ adha_status remap_checked(const uint8_t* src, const Layout& ls, uint8_t* dst, co
                           const Checked& ck, cudaStream_t st) {
     if (n == 0) return ADHA_OK;
     auto plan = get_plan(ls, ld);
-    if (!plan->tiled) return launch_naive(src, ls, ck.bs, dst, ld, ck.bd, 0, n, st);
+    // small remaps (<= ADHA_SMALL_BYTES of payload, 64 KB by default) are latency-bound: direct kernel
+    if (!plan->tiled || (uint64_t)n * ls.record_bytes <= small_bytes())
+        return launch_naive(src, ls, ck.bs, dst, ld, ck.bd, 0, n, st);
 
     const void* fn = nullptr;
     TiledLauncher launch = pick(plan->unit, plan->table_class, &fn);
@@ -412,6 +442,10 @@ adha_status remap_checked(const uint8_t* src, const Layout& ls, uint8_t* dst, co
     P->stage_bytes = plan->stage_bytes;
     P->s_in = plan->s_in;
     P->s_out = plan->s_out;
+    {
+        const char* h = std::getenv("ADHA_L2_HINTS");   // bit 0: loads evict_first, bit 1: stores evict_first
+        P->l2_hints = h && *h ? (uint32_t)std::strtoul(h, nullptr, 10) : 0u;
+    }
     P->n_comp = (uint32_t)plan->comps.size();
     P->unit = plan->unit;
     int64_t tiles = 0;
@@ -558,9 +592,11 @@ extern "C" adha_status adha_remap_sharded(const void* const* src_shards, const a
 // ---------------------------------------------------------------------------- host end-to-end
 namespace adha {
 namespace {
+constexpr int PIPE_SLOTS = 4;        // chunks in flight through the device scratch
+
 struct HostPipe {
-    cudaStream_t s[2] = {nullptr, nullptr};
-    cudaEvent_t start = nullptr, done[2] = {nullptr, nullptr};
+    cudaStream_t s[PIPE_SLOTS] = {};
+    cudaEvent_t start = nullptr, done[PIPE_SLOTS] = {};
 };
 std::mutex g_pipe_mu;
 std::map<int, HostPipe> g_pipes;
@@ -573,7 +609,7 @@ adha_status get_pipe(HostPipe** out) {
     auto it = g_pipes.find(dev);
     if (it == g_pipes.end()) {
         HostPipe hp;
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < PIPE_SLOTS; ++i) {
             if ((e = cudaStreamCreateWithFlags(&hp.s[i], cudaStreamNonBlocking)) != cudaSuccess)
                 return cuda_fail(e, "cudaStreamCreate");
             if ((e = cudaEventCreateWithFlags(&hp.done[i], cudaEventDisableTiming)) != cudaSuccess)
@@ -589,6 +625,24 @@ adha_status get_pipe(HostPipe** out) {
 }  // namespace
 }  // namespace adha
 
+namespace adha {
+namespace {
+bool is_pinned_host(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost && a.devicePointer == p;   // pinned and UVA-mapped at the same address
+}
+
+uint64_t env_bytes(const char* name, uint64_t dflt) {
+    const char* e = std::getenv(name);
+    return e && *e ? std::strtoull(e, nullptr, 10) : dflt;
+}
+}  // namespace
+}  // namespace adha
+
 extern "C" adha_status adha_remap_host(const void* src_host, const adha_layout* hs, void* dst_host,
                                        const adha_layout* hd, int64_t n, void* scratch, uint64_t scratch_bytes,
                                        void* stream) {
@@ -597,44 +651,67 @@ extern "C" adha_status adha_remap_host(const void* src_host, const adha_layout* 
     adha_status s = validate(src_host, hs, dst_host, hd, n, &ck, false);
     if (s != ADHA_OK) return s;
     if (n == 0) return ADHA_OK;
-    if (!scratch || ((uintptr_t)scratch & 255)) return fail(ADHA_ERR_ALIGNMENT, "scratch must be 256-byte aligned");
     const Layout& ls = hs->L;
     const Layout& ld = hd->L;
-    // chunk records: two slots, each holding a src and a dst instance of `nc` records
-    const uint64_t slot = (scratch_bytes / 2) & ~uint64_t(255);
+    cudaStream_t user = (cudaStream_t)stream;
+    const bool src_pinned = is_pinned_host(src_host), dst_pinned = is_pinned_host(dst_host);
+    const bool aligned = !(((uintptr_t)src_host | (uintptr_t)dst_host) & 255);
+    // Modes (ADHA_HOST_MODE = auto | zero | hybrid | staged):
+    //   hybrid  the copy engine streams src chunks into the device scratch (one H2D per src region),
+    //           the remap kernel of each chunk writes its records straight into the pinned host dst
+    //           over PCIe -- both PCIe directions busy, no D2H copies;
+    //   zero    one remap kernel reads the pinned host src (TMA over PCIe) and writes the pinned
+    //           host dst directly, no scratch at all;
+    //   staged  H2D per src region, remap in device memory, D2H per dst region (pageable memory).
+    std::string mode = std::getenv("ADHA_HOST_MODE") ? std::getenv("ADHA_HOST_MODE") : "auto";
+    if (mode == "auto") mode = (dst_pinned && aligned && scratch) ? "hybrid" : "staged";
+    if ((mode == "zero" && !(src_pinned && dst_pinned && aligned)) || (mode == "hybrid" && !(dst_pinned && aligned)))
+        mode = "staged";
+    if (mode == "zero") return remap_checked((const uint8_t*)src_host, ls, (uint8_t*)dst_host, ld, n, ck, user);
+
+    if (!scratch || ((uintptr_t)scratch & 255)) return fail(ADHA_ERR_ALIGNMENT, "scratch must be 256-byte aligned");
+    const bool hybrid = mode == "hybrid";
+    // Records stream through the scratch in chunks of nc records (a multiple of 4096, so host
+    // region offsets lo*stride stay 16-byte aligned); each chunk is its own layout instance
+    // (record locality).  PIPE_SLOTS chunks are in flight on PIPE_SLOTS internal streams.
+    int slots = PIPE_SLOTS;
     const uint64_t pad = 256ull * (ls.n_clusters() + ld.n_clusters() + 2);
     const uint64_t R = ls.record_bytes;
-    if (slot <= pad + 2 * R) return fail(ADHA_ERR_INVALID_ARG, "scratch too small for two chunks");
-    int64_t nc = (int64_t)((slot - pad) / (2 * R));
-    if (nc > 4096) nc = nc / 4096 * 4096;
+    const uint64_t per_rec = hybrid ? R : 2 * R;
+    uint64_t slot = 0;
+    for (; slots >= 1; --slots) {
+        slot = (scratch_bytes / slots) & ~uint64_t(255);
+        if (slot > pad + 4096 * per_rec) break;
+    }
+    if (slots < 1) return fail(ADHA_ERR_INVALID_ARG, "scratch too small for a chunk of 4096 records");
+    const uint64_t chunk_bytes = env_bytes("ADHA_HOST_CHUNK_BYTES", hybrid ? (16ull << 20) : (64ull << 20));
+    int64_t nc = std::min<int64_t>((int64_t)((slot - pad) / per_rec), (int64_t)std::max<uint64_t>(1, chunk_bytes / R));
+    nc = std::max<int64_t>(4096, nc / 4096 * 4096);
     nc = std::min<int64_t>(nc, n);
-    // keep at least 4 chunks in flight for large N so copies overlap kernels
-    if (n > 4 * 4096 && nc > n / 4) nc = std::max<int64_t>(4096, (n / 4) / 4096 * 4096);
     std::vector<uint64_t> cbs, cbd;
     uint64_t cbytes_s = 0, cbytes_d = 0;
     ls.region_bases(nc, cbs, &cbytes_s);
     ld.region_bases(nc, cbd, &cbytes_d);
     const uint64_t off_d = align256(cbytes_s);
-    if (off_d + cbytes_d > slot) return fail(ADHA_ERR_INVALID_ARG, "scratch too small");
+    if ((hybrid ? cbytes_s : off_d + cbytes_d) > slot) return fail(ADHA_ERR_INVALID_ARG, "scratch too small");
 
     HostPipe* hp = nullptr;
     if ((s = get_pipe(&hp)) != ADHA_OK) return s;
-    cudaStream_t user = (cudaStream_t)stream;
     cudaError_t e = cudaEventRecord(hp->start, user);
     if (e != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
-    for (int i = 0; i < 2; ++i)
+    for (int i = 0; i < slots; ++i)
         if ((e = cudaStreamWaitEvent(hp->s[i], hp->start, 0)) != cudaSuccess) return cuda_fail(e, "cudaStreamWaitEvent");
 
     const uint8_t* hsrc = (const uint8_t*)src_host;
     uint8_t* hdst = (uint8_t*)dst_host;
     int64_t k = 0;
+    std::vector<uint64_t> ms, md;
     for (int64_t lo = 0; lo < n; lo += nc, ++k) {
         const int64_t m = std::min<int64_t>(nc, n - lo);
-        const int i = (int)(k & 1);
+        const int i = (int)(k % slots);
         cudaStream_t st = hp->s[i];
         uint8_t* dsrc = (uint8_t*)scratch + (uint64_t)i * slot;
         uint8_t* ddst = dsrc + off_d;
-        std::vector<uint64_t> ms, md;
         uint64_t mbs = 0, mbd = 0;
         ls.region_bases(m, ms, &mbs);
         ld.region_bases(m, md, &mbd);
@@ -645,17 +722,24 @@ extern "C" adha_status adha_remap_host(const void* src_host, const adha_layout* 
         }
         Checked cm;
         cm.bs = ms;
-        cm.bd = md;
         cm.bytes_s = mbs;
-        cm.bytes_d = mbd;
-        if ((s = remap_checked(dsrc, ls, ddst, ld, m, cm, st)) != ADHA_OK) return s;
-        for (int c = 0; c < ld.n_clusters(); ++c) {
-            e = cudaMemcpyAsync(hdst + ck.bd[c] + (uint64_t)lo * ld.stride[c], ddst + md[c], (uint64_t)m * ld.stride[c],
-                                cudaMemcpyDeviceToHost, st);
-            if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync D2H");
+        if (hybrid) {
+            // dst regions of this chunk inside the host buffer: base_c(N) + lo * stride_c
+            cm.bd.resize(ld.n_clusters());
+            for (int c = 0; c < ld.n_clusters(); ++c) cm.bd[c] = ck.bd[c] + (uint64_t)lo * ld.stride[c];
+            if ((s = remap_checked(dsrc, ls, hdst, ld, m, cm, st)) != ADHA_OK) return s;
+        } else {
+            cm.bd = md;
+            cm.bytes_d = mbd;
+            if ((s = remap_checked(dsrc, ls, ddst, ld, m, cm, st)) != ADHA_OK) return s;
+            for (int c = 0; c < ld.n_clusters(); ++c) {
+                e = cudaMemcpyAsync(hdst + ck.bd[c] + (uint64_t)lo * ld.stride[c], ddst + md[c],
+                                    (uint64_t)m * ld.stride[c], cudaMemcpyDeviceToHost, st);
+                if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync D2H");
+            }
         }
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < slots; ++i) {
         if ((e = cudaEventRecord(hp->done[i], hp->s[i])) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
         if ((e = cudaStreamWaitEvent(user, hp->done[i], 0)) != cudaSuccess) return cuda_fail(e, "cudaStreamWaitEvent");
     }

@@ -79,6 +79,8 @@ struct TiledParams {
     uint32_t s_out;       // output buffers: 2 = double-buffered, 1 = one buffer + a barrier before reuse
     uint32_t n_comp;
     uint32_t unit;        // g
+    uint32_t l2_hints;    // bit 0: TMA loads with L2 evict_first; bit 1: stores with L2 evict_first
+    uint32_t pad0;
     CompDesc comp[MAXK];
     ClusterDesc srcc[MAXC];
     ClusterDesc dstc[MAXC];
@@ -102,14 +104,18 @@ struct NaiveField {
     uint64_t sbase, dbase;
     uint32_t sstride, dstride, soff, doff, width, pad;
 };
-struct NaiveParams {
+template <int NF>
+struct NaiveParamsT {
     uint64_t src;
     uint64_t dst;
     int64_t n_records;
     int64_t lo;           // first record
     uint32_t n_fields;
-    NaiveField f[MAXF];
+    NaiveField f[NF];
 };
+using NaiveParams = NaiveParamsT<MAXF>;
+constexpr int SMALL_NF = 32;                  // direct kernel with small parameters (latency path)
+using SmallParams = NaiveParamsT<SMALL_NF>;
 
 }  // namespace dev
 

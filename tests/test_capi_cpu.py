@@ -296,3 +296,16 @@ def test_plan_falls_back_beyond_limits():
     widths = [4] * 300
     d = A.plan_describe(A.Layout.aos(widths), A.Layout.soa(widths))
     assert not d["tiled"] and "fields" in d["why_naive"]
+
+
+def test_plan_layouts_follow_the_plan(expected):
+    plan = A.plan_pdl(golden("medical_program.json"), golden("medical_arch.json"), golden("medical_profile.json"))
+    names = [f["name"] for f in golden("medical_program.json")["fields"]]
+    lays = A.plan_layouts(plan, names, [4] * 9)
+    assert [l.to_string() for l in lays] == [r[2] for r in expected["medical_plan"]["runs"]]
+    # the remap edge moves exactly the fields whose cluster differs (same-device reading)
+    a, b = lays
+    moved = [names[f] for f in range(9)
+             if {g for g in range(9) if a.cluster_of[g] == a.cluster_of[f]} !=
+                {g for g in range(9) if b.cluster_of[g] == b.cluster_of[f]}]
+    assert moved == expected["medical_plan"]["remap_moved"]

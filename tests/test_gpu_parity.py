@@ -25,6 +25,17 @@ if not torch.cuda.is_available():
 import paper_1407_4859_b200 as A  # noqa: E402
 
 
+@pytest.fixture(params=["tiled", "direct-small"])
+def small_path(request, monkeypatch):
+    """Run a test twice: with every remap on the tiled kernel (ADHA_SMALL_BYTES=0), and with the
+    default routing where remaps of <= 64 KB take the direct latency kernel."""
+    if request.param == "tiled":
+        monkeypatch.setenv("ADHA_SMALL_BYTES", "0")
+    else:
+        monkeypatch.delenv("ADHA_SMALL_BYTES", raising=False)
+    return request.param
+
+
 def oracle_dst(src, ls, ld, widths, n):
     dst = np.full(O.layout_bytes(widths, ld, n), SENT, np.uint8)
     O.remap(src, ls, dst, ld, widths, n, threads=min(8, os.cpu_count() or 1))
@@ -48,7 +59,7 @@ def plan_T(widths, ls, ld):
 
 # ----------------------------------------------------------------------------- C1
 
-def test_c1_xyz_aos_soa_and_back():
+def test_c1_xyz_aos_soa_and_back(small_path):
     widths, n = [4, 4, 4], 1024
     cols = field_columns(SEED_BASE + 0, n, widths)
     aos, soa = [0, 0, 0], [0, 1, 2]
@@ -63,7 +74,7 @@ def test_c1_xyz_aos_soa_and_back():
 # ----------------------------------------------------------------------------- brute force
 
 @pytest.mark.parametrize("widths", [[1, 2, 3, 4, 8], [4, 4, 4, 8, 4], [2, 2, 6, 4, 2]])
-def test_all_layout_pairs_5_fields(widths):
+def test_all_layout_pairs_5_fields(widths, small_path):
     parts = set_partitions(5)
     rng = np.random.default_rng(sum(widths))
     for ls in parts:
@@ -105,7 +116,7 @@ AOSV = [0, 0, 0, 1, 2, 3, 4, 5, 6]
     ("P2-soa-4x8", [4] * 32, list(range(32)), [i // 8 for i in range(32)]),
     ("identity-hybrid", [4] * 9, AOSV, AOSV),
 ])
-def test_config_shapes_small(name, widths, ls, ld):
+def test_config_shapes_small(name, widths, ls, ld, small_path):
     T = plan_T(widths, ls, ld)
     for n in (1, 33, T + 7, 5 * T + 31, 151 * T + 3):
         check_pair(widths, ls, ld, n, seed=n)
@@ -285,3 +296,22 @@ def test_remap_regions_moves_only_changed_fields():
     with pytest.raises(A.AdhaError) as e:
         A.remap_regions([v_reg] + singles, Lv, [v_reg] + dst_v[1:] + singles, Ls, n)
     assert e.value.name == "ADHA_ERR_OVERLAP"
+
+
+def test_pdl_plan_drives_the_remap():
+    """Planner -> remap: the Medical PDL plan (Table 4 row 1) has two runs, AoSV on
+    the CPU side and SoA on the GPU side; materialising them runs the plan's one remap edge."""
+    from tests.conftest import golden
+    plan = A.plan_pdl(golden("medical_program.json"), golden("medical_arch.json"), golden("medical_profile.json"))
+    names = [f["name"] for f in golden("medical_program.json")["fields"]]
+    widths = [4] * 9
+    n = 300_007
+    lays = A.plan_layouts(plan, names, widths)
+    assert [l.to_string() for l in lays] == [r["layout"] for r in plan["runs"]]
+    labs = [l.cluster_of for l in lays]
+    cols = field_columns(31, n, widths)
+    src = O.pack(cols, widths, labs[0], n)
+    bufs = [to_dev(src), sentinel_dev(lays[1].nbytes(n))]
+    A.run_plan_remaps(plan, names, widths, bufs, n)
+    torch.cuda.synchronize()
+    assert np.array_equal(bufs[1].cpu().numpy(), oracle_dst(src, labs[0], labs[1], widths, n))
