@@ -46,7 +46,7 @@ using namespace adha::ptx;
 // cluster order).  Vector u lands at dst + gofs[u] + lt * gstep[u] for local tile lt.
 // The mapping is the same for every tile of the component, so it is computed once per
 // component switch and kept in registers.
-constexpr uint32_t VMAX = 14;                  // 14 * 16 B * 256 threads = 57344 B >= stage_bytes
+constexpr uint32_t VMAX = 12;                  // 12 * 16 B * 256 threads = 49152 B >= stage_bytes
 
 __device__ __forceinline__ uint32_t copy_plan(const TiledParams& p, uint32_t c_lo, uint32_t T, uint32_t total,
                                               uint32_t tid, uint64_t (&gofs)[VMAX], uint32_t (&gstep)[VMAX]) {
@@ -94,8 +94,11 @@ __device__ __forceinline__ void copy_out(uint8_t* dst, uint32_t sm_base, uint32_
     }
 }
 
+// 9 warps per CTA: the register file is split over the 4 SM sub-partitions (16K registers
+// each) and one of them holds 3 warps, so a thread may use at most 16384 / 96 = 168 registers;
+// __launch_bounds__(NTHREADS, 1) gives ptxas exactly that budget.
 template <typename U, int NENT, int EMAX>
-__global__ void __maxnreg__(224)
+__global__ void __launch_bounds__(NTHREADS, 1)
     remap_tiled_kernel(const __grid_constant__ TiledParams p, const __grid_constant__ EntryTable<NENT> et) {
     extern __shared__ __align__(1024) uint8_t smem[];
     const uint32_t warp = threadIdx.x >> 5;
@@ -343,6 +346,12 @@ adha_status device_setup(const void* fn, int* n_sm) {
     if (fn && !c.attr_done.count({dev, fn})) {
         e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
         if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+        cudaFuncAttributes fa;
+        e = cudaFuncGetAttributes(&fa, fn);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaFuncGetAttributes");
+        if (fa.maxThreadsPerBlock < NTHREADS)      // register budget regression guard
+            return fail(ADHA_ERR_UNSUPPORTED, "remap_tiled_kernel uses " + std::to_string(fa.numRegs) +
+                                                  " registers: cannot launch " + std::to_string(NTHREADS) + " threads");
         c.attr_done.insert({dev, fn});
     }
     return ADHA_OK;
@@ -684,7 +693,10 @@ extern "C" adha_status adha_remap_host(const void* src_host, const adha_layout* 
         if (slot > pad + 4096 * per_rec) break;
     }
     if (slots < 1) return fail(ADHA_ERR_INVALID_ARG, "scratch too small for a chunk of 4096 records");
-    const uint64_t chunk_bytes = env_bytes("ADHA_HOST_CHUNK_BYTES", hybrid ? (16ull << 20) : (64ull << 20));
+    // chunk: ~16 MB (hybrid) / 64 MB (staged), but at least 4 MB per src region so every H2D
+    // copy stays large (C3's 64 SoA regions -> 256 MB chunks)
+    const uint64_t dflt = std::max<uint64_t>(hybrid ? (16ull << 20) : (64ull << 20), (4ull << 20) * ls.n_clusters());
+    const uint64_t chunk_bytes = env_bytes("ADHA_HOST_CHUNK_BYTES", dflt);
     int64_t nc = std::min<int64_t>((int64_t)((slot - pad) / per_rec), (int64_t)std::max<uint64_t>(1, chunk_bytes / R));
     nc = std::max<int64_t>(4096, nc / 4096 * 4096);
     nc = std::min<int64_t>(nc, n);

@@ -42,7 +42,7 @@ constexpr int MAXK = 64;                       // components
 constexpr int S_OUT_MAX = 2;                   // output staging buffers (1 or 2)
 constexpr int HDR_BYTES = 1024;                // barrier header at the start of dynamic smem
 constexpr int MAX_S_IN = 8;
-constexpr uint32_t STAGE_MAX = 14 * 16 * NCONS * 32;   // copy-out covers 14 16-byte vectors per thread
+constexpr uint32_t STAGE_MAX = 12 * 16 * NCONS * 32;   // copy-out covers 12 16-byte vectors per thread
 
 struct ClusterDesc {
     uint64_t region;    // region base in the buffer for this N (bytes)
