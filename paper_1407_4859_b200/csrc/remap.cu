@@ -94,6 +94,16 @@ __device__ __forceinline__ void copy_out(uint8_t* dst, uint32_t sm_base, uint32_
     }
 }
 
+// Tile order of a CTA: interleaved (t = b, b+G, ...: the GPU sweeps the arrays as one front)
+// or blocked (CTA b takes the contiguous range [b*M/G, (b+1)*M/G)).
+__device__ __forceinline__ int64_t t_first(const TiledParams& p) {
+    return p.blocked ? (int64_t)blockIdx.x * p.total_tiles / gridDim.x : (int64_t)blockIdx.x;
+}
+__device__ __forceinline__ int64_t t_end(const TiledParams& p) {
+    return p.blocked ? (int64_t)(blockIdx.x + 1) * p.total_tiles / gridDim.x : p.total_tiles;
+}
+__device__ __forceinline__ int64_t t_step(const TiledParams& p) { return p.blocked ? 1 : (int64_t)gridDim.x; }
+
 // 9 warps per CTA: the register file is split over the 4 SM sub-partitions (16K registers
 // each) and one of them holds 3 warps, so a thread may use at most 16384 / 96 = 168 registers;
 // __launch_bounds__(NTHREADS, 1) gives ptxas exactly that budget.
@@ -122,7 +132,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         // ------------------------------------------------------------ TMA producer
         const uint64_t pol = policy_evict_first();        // src is read once: evict it first from L2
         uint32_t stage = 0, phase = 0, k = 0;
-        for (int64_t t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
+        for (int64_t t = t_first(p), te = t_end(p); t < te; t += t_step(p)) {
             while (t >= p.comp[k].tile_base + p.comp[k].n_tiles) ++k;
             const int64_t lt = t - p.comp[k].tile_base;
             const uint32_t T = p.comp[k].T;
@@ -150,7 +160,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     uint32_t ne = 0, nv = 0;
     int k_cur = -1;
     uint32_t stage = 0, phase = 0, oslot = 0, k = 0;
-    for (int64_t t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
+    for (int64_t t = t_first(p), te = t_end(p); t < te; t += t_step(p)) {
         while (t >= p.comp[k].tile_base + p.comp[k].n_tiles) ++k;
         const int64_t lt = t - p.comp[k].tile_base;
         const uint32_t T = p.comp[k].T;
@@ -454,6 +464,8 @@ adha_status remap_checked(const uint8_t* src, const Layout& ls, uint8_t* dst, co
     {
         const char* h = std::getenv("ADHA_L2_HINTS");   // bit 0: loads evict_first, bit 1: stores evict_first
         P->l2_hints = h && *h ? (uint32_t)std::strtoul(h, nullptr, 10) : 0u;
+        const char* b = std::getenv("ADHA_TILE_ORDER");   // "blocked" | default interleaved
+        P->blocked = (b && std::string(b) == "blocked") ? 1u : 0u;
     }
     P->n_comp = (uint32_t)plan->comps.size();
     P->unit = plan->unit;

@@ -80,7 +80,7 @@ struct TiledParams {
     uint32_t n_comp;
     uint32_t unit;        // g
     uint32_t l2_hints;    // bit 0: TMA loads with L2 evict_first; bit 1: stores with L2 evict_first
-    uint32_t pad0;
+    uint32_t blocked;     // 1: CTA b processes a contiguous tile range, 0: tiles b, b+G, b+2G, ...
     CompDesc comp[MAXK];
     ClusterDesc srcc[MAXC];
     ClusterDesc dstc[MAXC];

@@ -315,3 +315,19 @@ def test_pdl_plan_drives_the_remap():
     A.run_plan_remaps(plan, names, widths, bufs, n)
     torch.cuda.synchronize()
     assert np.array_equal(bufs[1].cpu().numpy(), oracle_dst(src, labs[0], labs[1], widths, n))
+
+
+def test_random_layout_pairs_tiled(monkeypatch):
+    """Random records (1..40 fields, widths 1..16 incl. odd), random partitions on both sides,
+    random N around tile boundaries: tiled kernel forced (ADHA_SMALL_BYTES=0)."""
+    monkeypatch.setenv("ADHA_SMALL_BYTES", "0")
+    rng = np.random.default_rng(1407)
+    for trial in range(120):
+        F = int(rng.integers(1, 41))
+        widths = [int(x) for x in rng.choice([1, 2, 3, 4, 4, 4, 8, 8, 12, 16], size=F)]
+        k1, k2 = int(rng.integers(1, F + 1)), int(rng.integers(1, F + 1))
+        ls = [int(x) for x in rng.integers(0, k1, size=F)]
+        ld = [int(x) for x in rng.integers(0, k2, size=F)]
+        T = plan_T(widths, ls, ld)
+        n = int(rng.choice([T - 1, T, T + 1, 3 * T + int(rng.integers(0, T)), 160 * T + 7]))
+        check_pair(widths, ls, ld, max(n, 1), seed=trial)
