@@ -244,10 +244,18 @@ def main():
 
     import torch
     import torch.distributed as dist
+    # ADHA_BENCH_SHARE_GPU=1 (test only): every rank on cuda:0 with a gloo group, to exercise the
+    # multi-rank code path on a one-GPU box (the ranks' kernels never wait on one another)
+    share = os.environ.get("ADHA_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     import paper_1407_4859_b200 as A
     from paper_1407_4859_b200.sharding import shard_for, max_over_ranks, aggregate_gbs
@@ -294,7 +302,10 @@ def main():
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local])
+            if share:
+                dist.barrier()
+            else:
+                dist.barrier(device_ids=[local])
 
     for _ in range(max(args.warmup, 3)):
         step()
