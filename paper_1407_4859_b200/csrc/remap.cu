@@ -46,6 +46,7 @@ using namespace adha::ptx;
 // cluster order).  Vector u lands at dst + gofs[u] + lt * gstep[u] for local tile lt.
 // The mapping is the same for every tile of the component, so it is computed once per
 // component switch and kept in registers.
+constexpr uint32_t PMAX = 4;                   // bulk-load pieces per producer lane per tile
 constexpr uint32_t VMAX = 12;                  // 12 * 16 B * 256 threads = 49152 B >= stage_bytes
 
 __device__ __forceinline__ uint32_t copy_plan(const TiledParams& p, uint32_t c_lo, uint32_t T, uint32_t total,
@@ -130,21 +131,62 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
     if (warp == NCONS) {
         // ------------------------------------------------------------ TMA producer
+        // Per component, every lane holds up to PMAX bulk-load pieces of the tile (src chunks cut
+        // into pieces of at most `split` bytes): smem offset, global offset of tile 0, bytes, and
+        // the per-tile global step.  Issue is then one bulk copy per piece per lane, no parameter
+        // walks on the critical path (the producer's issue time gates the 2-stage pipeline).
         const uint64_t pol = policy_evict_first();        // src is read once: evict it first from L2
+        uint32_t psm[PMAX], pbytes[PMAX], pstep[PMAX];
+        uint64_t pg[PMAX];
+        uint32_t np = 0;
+        int kp = -1;
         uint32_t stage = 0, phase = 0, k = 0;
         for (int64_t t = t_first(p), te = t_end(p); t < te; t += t_step(p)) {
             while (t >= p.comp[k].tile_base + p.comp[k].n_tiles) ++k;
             const int64_t lt = t - p.comp[k].tile_base;
-            const uint32_t T = p.comp[k].T;
+            if ((int)k != kp) {
+                kp = (int)k;
+                const uint32_t T = p.comp[k].T;
+                // piece size: the configured split, grown until the tile needs at most 32*PMAX pieces
+                uint32_t split = p.tma_split ? p.tma_split : 0xFFFFFFF0u;
+                uint32_t pieces;
+                for (;;) {
+                    pieces = 0;
+                    for (uint32_t c = p.comp[k].sc_lo; c < p.comp[k].sc_hi; ++c)
+                        pieces += (T * p.srcc[c].stride + split - 1) / split;
+                    if (pieces <= 32 * PMAX) break;
+                    split = ((split + split / 2) + 15) & ~15u;
+                }
+                np = 0;
+                uint32_t piece = 0;
+#pragma unroll 1
+                for (uint32_t c = p.comp[k].sc_lo; c < p.comp[k].sc_hi; ++c) {
+                    const uint32_t bytes = T * p.srcc[c].stride;
+                    for (uint32_t o = 0; o < bytes; o += split, ++piece) {
+                        if ((piece & 31) != lane) continue;
+#pragma unroll
+                        for (uint32_t q = 0; q < PMAX; ++q)
+                            if (q == np) {
+                                psm[q] = p.srcc[c].smem + o;
+                                pg[q] = p.src + p.srcc[c].region + o;
+                                pbytes[q] = min(split, bytes - o);
+                                pstep[q] = bytes;
+                            }
+                        ++np;
+                    }
+                }
+            }
             mbar_wait(empty0 + 8 * stage, phase ^ 1);
             if (lane == 0) mbar_arrive_expect_tx(full0 + 8 * stage, p.comp[k].tile_bytes);
             __syncwarp();
             const uint32_t ib = in0 + stage * p.stage_bytes;
-            for (uint32_t c = p.comp[k].sc_lo + lane; c < p.comp[k].sc_hi; c += 32) {
-                const uint32_t bytes = T * p.srcc[c].stride;
-                const void* g = (const void*)(p.src + p.srcc[c].region + (uint64_t)lt * bytes);
-                if (p.l2_hints & 1) bulk_load_hint(ib + p.srcc[c].smem, g, bytes, full0 + 8 * stage, pol);
-                else bulk_load(ib + p.srcc[c].smem, g, bytes, full0 + 8 * stage);
+#pragma unroll
+            for (uint32_t q = 0; q < PMAX; ++q) {
+                if (q < np) {
+                    const void* g = (const void*)(pg[q] + (uint64_t)lt * pstep[q]);
+                    if (p.l2_hints & 1) bulk_load_hint(ib + psm[q], g, pbytes[q], full0 + 8 * stage, pol);
+                    else bulk_load(ib + psm[q], g, pbytes[q], full0 + 8 * stage);
+                }
             }
             if (++stage == p.s_in) { stage = 0; phase ^= 1; }
         }
@@ -187,32 +229,44 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
         mbar_wait(full0 + 8 * stage, phase);
         const uint32_t ib = in0 + stage * p.stage_bytes;
-        if (p.comp[k].identity) {
-            if (p.l2_hints & 2) copy_out<true>((uint8_t*)p.dst, ib, tid, lt, nv, gofs, gstep, spol);
-            else copy_out<false>((uint8_t*)p.dst, ib, tid, lt, nv, gofs, gstep, spol);
-            __syncwarp();
-            if (lane == 0) mbar_arrive(empty0 + 8 * stage);
-        } else {
+        {
             const uint32_t ob = out0 + oslot * p.stage_bytes;
-            const uint32_t periods = T / 32;
             if (p.s_out == 1) named_bar_sync(1, NCONS * 32);   // previous copy-out done with the buffer
+            if (p.comp[k].identity) {
+                // same cluster on both sides: the staged chunk is already the output chunk; move it
+                // to the output buffer with 16-byte shared copies so the input stage is released as
+                // early as after a permutation (holding it through the copy-out starves the loads)
+                const uint32_t tb = p.comp[k].tile_bytes;
+                uint32_t v = tid * 16;
+                for (; v + 3 * NCONS * 32 * 16 < tb; v += 4 * NCONS * 32 * 16) {
+                    const uint4 a0 = lds128(ib + v), a1 = lds128(ib + v + NCONS * 32 * 16);
+                    const uint4 a2 = lds128(ib + v + 2 * NCONS * 32 * 16), a3 = lds128(ib + v + 3 * NCONS * 32 * 16);
+                    sts128(ob + v, a0);
+                    sts128(ob + v + NCONS * 32 * 16, a1);
+                    sts128(ob + v + 2 * NCONS * 32 * 16, a2);
+                    sts128(ob + v + 3 * NCONS * 32 * 16, a3);
+                }
+                for (; v < tb; v += NCONS * 32 * 16) sts128(ob + v, lds128(ib + v));
+            } else {
+                const uint32_t periods = T / 32;
 #pragma unroll
-            for (int e = 0; e < EMAX; ++e) {
-                if ((uint32_t)e < ne) {
-                    const uint32_t ia = ib + ioff[e], oa = ob + ooff[e];
-                    const uint32_t di = din[e], dO = dout[e];
-                    uint32_t q = 0;
-                    for (; q + 4 <= periods; q += 4) {
-                        const U v0 = lds<U>(ia + (q + 0) * di);
-                        const U v1 = lds<U>(ia + (q + 1) * di);
-                        const U v2 = lds<U>(ia + (q + 2) * di);
-                        const U v3 = lds<U>(ia + (q + 3) * di);
-                        sts(oa + (q + 0) * dO, v0);
-                        sts(oa + (q + 1) * dO, v1);
-                        sts(oa + (q + 2) * dO, v2);
-                        sts(oa + (q + 3) * dO, v3);
+                for (int e = 0; e < EMAX; ++e) {
+                    if ((uint32_t)e < ne) {
+                        const uint32_t ia = ib + ioff[e], oa = ob + ooff[e];
+                        const uint32_t di = din[e], dO = dout[e];
+                        uint32_t q = 0;
+                        for (; q + 4 <= periods; q += 4) {
+                            const U v0 = lds<U>(ia + (q + 0) * di);
+                            const U v1 = lds<U>(ia + (q + 1) * di);
+                            const U v2 = lds<U>(ia + (q + 2) * di);
+                            const U v3 = lds<U>(ia + (q + 3) * di);
+                            sts(oa + (q + 0) * dO, v0);
+                            sts(oa + (q + 1) * dO, v1);
+                            sts(oa + (q + 2) * dO, v2);
+                            sts(oa + (q + 3) * dO, v3);
+                        }
+                        for (; q < periods; ++q) sts(oa + q * dO, lds<U>(ia + q * di));
                     }
-                    for (; q < periods; ++q) sts(oa + q * dO, lds<U>(ia + q * di));
                 }
             }
             __syncwarp();
@@ -464,6 +518,8 @@ adha_status remap_checked(const uint8_t* src, const Layout& ls, uint8_t* dst, co
     {
         const char* h = std::getenv("ADHA_L2_HINTS");   // bit 0: loads evict_first, bit 1: stores evict_first
         P->l2_hints = h && *h ? (uint32_t)std::strtoul(h, nullptr, 10) : 0u;
+        const char* ts = std::getenv("ADHA_TMA_SPLIT");   // bytes per TMA bulk load (multiple of 16), 0 = whole chunk
+        P->tma_split = ts && *ts ? ((uint32_t)std::strtoul(ts, nullptr, 10) & ~15u) : 0u;
         const char* b = std::getenv("ADHA_TILE_ORDER");   // "blocked" | default interleaved
         P->blocked = (b && std::string(b) == "blocked") ? 1u : 0u;
     }

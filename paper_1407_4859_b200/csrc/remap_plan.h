@@ -81,6 +81,8 @@ struct TiledParams {
     uint32_t unit;        // g
     uint32_t l2_hints;    // bit 0: TMA loads with L2 evict_first; bit 1: stores with L2 evict_first
     uint32_t blocked;     // 1: CTA b processes a contiguous tile range, 0: tiles b, b+G, b+2G, ...
+    uint32_t tma_split;   // 0: one bulk load per src chunk; else pieces of at most this many bytes
+    uint32_t pad1;
     CompDesc comp[MAXK];
     ClusterDesc srcc[MAXC];
     ClusterDesc dstc[MAXC];
