@@ -200,6 +200,52 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     uint64_t gofs[VMAX];
     uint32_t gstep[VMAX];
     uint32_t ne = 0, nv = 0;
+
+    // Tails first: records [n_tiles*T_k, N) of every component, spread over the consumer threads
+    // of ALL CTAs, four records in flight per thread.  Done while the producer's first tiles are
+    // still in flight, so the latency-bound scalar copies hide under the pipeline fill (one CTA
+    // copying a 48 KB tail alone took ~40 us).
+    {
+        const int64_t gid = (int64_t)blockIdx.x * (NCONS * 32) + tid;
+        const int64_t gstride = (int64_t)gridDim.x * (NCONS * 32);
+        for (uint32_t kk = 0; kk < p.n_comp; ++kk) {
+            const CompDesc& K = p.comp[kk];
+            if (K.skip) continue;
+            const int64_t lo = K.n_tiles * (int64_t)K.T;
+            const int64_t n_tail = p.n_records - lo;
+            if (n_tail <= 0) continue;
+            const int64_t total = n_tail * (int64_t)(K.f_hi - K.f_lo);
+            for (int64_t x0 = gid; x0 < total; x0 += 4 * gstride) {
+                const U* sp[4];
+                U* dp[4];
+                uint32_t nu[4];
+#pragma unroll
+                for (int m = 0; m < 4; ++m) {
+                    const int64_t x = x0 + m * gstride;
+                    nu[m] = 0;
+                    if (x < total) {
+                        const uint32_t f = K.f_lo + (uint32_t)(x / n_tail);
+                        const int64_t r = lo + (x % n_tail);
+                        const FieldDesc fd = et.fields[f];
+                        sp[m] = (const U*)(p.src + p.srcc[fd.sc].region + (uint64_t)r * p.srcc[fd.sc].stride + fd.soff);
+                        dp[m] = (U*)(p.dst + p.dstc[fd.dc].region + (uint64_t)r * p.dstc[fd.dc].stride + fd.doff);
+                        nu[m] = fd.width / (uint32_t)sizeof(U);
+                    }
+                }
+                const uint32_t mx = max(max(nu[0], nu[1]), max(nu[2], nu[3]));
+                for (uint32_t j = 0; j < mx; ++j) {
+                    U v[4];
+#pragma unroll
+                    for (int m = 0; m < 4; ++m)
+                        if (j < nu[m]) v[m] = sp[m][j];
+#pragma unroll
+                    for (int m = 0; m < 4; ++m)
+                        if (j < nu[m]) dp[m][j] = v[m];
+                }
+            }
+        }
+    }
+
     int k_cur = -1;
     uint32_t stage = 0, phase = 0, oslot = 0, k = 0;
     for (int64_t t = t_first(p), te = t_end(p); t < te; t += t_step(p)) {
@@ -279,25 +325,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         if (++stage == p.s_in) { stage = 0; phase ^= 1; }
     }
 
-    // ---------------------------------------------------------------- tails: records [n_tiles*T, N)
-    for (uint32_t kk = 0; kk < p.n_comp; ++kk) {
-        if (gridDim.x - 1 - (kk % gridDim.x) != blockIdx.x) continue;
-        const CompDesc& K = p.comp[kk];
-        if (K.skip) continue;
-        const int64_t lo = K.n_tiles * (int64_t)K.T;
-        const int64_t n_tail = p.n_records - lo;
-        if (n_tail <= 0) continue;
-        const int64_t total = n_tail * (int64_t)(K.f_hi - K.f_lo);
-        for (int64_t x = tid; x < total; x += NCONS * 32) {
-            const uint32_t f = K.f_lo + (uint32_t)(x / n_tail);
-            const int64_t r = lo + (x % n_tail);
-            const FieldDesc fd = et.fields[f];
-            const uint8_t* s = (const uint8_t*)(p.src + p.srcc[fd.sc].region + (uint64_t)r * p.srcc[fd.sc].stride + fd.soff);
-            uint8_t* d = (uint8_t*)(p.dst + p.dstc[fd.dc].region + (uint64_t)r * p.dstc[fd.dc].stride + fd.doff);
-            for (uint32_t j = 0; j < fd.width; j += sizeof(U))
-                *reinterpret_cast<U*>(d + j) = *reinterpret_cast<const U*>(s + j);
-        }
-    }
 }
 
 template <int NF>

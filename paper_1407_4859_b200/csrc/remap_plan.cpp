@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <climits>
 #include <cstring>
 #include <map>
 #include <numeric>
@@ -86,7 +87,18 @@ uint32_t call_tile(const RemapPlan& p, int k, int64_t n, int n_sm) {
         t = (t + 31) / 32 * 32;
         return (uint32_t)std::max<int64_t>(32, std::min<int64_t>(t, T));
     }
-    return T;
+    // Balance the last round: among T_max*3/4 .. T_max (multiples of 32) pick the tile size that
+    // minimises rounds * T (rounds = ceil(tiles / SMs)), i.e. the critical-path records per CTA.
+    const char* e = std::getenv("ADHA_BALANCE");
+    if (n_sm <= 0 || (e && *e == '0') || p.comps.size() != 1) return T;
+    uint32_t best = T;
+    int64_t best_cost = INT64_MAX;
+    for (int64_t t = T; t >= std::max<int64_t>(32, (int64_t)T * 3 / 4); t -= 32) {
+        const int64_t tiles = n / t, rounds = (tiles + n_sm - 1) / n_sm;
+        const int64_t cost = rounds * t;
+        if (cost < best_cost) { best_cost = cost; best = (uint32_t)t; }
+    }
+    return best;
 }
 
 RemapPlan compile_plan(const Layout& ls, const Layout& ld) {
