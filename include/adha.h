@@ -259,6 +259,32 @@ ADHA_API adha_status adha_plan_ods(const char* program_json, const char* arch_js
 ADHA_API adha_status adha_plan_pdl(const char* program_json, const char* arch_json,
                           const char* profile_json, char** plan_out);
 
+/* The run graph's nodes ([OP] build_run_graph): every contiguous run of
+ * sections x every device allowed by all its members, with the run's layout (ODS of the
+ * merged run) and its execution estimate under `profile_json` (nullable).
+ * *runs_out = {"runs":[{"begin","end","sections","device","layout","exec_ns"}]} (adha_free).
+ * Used to know which (section, device, layout) triples a tuning profile must cover
+ * (PAPER.md:59-60).  Errors: PARSE, PLANNER, CAPACITY. */
+ADHA_API adha_status adha_plan_candidates(const char* program_json, const char* arch_json,
+                                          const char* profile_json, char** runs_out);
+
+/* ------------------------------------------------------------------ synthetic consumer sections
+ *
+ * A section kernel reading records THROUGH a layout, for measuring a B200 tuning profile
+ * ("we provide a tuning profile of the execution times").
+ * For i in [0, n_out): r = idx ? idx[i] : i;  out[i] = sum over the listed fields f of x_f(r)^2,
+ * fields read as fp32 (width 4, 4-byte aligned in the layout) and summed in list order with
+ * fused multiply-add.  idx == NULL is a streaming pass over records 0..n_out-1 (a vectorizable
+ * section); idx != NULL is an irregular gather (heavy control flow).
+ *   buf        DEVICE buffer holding n_records records in `layout` (256-byte aligned)
+ *   fields     host array of n_fields_used field indices (1..32)
+ *   idx        DEVICE array of n_out record indices in [0, n_records), or NULL
+ *   out        DEVICE float array of n_out
+ * Asynchronous on `stream`.  Errors: INVALID_ARG, UNSUPPORTED (field not fp32-addressable), CUDA. */
+ADHA_API adha_status adha_section_run(const void* buf, const adha_layout* layout, int64_t n_records,
+                                      const int32_t* fields, int32_t n_fields_used, const int64_t* idx,
+                                      int64_t n_out, float* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -59,6 +59,8 @@ _SIGS = {
     "adha_remap_plan_describe": (ctypes.c_int, [_L, _L, ctypes.POINTER(_vp)]),
     "adha_plan_ods": (ctypes.c_int, [_cp, _cp, _cp, _cp, ctypes.POINTER(_vp)]),
     "adha_plan_pdl": (ctypes.c_int, [_cp, _cp, _cp, ctypes.POINTER(_vp)]),
+    "adha_plan_candidates": (ctypes.c_int, [_cp, _cp, _cp, ctypes.POINTER(_vp)]),
+    "adha_section_run": (ctypes.c_int, [_vp, _L, _i64, ctypes.POINTER(_i32), _i32, _vp, _i64, _vp, _vp]),
 }
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -324,6 +326,24 @@ def plan_pdl(program, arch, profile=None) -> dict:
     return json.loads(_take_string(p))
 
 
+def plan_candidates(program, arch, profile=None) -> dict:
+    """The run graph's nodes (adha_plan_candidates): every contiguous run x device with its ODS
+    layout and execution estimate -- the (section, device, layout) triples a profile must cover."""
+    p = _vp()
+    _check(_lib.adha_plan_candidates(_js(program), _js(arch), None if profile is None else _js(profile),
+                                     ctypes.byref(p)))
+    return json.loads(_take_string(p))
+
+
+def section_run(buf, layout: Layout, n_records: int, fields: Sequence[int], out, idx=None, n_out=None,
+                stream=None) -> None:
+    """Synthetic consumer section (adha_section_run): out[i] = sum_f x_f(r_i)^2 over the listed fp32
+    fields, r_i = idx[i] (irregular gather) or i (streaming pass)."""
+    n_out = int(n_out if n_out is not None else (idx.numel() if idx is not None else n_records))
+    _check(_lib.adha_section_run(_ptr(buf), layout.handle, int(n_records), _i32a(fields), len(fields),
+                                 _ptr(idx), n_out, _ptr(out), _stream(stream)))
+
+
 def plan_layouts(plan: dict, field_names: Sequence[str], widths: Sequence[int]) -> List[Layout]:
     """One Layout per run of a PDL plan (adha_plan_pdl output), in execution order.  Consecutive
     runs with different layouts are the plan's remap edges."""
@@ -343,5 +363,6 @@ def run_plan_remaps(plan: dict, field_names: Sequence[str], widths: Sequence[int
     return lays
 
 
-__all__ = ["Layout", "AdhaError", "remap", "remap_regions", "remap_chain", "plan_layouts", "run_plan_remaps", "shard_range", "remap_sharded", "remap_host",
+__all__ = ["Layout", "AdhaError", "remap", "remap_regions", "remap_chain", "plan_layouts", "run_plan_remaps",
+           "plan_candidates", "section_run", "shard_range", "remap_sharded", "remap_host",
            "plan_describe", "plan_ods", "plan_pdl", "version", "LIB_PATH"]

@@ -410,7 +410,8 @@ static bool path_less(const std::vector<Run>& R, const Path& x, const Path& y) {
     return false;
 }
 
-static std::string plan_pdl(const Program& p, const Arch& a, const Profile& prof) {
+// the run graph's nodes: every contiguous run x every device allowed by all members
+static std::vector<Run> run_nodes(const Program& p, const Arch& a, const Profile& prof) {
     const int k = (int)p.order.size();
     if (k == 0) throw PlanError(ADHA_ERR_PLANNER, "program has no sections");
     for (auto& s : p.sections)
@@ -423,6 +424,29 @@ static std::string plan_pdl(const Program& p, const Arch& a, const Profile& prof
                 for (int i = b; i <= e; ++i) ok = ok && allowed(p.sections[p.order[i]], d.name);
                 if (ok) R.push_back(make_run(p, a, b, e, d, prof));
             }
+    return R;
+}
+
+static std::string candidates_json(const Program& p, const Arch& a, const Profile& prof) {
+    std::vector<Run> R = run_nodes(p, a, prof);
+    std::string out = "{\"schema_version\":1,\"runs\":[";
+    for (size_t r = 0; r < R.size(); ++r) {
+        const Run& x = R[r];
+        if (r) out += ',';
+        out += "{\"begin\":" + std::to_string(x.begin) + ",\"end\":" + std::to_string(x.end) + ",\"sections\":[";
+        for (int i = x.begin; i <= x.end; ++i) {
+            if (i > x.begin) out += ',';
+            out += json::quote(p.sections[p.order[i]].id);
+        }
+        out += "],\"device\":" + json::quote(x.device) + ",\"layout\":" + json::quote(lstring(p, x.layout)) +
+               ",\"exec_ns\":" + json::number(x.exec_ns) + "}";
+    }
+    return out + "]}";
+}
+
+static std::string plan_pdl(const Program& p, const Arch& a, const Profile& prof) {
+    const int k = (int)p.order.size();
+    std::vector<Run> R = run_nodes(p, a, prof);
     std::vector<int> order(R.size());
     for (size_t i = 0; i < R.size(); ++i) order[i] = (int)i;
     std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
@@ -535,6 +559,26 @@ extern "C" adha_status adha_plan_pdl(const char* program_json, const char* arch_
         Profile pr = parse_profile(profile_json);
         *plan_out = dup(plan_pdl(p, a, pr));
         if (!*plan_out) return fail(ADHA_ERR_OOM, "out of host memory");
+        return ADHA_OK;
+    } catch (const json::ParseError& e) {
+        return fail(ADHA_ERR_PARSE, e.what());
+    } catch (const PlanError& e) {
+        return fail(e.code, e.what());
+    } catch (const std::bad_alloc&) {
+        return fail(ADHA_ERR_OOM, "out of host memory");
+    }
+}
+
+extern "C" adha_status adha_plan_candidates(const char* program_json, const char* arch_json, const char* profile_json,
+                                            char** runs_out) {
+    clear_error();
+    if (!program_json || !arch_json || !runs_out) return fail(ADHA_ERR_INVALID_ARG, "null argument");
+    try {
+        Program p = parse_program(program_json);
+        Arch a = parse_arch(arch_json);
+        Profile pr = parse_profile(profile_json);
+        *runs_out = dup(candidates_json(p, a, pr));
+        if (!*runs_out) return fail(ADHA_ERR_OOM, "out of host memory");
         return ADHA_OK;
     } catch (const json::ParseError& e) {
         return fail(ADHA_ERR_PARSE, e.what());

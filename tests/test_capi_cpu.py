@@ -309,3 +309,29 @@ def test_plan_layouts_follow_the_plan(expected):
              if {g for g in range(9) if a.cluster_of[g] == a.cluster_of[f]} !=
                 {g for g in range(9) if b.cluster_of[g] == b.cluster_of[f]}]
     assert moved == expected["medical_plan"]["remap_moved"]
+
+
+def test_plan_candidates_match_oracle_run_graph():
+    """adha_plan_candidates = the oracle's build_run_graph nodes: same runs, devices,
+    layouts, exec estimates."""
+    from tests.test_oracle_planner import random_program, random_arch
+    cases = [(golden("medical_program.json"), golden("medical_arch.json"), golden("medical_profile.json"))]
+    rng = random.Random(77)
+    for _ in range(40):
+        p, a = random_program(rng), random_arch(rng)
+        cases.append((json.loads(_prog_json(p)), json.loads(_arch_json(a)), None))
+    for prog, arch, prof in cases:
+        p, a = P.program_from_json(prog), P.arch_from_json(arch)
+        pr = P.profile_from_json(prof) if prof else None
+        try:
+            exp = P.build_run_graph(p, a, pr)
+        except P.PlannerError:
+            with pytest.raises(A.AdhaError):
+                A.plan_candidates(prog, arch, prof)
+            continue
+        got = A.plan_candidates(prog, arch, prof)["runs"]
+        assert len(got) == len(exp)
+        for g, e in zip(got, exp):
+            assert (g["begin"], g["end"], g["device"], g["layout"]) == (e.begin, e.end, e.device, P.layout_string(e.layout))
+            assert g["exec_ns"] == pytest.approx(e.exec_ns, rel=1e-12)
+    assert len(A.plan_candidates(golden("medical_program.json"), golden("medical_arch.json"))["runs"]) == 56

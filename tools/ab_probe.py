@@ -36,6 +36,15 @@ def timed(fn, reps=10):
     return 2 * N * R / (e0.elapsed_time(e1) / reps) / 1e6
 
 
+import time
+soak = float(os.environ.get("SOAK_S", "0"))
+if soak > 0:                                       # sustained load first: power cap / clocks settle
+    Ls0, Ld0 = A.Layout(w, [0] * 16), A.Layout(w, list(range(16)))
+    t_end = time.time() + soak
+    while time.time() < t_end:
+        for _ in range(20):
+            A.remap(a, Ls0, b, Ld0, N)
+        torch.cuda.synchronize()
 res = {}
 copy = []
 for rnd in range(5):
