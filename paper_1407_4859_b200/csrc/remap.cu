@@ -31,6 +31,7 @@
 #include <set>
 #include <string>
 #include <tuple>
+#include <type_traits>
 
 #include "internal.h"
 #include "ptx.cuh"
@@ -108,9 +109,14 @@ __device__ __forceinline__ int64_t t_step(const TiledParams& p) { return p.block
 // 9 warps per CTA: the register file is split over the 4 SM sub-partitions (16K registers
 // each) and one of them holds 3 warps, so a thread may use at most 16384 / 96 = 168 registers;
 // __launch_bounds__(NTHREADS, 1) gives ptxas exactly that budget.
-template <typename U, int NENT, int EMAX>
+template <int NENT, int NG>
+using TableOf = typename std::conditional<(NG > 0), GroupTable<NG>, EntryTable<NENT>>::type;
+
+// NG = 0: unit mode (EntryTable<NENT>, EMAX instructions per warp); NG > 0: byte-group mode
+// (GroupTable<NG>, GMAX slots per warp, U = uint8_t for the tails).
+template <typename U, int NENT, int EMAX, int NG = 0, int GMAX = 1>
 __global__ void __launch_bounds__(NTHREADS, 1)
-    remap_tiled_kernel(const __grid_constant__ TiledParams p, const __grid_constant__ EntryTable<NENT> et) {
+    remap_tiled_kernel(const __grid_constant__ TiledParams p, const __grid_constant__ TableOf<NENT, NG> et) {
     extern __shared__ __align__(1024) uint8_t smem[];
     const uint32_t warp = threadIdx.x >> 5;
     const uint32_t lane = threadIdx.x & 31;
@@ -197,6 +203,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const uint32_t tid = threadIdx.x;
     const uint64_t spol = policy_evict_first();
     uint32_t ioff[EMAX], ooff[EMAX], din[EMAX], dout[EMAX];
+    // byte-group mode: per slot j, source words m and output words o of this lane's group
+    uint32_t gsrc[GMAX][4], gsst[GMAX][4], gout[GMAX][4], gost[GMAX][4], gsel[GMAX][4][2];
+    uint32_t gns[GMAX], gno[GMAX], grho[GMAX], gP = 1;
     uint64_t gofs[VMAX];
     uint32_t gstep[VMAX];
     uint32_t ne = 0, nv = 0;
@@ -256,6 +265,40 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             // this warp's instructions of component k: i = warp + NCONS*e; lane's unit = entry i*32 + lane
             k_cur = (int)k;
             nv = copy_plan(p, p.comp[k].dc_lo, T, p.comp[k].tile_bytes, tid, gofs, gstep);
+            if constexpr (NG > 0) {
+                // G groups per period -> I instructions of 32 lanes; with I < NCONS the periods are
+                // split over P = NCONS / I warps per instruction (slot s -> instruction s % I,
+                // periods q = s / I (mod P))
+                const uint32_t G = p.comp[k].n_instr;
+                const uint32_t I = (G + 31) / 32;
+                gP = I ? max(1u, (uint32_t)NCONS / I) : 1u;
+#pragma unroll
+                for (int j = 0; j < GMAX; ++j) {
+                    gns[j] = gno[j] = 0;
+                    grho[j] = 0;
+                    const uint32_t slot = warp + NCONS * j;
+                    if (I && slot < I * gP) {
+                        const uint32_t i = slot % I, gi = i * 32 + lane;
+                        grho[j] = slot / I;
+                        if (gi < G) {
+                            const ByteGroup& gr = et.g[p.comp[k].instr_base + gi];
+                            gns[j] = gr.n_src;
+                            gno[j] = gr.n_out;
+#pragma unroll
+                            for (int m = 0; m < 4; ++m) {
+                                const ClusterDesc& cs = p.srcc[gr.src_sc[m]];
+                                const ClusterDesc& cd = p.dstc[gr.out_dc[m]];
+                                gsrc[j][m] = cs.smem + gr.src_off[m];
+                                gsst[j][m] = 32u * cs.stride;
+                                gout[j][m] = cd.smem + gr.out_off[m];
+                                gost[j][m] = 32u * cd.stride;
+                                gsel[j][m][0] = (uint32_t)gr.sel[m][0] | ((uint32_t)gr.sel[m][1] << 16);
+                                gsel[j][m][1] = gr.sel[m][2];
+                            }
+                        }
+                    }
+                }
+            } else {
             const uint32_t W = p.comp[k].n_instr;
             ne = W > warp ? (W - warp + NCONS - 1) / NCONS : 0;
 #pragma unroll
@@ -271,6 +314,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     din[e] = 32u * cs.stride;
                     dout[e] = 32u * cd.stride;
                 }
+            }
             }
         }
         mbar_wait(full0 + 8 * stage, phase);
@@ -293,6 +337,27 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     sts128(ob + v + 3 * NCONS * 32 * 16, a3);
                 }
                 for (; v < tb; v += NCONS * 32 * 16) sts128(ob + v, lds128(ib + v));
+            } else if constexpr (NG > 0) {
+                const uint32_t periods = T / 32;
+#pragma unroll
+                for (int j = 0; j < GMAX; ++j) {
+                    if (gno[j]) {
+                        for (uint32_t q = grho[j]; q < periods; q += gP) {
+                            uint32_t w[4];
+#pragma unroll
+                            for (int m = 0; m < 4; ++m)
+                                w[m] = ((uint32_t)m < gns[j]) ? lds<uint32_t>(ib + gsrc[j][m] + q * gsst[j][m]) : 0u;
+#pragma unroll
+                            for (int o = 0; o < 4; ++o) {
+                                if ((uint32_t)o < gno[j]) {
+                                    const uint32_t a = __byte_perm(w[0], w[1], gsel[j][o][0] & 0xFFFFu);
+                                    const uint32_t b = __byte_perm(w[2], w[3], gsel[j][o][0] >> 16);
+                                    sts(ob + gout[j][o] + q * gost[j][o], __byte_perm(a, b, gsel[j][o][1]));
+                                }
+                            }
+                        }
+                    }
+                }
             } else {
                 const uint32_t periods = T / 32;
 #pragma unroll
@@ -356,6 +421,9 @@ using namespace dev;
 
 static_assert(sizeof(dev::TiledParams) + sizeof(dev::EntryTable<dev::CLASS_NENT[3]>) <= 32764,
               "tiled kernel parameters exceed the 32764-byte kernel parameter limit");
+static_assert(sizeof(dev::TiledParams) + sizeof(dev::GroupTable<dev::GCLASS_NG[1]>) <= 32764,
+              "byte-group kernel parameters exceed the 32764-byte kernel parameter limit");
+static_assert(sizeof(dev::ByteGroup) == 52, "ByteGroup layout");
 static_assert(sizeof(dev::NaiveParams) <= 32764, "naive kernel parameters too large");
 
 namespace {
@@ -384,6 +452,23 @@ TiledLauncher pick_cls(int cls, const void** fn) {
         case 2: *fn = tiled_fn<U, 2>(); return &launch_tiled<U, 2>;
         default: *fn = tiled_fn<U, 3>(); return &launch_tiled<U, 3>;
     }
+}
+
+template <int GC>
+void launch_groups(dim3 grid, dim3 block, size_t smem, cudaStream_t st, const TiledParams& p, const void* table) {
+    constexpr int NG = GCLASS_NG[GC];
+    constexpr int GMAX = GCLASS_GMAX[GC];
+    remap_tiled_kernel<uint8_t, 32, 1, NG, GMAX><<<grid, block, smem, st>>>(p, *static_cast<const GroupTable<NG>*>(table));
+}
+template <int GC>
+const void* groups_fn() {
+    return (const void*)&remap_tiled_kernel<uint8_t, 32, 1, GCLASS_NG[GC], GCLASS_GMAX[GC]>;
+}
+
+TiledLauncher pick_groups(int gcls, const void** fn) {
+    if (gcls == 0) { *fn = groups_fn<0>(); return &launch_groups<0>; }
+    *fn = groups_fn<1>();
+    return &launch_groups<1>;
 }
 
 TiledLauncher pick(uint32_t unit, int cls, const void** fn) {
@@ -529,7 +614,8 @@ adha_status remap_checked(const uint8_t* src, const Layout& ls, uint8_t* dst, co
         return launch_naive(src, ls, ck.bs, dst, ld, ck.bd, 0, n, st);
 
     const void* fn = nullptr;
-    TiledLauncher launch = pick(plan->unit, plan->table_class, &fn);
+    TiledLauncher launch = plan->byte_groups ? pick_groups(plan->group_class, &fn)
+                                             : pick(plan->unit, plan->table_class, &fn);
     int n_sm = 0;
     adha_status s = device_setup(fn, &n_sm);
     if (s != ADHA_OK) return s;

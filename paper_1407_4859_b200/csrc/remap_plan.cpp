@@ -194,6 +194,136 @@ RemapPlan compile_plan(const Layout& ls, const Layout& ld) {
     P.stage_bytes = (uint32_t)stage;
     P.smem_bytes = HDR_BYTES + 128 + (s_in + S_OUT) * P.stage_bytes;
 
+    // ---- byte-group mode for unit sizes below 4 bytes (see ByteGroup in remap_plan.h)
+    const char* bg_env = std::getenv("ADHA_BYTE_GROUPS");
+    if (g < 4 && !(bg_env && *bg_env == '0')) {
+        struct OW {
+            uint16_t out;
+            uint8_t dc;
+            std::pair<int, uint32_t> src[4];   // (src cluster slot, aligned word offset) per output byte
+            uint8_t byte[4];
+            std::vector<std::pair<int, uint32_t>> set;   // distinct source words, sorted
+        };
+        std::vector<ByteGroup> groups;
+        std::vector<uint32_t> base(P.comps.size()), count(P.comps.size());
+        for (size_t ki = 0; ki < P.comps.size(); ++ki) {
+            auto& K = P.comps[ki];
+            base[ki] = (uint32_t)groups.size();
+            count[ki] = 0;
+            if (K.identity) continue;
+            // the output words of one 32-record period with the source word of each byte
+            std::vector<OW> ows;
+            for (int cd : K.dst_clusters) {
+                const uint32_t sd = (uint32_t)ld.stride[cd];
+                std::vector<int> field_at(sd, -1);
+                for (int f : ld.members[cd])
+                    for (uint32_t b = 0; b < ld.width[f]; ++b) field_at[ld.offset[f] + b] = f;
+                for (uint32_t w = 0; w < 8 * sd; ++w) {
+                    OW o;
+                    o.out = (uint16_t)(4 * w);
+                    o.dc = (uint8_t)P.dst_slot[cd];
+                    for (uint32_t j = 0; j < 4; ++j) {
+                        const uint32_t B = 4 * w + j, r = B / sd, b = B % sd;
+                        const int f = field_at[b];
+                        const int cs = ls.cluster[f];
+                        const uint64_t local = r * ls.stride[cs] + ls.offset[f] + (b - ld.offset[f]);
+                        o.src[j] = {P.src_slot[cs], (uint32_t)(local & ~uint64_t(3))};
+                        o.byte[j] = (uint8_t)(local & 3);
+                        if (std::find(o.set.begin(), o.set.end(), o.src[j]) == o.set.end()) o.set.push_back(o.src[j]);
+                    }
+                    std::sort(o.set.begin(), o.set.end());
+                    ows.push_back(o);
+                }
+            }
+            // greedy grouping: output words sorted by their first source word; a group takes up to
+            // 4 output words whose source words together are at most 4 (looked for in a window)
+            std::vector<uint32_t> ord(ows.size());
+            std::iota(ord.begin(), ord.end(), 0u);
+            std::stable_sort(ord.begin(), ord.end(), [&](uint32_t a, uint32_t b) { return ows[a].set < ows[b].set; });
+            std::vector<char> used(ows.size(), 0);
+            const size_t window = 256;
+            for (size_t a = 0; a < ord.size(); ++a) {
+                if (used[ord[a]]) continue;
+                std::vector<uint32_t> members = {ord[a]};
+                std::vector<std::pair<int, uint32_t>> uni = ows[ord[a]].set;
+                used[ord[a]] = 1;
+                for (size_t b = a + 1; b < ord.size() && b < a + window && members.size() < 4; ++b) {
+                    const OW& c = ows[ord[b]];
+                    if (used[ord[b]]) continue;
+                    std::vector<std::pair<int, uint32_t>> u2 = uni;
+                    for (auto& x : c.set)
+                        if (std::find(u2.begin(), u2.end(), x) == u2.end()) u2.push_back(x);
+                    if (u2.size() > 4) continue;
+                    uni = u2;
+                    members.push_back(ord[b]);
+                    used[ord[b]] = 1;
+                }
+                ByteGroup gr;
+                std::memset(&gr, 0, sizeof gr);
+                gr.n_src = (uint8_t)uni.size();
+                for (size_t m = 0; m < uni.size(); ++m) {
+                    gr.src_sc[m] = (uint8_t)uni[m].first;
+                    gr.src_off[m] = (uint16_t)uni[m].second;
+                }
+                gr.n_out = (uint8_t)members.size();
+                for (size_t o = 0; o < members.size(); ++o) {
+                    const OW& ow = ows[members[o]];
+                    gr.out_off[o] = ow.out;
+                    gr.out_dc[o] = ow.dc;
+                    uint32_t s0 = 0, s1 = 0, s2 = 0;
+                    for (uint32_t j = 0; j < 4; ++j) {
+                        const uint32_t m = (uint32_t)(std::find(uni.begin(), uni.end(), ow.src[j]) - uni.begin());
+                        const uint32_t by = ow.byte[j];
+                        s0 |= (m == 0 ? by : m == 1 ? 4 + by : 0) << (4 * j);
+                        s1 |= (m == 2 ? by : m == 3 ? 4 + by : 0) << (4 * j);
+                        s2 |= (m < 2 ? j : 4 + j) << (4 * j);
+                    }
+                    gr.sel[o][0] = (uint16_t)s0;
+                    gr.sel[o][1] = (uint16_t)s1;
+                    gr.sel[o][2] = (uint16_t)s2;
+                }
+                groups.push_back(gr);
+                ++count[ki];
+            }
+        }
+        // class: all groups fit, and every component's slots fit GMAX per warp
+        int gcls = -1;
+        for (int c = 0; c < 2 && gcls < 0; ++c) {
+            if (groups.size() > (size_t)GCLASS_NG[c]) continue;
+            bool fits = true;
+            for (size_t ki = 0; ki < P.comps.size(); ++ki) {
+                const uint32_t I = (count[ki] + 31) / 32;
+                if (!I) continue;
+                const uint32_t Pq = std::max<uint32_t>(1, NCONS / I);
+                fits = fits && (I * Pq + NCONS - 1) / NCONS <= (uint32_t)GCLASS_GMAX[c];
+            }
+            if (fits) gcls = c;
+        }
+        if (gcls >= 0) {
+            for (size_t ki = 0; ki < P.comps.size(); ++ki) {
+                P.comps[ki].instr_base = base[ki];
+                P.comps[ki].n_instr = count[ki];
+                P.comps[ki].n_groups = count[ki];
+            }
+            const int ng = GCLASS_NG[gcls];
+            const size_t bytes = sizeof(ByteGroup) * ng + sizeof(FieldDesc) * MAXF;
+            P.table.assign((bytes + 3) / 4, 0u);
+            uint8_t* img = reinterpret_cast<uint8_t*>(P.table.data());
+            std::memcpy(img, groups.data(), groups.size() * sizeof(ByteGroup));
+            FieldDesc* fd = reinterpret_cast<FieldDesc*>(img + sizeof(ByteGroup) * ng);
+            int fi = 0;
+            for (auto& K : P.comps)
+                for (int f : K.fields)
+                    fd[fi++] = {(uint16_t)P.src_slot[ls.cluster[f]], (uint16_t)P.dst_slot[ld.cluster[f]],
+                                ls.offset[f], ld.offset[f], ls.width[f]};
+            P.byte_groups = true;
+            P.group_class = gcls;
+            P.matched = false;
+            P.tiled = true;
+            return P;
+        }
+    }
+
     // instructions: 32 * W_k units per non-identity component
     uint64_t total_w = 0, max_w = 0;
     for (auto& K : P.comps) {
@@ -279,6 +409,7 @@ std::string describe_plan(const RemapPlan& p, const Layout& ls, const Layout& ld
     o += ",\"table_class\":" + std::to_string(p.table_class);
     o += ",\"table_entries\":" + std::to_string(dev::CLASS_NENT[p.table_class]);
     o += ",\"matched\":" + std::string(p.matched ? "true" : "false");
+    o += ",\"byte_groups\":" + std::string(p.byte_groups ? "true" : "false");
     auto arr = [](const std::vector<uint32_t>& v) {
         std::string s = "[";
         for (size_t i = 0; i < v.size(); ++i) s += (i ? "," : "") + std::to_string(v[i]);
@@ -312,6 +443,26 @@ std::string describe_plan(const RemapPlan& p, const Layout& ls, const Layout& ld
     }
     o += ",\"src_stride\":" + arr(sst) + ",\"dst_stride\":" + arr(dst);
     o += ",\"ent_in\":" + arr(ein) + ",\"ent_out\":" + arr(eout) + ",\"ent_sc\":" + arr(esc) + ",\"ent_dc\":" + arr(edc);
+    if (p.byte_groups) {
+        // [n_out, n_src, out_off x4, out_dc x4, src_off x4, src_sc x4, sel x12] per group
+        const int ng = dev::GCLASS_NG[p.group_class];
+        const dev::ByteGroup* gr = reinterpret_cast<const dev::ByteGroup*>(p.table.data());
+        uint32_t total = 0;
+        for (auto& K : p.comps) total = std::max(total, K.instr_base + K.n_groups);
+        o += ",\"group_class_size\":" + std::to_string(ng) + ",\"groups\":[";
+        for (uint32_t i = 0; i < total; ++i) {
+            const dev::ByteGroup& g = gr[i];
+            std::vector<uint32_t> v = {g.n_out, g.n_src};
+            for (int m = 0; m < 4; ++m) v.push_back(g.out_off[m]);
+            for (int m = 0; m < 4; ++m) v.push_back(g.out_dc[m]);
+            for (int m = 0; m < 4; ++m) v.push_back(g.src_off[m]);
+            for (int m = 0; m < 4; ++m) v.push_back(g.src_sc[m]);
+            for (int m = 0; m < 4; ++m)
+                for (int t = 0; t < 3; ++t) v.push_back(g.sel[m][t]);
+            o += (i ? "," : "") + arr(v);
+        }
+        o += "]";
+    }
     o += "}";
     return o;
 }

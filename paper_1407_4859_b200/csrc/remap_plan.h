@@ -65,8 +65,8 @@ struct CompDesc {
     uint16_t f_lo, f_hi;                   // field range in the field table
     uint16_t identity;
     uint16_t skip;        // 1: identity component whose dst region IS its src region (nothing moves)
-    uint32_t instr_base;  // first instruction of the component in the entry table
-    uint32_t n_instr;     // W_k = R_k / g
+    uint32_t instr_base;  // first instruction (unit mode) / first group (byte-group mode) in the table
+    uint32_t n_instr;     // unit mode: W_k = R_k / g; byte-group mode: groups per period
 };
 
 struct TiledParams {
@@ -97,6 +97,26 @@ struct EntryTable {
     uint8_t dc[NENT];     // dst cluster of the unit
     FieldDesc fields[MAXF];   // tail table, fields grouped by component
 };
+
+// Byte-group mode (g = 1 or 2 layouts): a lane builds up to 4 OUTPUT WORDS of one period from
+// up to 4 SOURCE WORDS with PRMT (byte permute) -- 4-byte shared loads/stores instead of one
+// shared instruction per byte.  Output words are grouped by identical source-word sets
+// (e.g. fields f..f+3 of records r..r+3 in a 1-byte AoS->SoA transpose share the same 4 words).
+struct ByteGroup {
+    uint16_t out_off[4];   // dst byte offset (multiple of 4) inside period 0 of the word's chunk
+    uint16_t src_off[4];   // src byte offset (multiple of 4) inside period 0 of the word's chunk
+    uint16_t sel[4][3];    // per output word: A = prmt(w0,w1,sel0), B = prmt(w2,w3,sel1), out = prmt(A,B,sel2)
+    uint8_t out_dc[4];     // dst cluster slot of each output word
+    uint8_t src_sc[4];     // src cluster slot of each source word
+    uint8_t n_out, n_src, pad0, pad1;
+};
+template <int NG>
+struct GroupTable {
+    ByteGroup g[NG];
+    FieldDesc fields[MAXF];
+};
+constexpr int GCLASS_NG[2] = {128, 384};
+constexpr int GCLASS_GMAX[2] = {1, 2};    // slots per warp: ceil(instructions * period-split / NCONS)
 
 // Table size classes (entries per warp EMAX = instructions per warp per component).
 constexpr int CLASS_NENT[4] = {512, 1024, 2048, 3552};
@@ -129,6 +149,7 @@ struct RemapPlan {
         uint32_t T_max = 0;           // records per tile at full size
         bool identity = false;
         uint32_t instr_base = 0, n_instr = 0;
+        uint32_t n_groups = 0;        // byte-group mode: groups of one period
     };
     bool tiled = false;
     std::string why_naive;            // reason when not tiled
@@ -137,6 +158,8 @@ struct RemapPlan {
     uint32_t smem_bytes = 0;
     int table_class = 0;
     bool matched = false;             // conflict-free matching used (g = 4)
+    bool byte_groups = false;         // g < 4: PRMT byte-group mode (GroupTable) instead of units
+    int group_class = 0;
     std::vector<Comp> comps;
     std::vector<int> src_order, dst_order;   // kernel cluster index -> canonical cluster
     std::vector<int> src_slot, dst_slot;     // canonical cluster -> kernel cluster index

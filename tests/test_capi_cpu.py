@@ -220,6 +220,9 @@ def _plan_checks(widths, ls, ld):
     Ls, Ld = A.Layout(widths, ls), A.Layout(widths, ld)
     d = A.plan_describe(Ls, Ld)
     assert d["tiled"], d["why_naive"]
+    if d["byte_groups"]:
+        _check_byte_groups(widths, ls, ld)
+        return d
     g = d["unit"]
     cs, cd = clusters_in_order(ls), clusters_in_order(ld)          # canonical clusters (field lists)
     csrc = {f: k for k, c in enumerate(cs) for f in c}
@@ -335,3 +338,81 @@ def test_plan_candidates_match_oracle_run_graph():
             assert (g["begin"], g["end"], g["device"], g["layout"]) == (e.begin, e.end, e.device, P.layout_string(e.layout))
             assert g["exec_ns"] == pytest.approx(e.exec_ns, rel=1e-12)
     assert len(A.plan_candidates(golden("medical_program.json"), golden("medical_arch.json"))["runs"]) == 56
+
+
+def _prmt(a, b, sel):
+    """__byte_perm semantics: bytes of {b:a} indexed 0..7, one selector nibble per result byte."""
+    src = [(a >> (8 * i)) & 0xFF for i in range(4)] + [(b >> (8 * i)) & 0xFF for i in range(4)]
+    return sum(src[(sel >> (4 * j)) & 7] << (8 * j) for j in range(4))
+
+
+def _check_byte_groups(widths, ls, ld):
+    """Simulate the byte-group plan of one 32-record period on the host: every dst byte must be
+    produced exactly once, from the src byte the oracle's record model names."""
+    from tests.test_oracle_remap import clusters_in_order
+    Ls, Ld = A.Layout(widths, ls), A.Layout(widths, ld)
+    d = A.plan_describe(Ls, Ld)
+    assert d["tiled"] and d["unit"] < 4 and d["byte_groups"], d
+    cs, cd = clusters_in_order(ls), clusters_in_order(ld)
+    csrc = {f: k for k, c in enumerate(cs) for f in c}
+    cdst = {f: k for k, c in enumerate(cd) for f in c}
+    _, ss, os_, _ = O.field_addresses(widths, ls, 32)
+    _, sd, od, _ = O.field_addresses(widths, ld, 32)
+    # a distinct value per src byte: (src cluster, local byte) -> tag
+    def tag(c, off):
+        return (c * 7919 + off * 131) & 0xFF
+    seen = {}
+    for K in d["components"]:
+        if K["identity"]:
+            continue
+        for gi in range(K["instr_base"], K["instr_base"] + K["n_instr"]):
+            g = d["groups"][gi]
+            n_out, n_src = g[0], g[1]
+            out_off, out_dc, src_off, src_sc, sel = g[2:6], g[6:10], g[10:14], g[14:18], g[18:30]
+            words = []
+            for m in range(4):
+                if m < n_src:
+                    c = d["src_order"][src_sc[m]]
+                    words.append(sum(tag(c, src_off[m] + j) << (8 * j) for j in range(4)))
+                else:
+                    words.append(0)
+            for o in range(n_out):
+                a = _prmt(words[0], words[1], sel[3 * o])
+                b = _prmt(words[2], words[3], sel[3 * o + 1])
+                v = _prmt(a, b, sel[3 * o + 2])
+                c = d["dst_order"][out_dc[o]]
+                for j in range(4):
+                    key = (c, out_off[o] + j)
+                    assert key not in seen
+                    seen[key] = (v >> (8 * j)) & 0xFF
+    # expected: every byte of every non-identity dst cluster in period 0
+    ident_dst = {K["dst_clusters"][0] for K in d["components"] if K["identity"]}     # canonical indices
+    count = 0
+    for f, w in enumerate(widths):
+        if cdst[f] in ident_dst:
+            continue
+        for r in range(32):
+            for j in range(w):
+                src_local = r * ss[f] + os_[f] + j
+                dst_local = r * sd[f] + od[f] + j
+                assert seen[(cdst[f], dst_local)] == tag(csrc[f], src_local), (f, r, j)
+                count += 1
+    assert count == len(seen)
+
+
+def test_byte_group_plans_cover_every_byte():
+    _check_byte_groups([1] * 24 + [8], [0] * 25, list(range(25)))          # 1-byte AoS -> SoA
+    _check_byte_groups([1] * 24 + [8], list(range(25)), [0] * 25)          # 1-byte SoA -> AoS
+    _check_byte_groups([2, 4, 6, 4] * 4, [0] * 16, list(range(16)))        # g = 2
+    _check_byte_groups([1, 3, 4, 8] * 4, [0] * 16, list(range(16)))        # odd widths
+    rng = random.Random(5)
+    for _ in range(30):
+        F = rng.randint(2, 10)
+        widths = [rng.choice([1, 2, 3, 4, 5, 8]) for _ in range(F)]
+        if all(w % 4 == 0 for w in widths):
+            widths[0] = 1
+        ls = [rng.randrange(F) for _ in range(F)]
+        ld = [rng.randrange(F) for _ in range(F)]
+        d = A.plan_describe(A.Layout(widths, ls), A.Layout(widths, ld))
+        if d["unit"] < 4 and d["byte_groups"]:
+            _check_byte_groups(widths, ls, ld)
