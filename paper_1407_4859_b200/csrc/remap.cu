@@ -67,7 +67,9 @@ __device__ __forceinline__ uint32_t copy_plan(const TiledParams& p, uint32_t c_l
                 cend = cbeg + T * p.dstc[c].stride;
             }
             gofs[u] = p.dstc[c].region + (b - cbeg);
-            gstep[u] = cend - cbeg;
+            // the per-tile step T*stride is a multiple of 128; its low 7 bits carry the chunk's
+            // padding in the output stage / 32 (smem offset - packed offset = 32 * chunk index)
+            gstep[u] = (cend - cbeg) | ((p.dstc[c].smem - cbeg) >> 5);
             nv = u + 1;
         }
     }
@@ -85,12 +87,13 @@ __device__ __forceinline__ void copy_out(uint8_t* dst, uint32_t sm_base, uint32_
             uint4 val[4];
 #pragma unroll
             for (uint32_t u = u0; u < u0 + 4 && u < VMAX; ++u)
-                if (u < nv) val[u - u0] = lds128(sm_base + tid * 16 + u * NT * 16);
+                if (u < nv) val[u - u0] = lds128(sm_base + tid * 16 + u * NT * 16 + ((gstep[u] & 127u) << 5));
 #pragma unroll
             for (uint32_t u = u0; u < u0 + 4 && u < VMAX; ++u)
                 if (u < nv) {
-                    if (HINT) stg128_hint(dst + gofs[u] + (uint64_t)lt * gstep[u], val[u - u0], pol);
-                    else stg128(dst + gofs[u] + (uint64_t)lt * gstep[u], val[u - u0]);
+                    const uint64_t step = gstep[u] & ~127u;
+                    if (HINT) stg128_hint(dst + gofs[u] + (uint64_t)lt * step, val[u - u0], pol);
+                    else stg128(dst + gofs[u] + (uint64_t)lt * step, val[u - u0]);
                 }
         }
     }
@@ -271,7 +274,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 // periods q = s / I (mod P))
                 const uint32_t G = p.comp[k].n_instr;
                 const uint32_t I = (G + 31) / 32;
-                gP = I ? max(1u, (uint32_t)NCONS / I) : 1u;
+                gP = I ? max(1u, (uint32_t)(NCONS * GMAX) / I) : 1u;
 #pragma unroll
                 for (int j = 0; j < GMAX; ++j) {
                     gns[j] = gno[j] = 0;
@@ -342,7 +345,28 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
                 for (int j = 0; j < GMAX; ++j) {
                     if (gno[j]) {
-                        for (uint32_t q = grho[j]; q < periods; q += gP) {
+                        uint32_t q = grho[j];
+                        // two periods per iteration: 8 independent shared loads in flight
+                        for (; q + gP < periods; q += 2 * gP) {
+                            uint32_t w[2][4];
+#pragma unroll
+                            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                                for (int m = 0; m < 4; ++m)
+                                    w[h][m] = ((uint32_t)m < gns[j])
+                                                  ? lds<uint32_t>(ib + gsrc[j][m] + (q + h * gP) * gsst[j][m]) : 0u;
+#pragma unroll
+                            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                                for (int o = 0; o < 4; ++o) {
+                                    if ((uint32_t)o < gno[j]) {
+                                        const uint32_t a = __byte_perm(w[h][0], w[h][1], gsel[j][o][0] & 0xFFFFu);
+                                        const uint32_t b = __byte_perm(w[h][2], w[h][3], gsel[j][o][0] >> 16);
+                                        sts(ob + gout[j][o] + (q + h * gP) * gost[j][o], __byte_perm(a, b, gsel[j][o][1]));
+                                    }
+                                }
+                        }
+                        for (; q < periods; q += gP) {
                             uint32_t w[4];
 #pragma unroll
                             for (int m = 0; m < 4; ++m)
@@ -653,17 +677,22 @@ adha_status remap_checked(const uint8_t* src, const Layout& ls, uint8_t* dst, co
         D.identity = K.identity ? 1 : 0;
         D.instr_base = K.instr_base;
         D.n_instr = K.n_instr;
+        // byte-group mode staggers chunk k of a component by 32*k bytes (cumulative: chunk k starts
+        // 32 bytes after the end of chunk k-1), so equal offsets in chunks k and k+1..k+3 fall in
+        // different banks (see remap_plan.cpp)
+        const bool stagger = plan->byte_groups;
         D.sc_lo = (uint16_t)sc;
-        uint32_t off = 0;
+        uint32_t off = 0, idx = 0;
         for (int c : K.src_clusters) {
-            P->srcc[sc++] = {ck.bs[c], (uint32_t)ls.stride[c], off};
+            P->srcc[sc++] = {ck.bs[c], (uint32_t)ls.stride[c], off + (stagger ? 32u * idx++ : 0u)};
             off += D.T * (uint32_t)ls.stride[c];
         }
         D.sc_hi = (uint16_t)sc;
         D.dc_lo = (uint16_t)dc;
         off = 0;
+        idx = 0;
         for (int c : K.dst_clusters) {
-            P->dstc[dc++] = {ck.bd[c], (uint32_t)ld.stride[c], off};
+            P->dstc[dc++] = {ck.bd[c], (uint32_t)ld.stride[c], off + (stagger ? 32u * idx++ : 0u)};
             off += D.T * (uint32_t)ld.stride[c];
         }
         D.dc_hi = (uint16_t)dc;

@@ -80,20 +80,60 @@ bool matched_order(const std::vector<Unit>& units, std::vector<uint32_t>& order)
 }
 }  // namespace
 
+// Reorder a byte group's slots: source word m moves to slot ps[m], output word o to slot po[o];
+// the PRMT selectors are re-encoded for the new source slots.
+static void permute_group(ByteGroup& g, const int ps[4], const int po[4]) {
+    ByteGroup h = g;
+    for (int m = 0; m < g.n_src; ++m) {
+        h.src_off[ps[m]] = g.src_off[m];
+        h.src_sc[ps[m]] = g.src_sc[m];
+    }
+    int inv[4] = {0, 1, 2, 3};
+    for (int m = 0; m < g.n_src; ++m) inv[m] = ps[m];
+    for (int o = 0; o < g.n_out; ++o) {
+        // decode (source slot, byte) of each output byte, then re-encode with the new slots
+        uint32_t s0 = 0, s1 = 0, s2 = 0;
+        for (uint32_t j = 0; j < 4; ++j) {
+            const uint32_t c = (g.sel[o][2] >> (4 * j)) & 7;
+            uint32_t m, by;
+            if (c < 4) {
+                const uint32_t a = (g.sel[o][0] >> (4 * j)) & 7;
+                m = a < 4 ? 0 : 1;
+                by = a & 3;
+            } else {
+                const uint32_t b = (g.sel[o][1] >> (4 * j)) & 7;
+                m = b < 4 ? 2 : 3;
+                by = b & 3;
+            }
+            m = (uint32_t)inv[m];
+            s0 |= (m == 0 ? by : m == 1 ? 4 + by : 0) << (4 * j);
+            s1 |= (m == 2 ? by : m == 3 ? 4 + by : 0) << (4 * j);
+            s2 |= (m < 2 ? j : 4 + j) << (4 * j);
+        }
+        h.out_off[po[o]] = g.out_off[o];
+        h.out_dc[po[o]] = g.out_dc[o];
+        h.sel[po[o]][0] = (uint16_t)s0;
+        h.sel[po[o]][1] = (uint16_t)s1;
+        h.sel[po[o]][2] = (uint16_t)s2;
+    }
+    g = h;
+}
+
 uint32_t call_tile(const RemapPlan& p, int k, int64_t n, int n_sm) {
     const uint32_t T = p.comps[k].T_max;
+    const int64_t qt = p.tile_quantum;              // 32 records (a period), 128 in byte-group mode
     if (n_sm > 0 && n < (int64_t)T * n_sm) {
         int64_t t = (n + n_sm - 1) / n_sm;
-        t = (t + 31) / 32 * 32;
-        return (uint32_t)std::max<int64_t>(32, std::min<int64_t>(t, T));
+        t = (t + qt - 1) / qt * qt;
+        return (uint32_t)std::max<int64_t>(qt, std::min<int64_t>(t, T));
     }
-    // Balance the last round: among T_max*3/4 .. T_max (multiples of 32) pick the tile size that
-    // minimises rounds * T (rounds = ceil(tiles / SMs)), i.e. the critical-path records per CTA.
+    // Balance the last round: among T_max*3/4 .. T_max (multiples of the quantum) pick the tile
+    // size that minimises rounds * T (rounds = ceil(tiles / SMs)), the critical-path records per CTA.
     const char* e = std::getenv("ADHA_BALANCE");
     if (n_sm <= 0 || (e && *e == '0') || p.comps.size() != 1) return T;
     uint32_t best = T;
     int64_t best_cost = INT64_MAX;
-    for (int64_t t = T; t >= std::max<int64_t>(32, (int64_t)T * 3 / 4); t -= 32) {
+    for (int64_t t = T; t >= std::max<int64_t>(qt, (int64_t)T * 3 / 4); t -= qt) {
         const int64_t tiles = n / t, rounds = (tiles + n_sm - 1) / n_sm;
         const int64_t cost = rounds * t;
         if (cost < best_cost) { best_cost = cost; best = (uint32_t)t; }
@@ -206,6 +246,15 @@ RemapPlan compile_plan(const Layout& ls, const Layout& ld) {
         };
         std::vector<ByteGroup> groups;
         std::vector<uint32_t> base(P.comps.size()), count(P.comps.size());
+        // chunk stagger (bytes) of every kernel cluster slot: 32 * (index in its component); only its
+        // value mod 128 matters for banks because chunk sizes T*stride are multiples of 128
+        std::vector<uint32_t> spad(P.src_order.size()), dpad(P.dst_order.size());
+        size_t max_chunks = 1;
+        for (auto& K : P.comps) {
+            for (size_t i = 0; i < K.src_clusters.size(); ++i) spad[P.src_slot[K.src_clusters[i]]] = 32 * i;
+            for (size_t i = 0; i < K.dst_clusters.size(); ++i) dpad[P.dst_slot[K.dst_clusters[i]]] = 32 * i;
+            max_chunks = std::max(max_chunks, std::max(K.src_clusters.size(), K.dst_clusters.size()));
+        }
         for (size_t ki = 0; ki < P.comps.size(); ++ki) {
             auto& K = P.comps[ki];
             base[ki] = (uint32_t)groups.size();
@@ -241,6 +290,7 @@ RemapPlan compile_plan(const Layout& ls, const Layout& ld) {
             std::iota(ord.begin(), ord.end(), 0u);
             std::stable_sort(ord.begin(), ord.end(), [&](uint32_t a, uint32_t b) { return ows[a].set < ows[b].set; });
             std::vector<char> used(ows.size(), 0);
+            std::vector<ByteGroup> comp_groups;
             const size_t window = 256;
             for (size_t a = 0; a < ord.size(); ++a) {
                 if (used[ord[a]]) continue;
@@ -282,9 +332,48 @@ RemapPlan compile_plan(const Layout& ls, const Layout& ld) {
                     gr.sel[o][1] = (uint16_t)s1;
                     gr.sel[o][2] = (uint16_t)s2;
                 }
-                groups.push_back(gr);
-                ++count[ki];
+                comp_groups.push_back(gr);
             }
+            // instruction order: fill each 32-lane instruction greedily with groups whose source
+            // words and output words can be put in slots (the m-th load / o-th store of all lanes)
+            // whose banks (period 0) are still unused in that instruction -- the slot order inside a
+            // group is free, so try every permutation of it
+            std::vector<char> taken(comp_groups.size(), 0);
+            size_t left = comp_groups.size();
+            while (left) {
+                uint32_t used_s[4] = {0, 0, 0, 0}, used_o[4] = {0, 0, 0, 0};
+                std::vector<size_t> pick;
+                for (size_t i = 0; i < comp_groups.size() && pick.size() < 32; ++i) {
+                    if (taken[i]) continue;
+                    ByteGroup& gr = comp_groups[i];
+                    int ps[4] = {0, 1, 2, 3}, po[4] = {0, 1, 2, 3};
+                    bool ok_s = false, ok_o = false;
+                    auto sbank = [&](const ByteGroup& x, int m) { return ((spad[x.src_sc[m]] + x.src_off[m]) / 4) % 32; };
+                    auto obank = [&](const ByteGroup& x, int o) { return ((dpad[x.out_dc[o]] + x.out_off[o]) / 4) % 32; };
+                    do {
+                        bool ok = true;
+                        for (int m = 0; m < gr.n_src && ok; ++m) ok = !(used_s[ps[m]] >> sbank(gr, m) & 1u);
+                        if (ok) { ok_s = true; break; }
+                    } while (std::next_permutation(ps, ps + gr.n_src));
+                    if (!ok_s) continue;
+                    do {
+                        bool ok = true;
+                        for (int o = 0; o < gr.n_out && ok; ++o) ok = !(used_o[po[o]] >> obank(gr, o) & 1u);
+                        if (ok) { ok_o = true; break; }
+                    } while (std::next_permutation(po, po + gr.n_out));
+                    if (!ok_o) continue;
+                    permute_group(gr, ps, po);
+                    for (int m = 0; m < gr.n_src; ++m) used_s[m] |= 1u << sbank(gr, m);
+                    for (int o = 0; o < gr.n_out; ++o) used_o[o] |= 1u << obank(gr, o);
+                    pick.push_back(i);
+                    taken[i] = 1;
+                }
+                for (size_t i = 0; i < comp_groups.size() && pick.size() < 32; ++i)
+                    if (!taken[i]) { pick.push_back(i); taken[i] = 1; }
+                for (size_t i : pick) groups.push_back(comp_groups[i]);
+                left -= pick.size();
+            }
+            count[ki] = (uint32_t)comp_groups.size();
         }
         // class: all groups fit, and every component's slots fit GMAX per warp
         int gcls = -1;
@@ -294,10 +383,26 @@ RemapPlan compile_plan(const Layout& ls, const Layout& ld) {
             for (size_t ki = 0; ki < P.comps.size(); ++ki) {
                 const uint32_t I = (count[ki] + 31) / 32;
                 if (!I) continue;
-                const uint32_t Pq = std::max<uint32_t>(1, NCONS / I);
+                const uint32_t Pq = std::max<uint32_t>(1, (uint32_t)(NCONS * GCLASS_GMAX[c]) / I);
                 fits = fits && (I * Pq + NCONS - 1) / NCONS <= (uint32_t)GCLASS_GMAX[c];
             }
             if (fits) gcls = c;
+        }
+        if (gcls >= 0) {
+            // chunk starts at multiples of 128 bytes keep each word's bank a function of its
+            // period-0 offset: tiles of 128-record multiples in byte-group mode
+            P.tile_quantum = 128;
+            uint64_t stage2 = 0;
+            for (auto& K : P.comps) {
+                K.T_max = std::max<uint32_t>(128, K.T_max / 128 * 128);
+                stage2 = std::max<uint64_t>(stage2, (uint64_t)K.T_max * K.R + 32 * max_chunks);   // + stagger
+            }
+            stage2 = (stage2 + 127) / 128 * 128;
+            if ((P.s_in + P.s_out) * stage2 > budget) gcls = -1;
+            else {
+                P.stage_bytes = (uint32_t)stage2;
+                P.smem_bytes = HDR_BYTES + 128 + (P.s_in + P.s_out) * P.stage_bytes;
+            }
         }
         if (gcls >= 0) {
             for (size_t ki = 0; ki < P.comps.size(); ++ki) {

@@ -159,6 +159,7 @@ struct RemapPlan {
     int table_class = 0;
     bool matched = false;             // conflict-free matching used (g = 4)
     bool byte_groups = false;         // g < 4: PRMT byte-group mode (GroupTable) instead of units
+    uint32_t tile_quantum = 32;       // tile sizes are multiples of this many records
     int group_class = 0;
     std::vector<Comp> comps;
     std::vector<int> src_order, dst_order;   // kernel cluster index -> canonical cluster
