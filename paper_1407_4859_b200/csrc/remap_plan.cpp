@@ -7,6 +7,7 @@
 #include "remap_plan.h"
 
 #include <algorithm>
+#include <array>
 #include <cstdlib>
 #include <climits>
 #include <cstring>
@@ -338,18 +339,18 @@ RemapPlan compile_plan(const Layout& ls, const Layout& ld) {
             // words and output words can be put in slots (the m-th load / o-th store of all lanes)
             // whose banks (period 0) are still unused in that instruction -- the slot order inside a
             // group is free, so try every permutation of it
-            std::vector<char> taken(comp_groups.size(), 0);
-            size_t left = comp_groups.size();
-            while (left) {
+            auto sbank = [&](const ByteGroup& x, int m) { return ((spad[x.src_sc[m]] + x.src_off[m]) / 4) % 32; };
+            auto obank = [&](const ByteGroup& x, int o) { return ((dpad[x.out_dc[o]] + x.out_off[o]) / 4) % 32; };
+            // one greedy pass over the remaining groups in `cand` order: picks conflict-free groups
+            // (with their slot permutations) until 32 or the candidates run out
+            auto greedy = [&](const std::vector<size_t>& cand, std::vector<size_t>& pick,
+                              std::vector<std::array<int, 8>>& perms) {
                 uint32_t used_s[4] = {0, 0, 0, 0}, used_o[4] = {0, 0, 0, 0};
-                std::vector<size_t> pick;
-                for (size_t i = 0; i < comp_groups.size() && pick.size() < 32; ++i) {
-                    if (taken[i]) continue;
-                    ByteGroup& gr = comp_groups[i];
+                for (size_t i : cand) {
+                    if (pick.size() == 32) break;
+                    const ByteGroup& gr = comp_groups[i];
                     int ps[4] = {0, 1, 2, 3}, po[4] = {0, 1, 2, 3};
                     bool ok_s = false, ok_o = false;
-                    auto sbank = [&](const ByteGroup& x, int m) { return ((spad[x.src_sc[m]] + x.src_off[m]) / 4) % 32; };
-                    auto obank = [&](const ByteGroup& x, int o) { return ((dpad[x.out_dc[o]] + x.out_off[o]) / 4) % 32; };
                     do {
                         bool ok = true;
                         for (int m = 0; m < gr.n_src && ok; ++m) ok = !(used_s[ps[m]] >> sbank(gr, m) & 1u);
@@ -362,16 +363,48 @@ RemapPlan compile_plan(const Layout& ls, const Layout& ld) {
                         if (ok) { ok_o = true; break; }
                     } while (std::next_permutation(po, po + gr.n_out));
                     if (!ok_o) continue;
-                    permute_group(gr, ps, po);
-                    for (int m = 0; m < gr.n_src; ++m) used_s[m] |= 1u << sbank(gr, m);
-                    for (int o = 0; o < gr.n_out; ++o) used_o[o] |= 1u << obank(gr, o);
+                    for (int m = 0; m < gr.n_src; ++m) used_s[ps[m]] |= 1u << sbank(gr, m);
+                    for (int o = 0; o < gr.n_out; ++o) used_o[po[o]] |= 1u << obank(gr, o);
                     pick.push_back(i);
-                    taken[i] = 1;
+                    perms.push_back({ps[0], ps[1], ps[2], ps[3], po[0], po[1], po[2], po[3]});
                 }
-                for (size_t i = 0; i < comp_groups.size() && pick.size() < 32; ++i)
-                    if (!taken[i]) { pick.push_back(i); taken[i] = 1; }
-                for (size_t i : pick) groups.push_back(comp_groups[i]);
-                left -= pick.size();
+            };
+            std::vector<char> taken(comp_groups.size(), 0);
+            size_t left = comp_groups.size();
+            uint64_t rng = 0x9E3779B97F4A7C15ull ^ (uint64_t)ki;
+            while (left) {
+                std::vector<size_t> remaining;
+                for (size_t i = 0; i < comp_groups.size(); ++i)
+                    if (!taken[i]) remaining.push_back(i);
+                // natural order first, then seeded shuffles; keep the largest conflict-free pick
+                std::vector<size_t> best_pick;
+                std::vector<std::array<int, 8>> best_perms;
+                std::vector<size_t> cand = remaining;
+                for (int attempt = 0; attempt < 24 && best_pick.size() < std::min<size_t>(32, remaining.size()); ++attempt) {
+                    if (attempt) {
+                        for (size_t i = cand.size(); i > 1; --i) {       // Fisher-Yates with splitmix64
+                            rng += 0x9E3779B97F4A7C15ull;
+                            uint64_t z = rng;
+                            z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+                            z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+                            z ^= z >> 31;
+                            std::swap(cand[i - 1], cand[z % i]);
+                        }
+                    }
+                    std::vector<size_t> pick;
+                    std::vector<std::array<int, 8>> perms;
+                    greedy(cand, pick, perms);
+                    if (pick.size() > best_pick.size()) { best_pick = pick; best_perms = perms; }
+                }
+                for (size_t t = 0; t < best_pick.size(); ++t) {
+                    const auto& pp = best_perms[t];
+                    permute_group(comp_groups[best_pick[t]], pp.data(), pp.data() + 4);
+                    taken[best_pick[t]] = 1;
+                }
+                for (size_t i : remaining)
+                    if (best_pick.size() < 32 && !taken[i]) { best_pick.push_back(i); taken[i] = 1; }
+                for (size_t i : best_pick) groups.push_back(comp_groups[i]);
+                left -= best_pick.size();
             }
             count[ki] = (uint32_t)comp_groups.size();
         }
