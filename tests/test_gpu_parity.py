@@ -361,3 +361,25 @@ def test_section_run_matches_numpy():
     with pytest.raises(A.AdhaError) as e:
         A.section_run(to_dev(np.zeros(1024, np.uint8)), A.Layout.aos([2, 2]), 10, [0], torch.empty(10, device="cuda"))
     assert e.value.name == "ADHA_ERR_UNSUPPORTED"
+
+
+@pytest.mark.parametrize("mode,pinned", [("auto", True), ("hybrid", True), ("zero", True), ("staged", True),
+                                         ("auto", False)])
+def test_remap_host_modes(mode, pinned, monkeypatch):
+    """adha_remap_host in every strategy (hybrid / zero-copy / staged; pageable memory falls back to
+    staged) equals the oracle, C3-like multi-region layouts included."""
+    monkeypatch.setenv("ADHA_HOST_MODE", mode)
+    monkeypatch.setenv("ADHA_HOST_CHUNK_BYTES", str(1 << 20))     # several chunks
+    for widths, ls, ld, n in [(config_widths(16), [0] * 16, list(range(16)), 300_001),
+                              (config_widths(64), list(range(64)), c3_labels(), 50_017),
+                              ([1, 3, 4, 8] * 4, list(range(16)), [0] * 16, 120_000)]:
+        La, Ld = A.Layout(widths, ls), A.Layout(widths, ld)
+        src_np = O.pack(field_columns(n, n, widths), widths, ls, n)
+        h_src = torch.from_numpy(src_np)
+        h_dst = torch.full((Ld.nbytes(n),), SENT, dtype=torch.uint8)
+        if pinned:
+            h_src, h_dst = h_src.pin_memory(), h_dst.pin_memory()
+        scratch = torch.empty(64 << 20, dtype=torch.uint8, device="cuda")
+        A.remap_host(h_src, La, h_dst, Ld, n, scratch)
+        torch.cuda.synchronize()
+        assert np.array_equal(h_dst.numpy(), oracle_dst(src_np, ls, ld, widths, n)), (mode, pinned, widths[:4])
