@@ -28,6 +28,11 @@ class _Addr(ctypes.Structure):
     _fields_ = [("base", ctypes.c_uint64), ("stride", ctypes.c_uint64), ("offset", ctypes.c_uint64)]
 
 
+class _AddrEx(ctypes.Structure):
+    _fields_ = [("base", ctypes.c_uint64), ("stride", ctypes.c_uint64), ("offset", ctypes.c_uint64),
+                ("block", ctypes.c_uint64), ("width", ctypes.c_uint64), ("region_bytes", ctypes.c_uint64)]
+
+
 def build(force: bool = False) -> str:
     """Compile the C oracle with plain gcc -O2 (building the checker is not using it)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
@@ -55,6 +60,12 @@ def lib():
         L.oracle_remap_threads.argtypes = [u8p, i32p, u8p, i32p, ctypes.c_int, u32p,
                                            ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int]
         L.oracle_remap_threads.restype = ctypes.c_int
+        L.oracle_field_addresses_ex.argtypes = [ctypes.c_int, u32p, i32p, i32p, ctypes.c_uint32, ctypes.c_int64,
+                                                ctypes.POINTER(_AddrEx), ctypes.POINTER(ctypes.c_uint64)]
+        L.oracle_field_addresses_ex.restype = ctypes.c_int
+        L.oracle_remap_ex.argtypes = [u8p, i32p, i32p, ctypes.c_uint32, u8p, i32p, i32p, ctypes.c_uint32,
+                                      ctypes.c_int, u32p, ctypes.c_int64]
+        L.oracle_remap_ex.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -152,3 +163,88 @@ def payload_mask(widths: Sequence[int], cluster_of: Sequence[int], n_records: in
         region = m[base[f]: base[f] + n_records * stride[f]].reshape(n_records, stride[f])
         region[:, offset[f]: offset[f] + w] = True
     return m
+
+
+# ----------------------------------------------------------------------------- generalised layouts
+# (natural alignment, AoSoA blocks; SURVEY.md 8(f) N4 -- see remap_oracle.c header)
+
+
+def _blocks(blocks, n_fields):
+    return _i32a_or_null(blocks, n_fields)
+
+
+def _i32a_or_null(xs, n):
+    if xs is None:
+        return None
+    assert len(xs) == n
+    return _i32(xs)
+
+
+def field_addresses_ex(widths, cluster_of, n_records, blocks=None, aligned=False):
+    """dict of per-field numpy arrays base/stride/offset/block/width/region_bytes, plus total."""
+    F = len(widths)
+    out = (_AddrEx * F)()
+    tot = ctypes.c_uint64(0)
+    rc = lib().oracle_field_addresses_ex(F, _u32(widths), _i32(cluster_of), _i32a_or_null(blocks, F),
+                                         1 if aligned else 0, int(n_records), out, ctypes.byref(tot))
+    if rc != 0:
+        raise ValueError("oracle_field_addresses_ex rejected the layout")
+    d = {k: np.array([getattr(out[f], k) for f in range(F)], dtype=np.int64)
+         for k in ("base", "stride", "offset", "block", "width", "region_bytes")}
+    d["total"] = int(tot.value)
+    return d
+
+
+def layout_bytes_ex(widths, cluster_of, n_records, blocks=None, aligned=False):
+    return field_addresses_ex(widths, cluster_of, n_records, blocks, aligned)["total"]
+
+
+def addr_ex(d, f, i):
+    """Element address of field f of record(s) i (numpy-vectorised over i)."""
+    B = int(d["block"][f])
+    return (int(d["base"][f]) + (i // B) * (B * int(d["stride"][f])) + int(d["offset"][f]) * B
+            + (i % B) * int(d["width"][f]))
+
+
+def remap_ex(src, src_cluster_of, dst, dst_cluster_of, widths, n_records, src_blocks=None, src_aligned=False,
+             dst_blocks=None, dst_aligned=False):
+    F = len(widths)
+    need_s = layout_bytes_ex(widths, src_cluster_of, n_records, src_blocks, src_aligned)
+    need_d = layout_bytes_ex(widths, dst_cluster_of, n_records, dst_blocks, dst_aligned)
+    if src.nbytes < need_s or dst.nbytes < need_d:
+        raise ValueError("buffer smaller than the layout")
+    if n_records == 0:
+        return
+    rc = lib().oracle_remap_ex(_ptr(src), _i32(src_cluster_of), _i32a_or_null(src_blocks, F), 1 if src_aligned else 0,
+                               _ptr(dst), _i32(dst_cluster_of), _i32a_or_null(dst_blocks, F), 1 if dst_aligned else 0,
+                               F, _u32(widths), int(n_records))
+    if rc != 0:
+        raise ValueError("oracle_remap_ex rejected its arguments")
+
+
+def pack_ex(columns, widths, cluster_of, n_records, blocks=None, aligned=False, fill=0xA5):
+    """Lay per-field columns out in a generalised layout: region bytes that are not payload are 0,
+    bytes between regions are `fill`."""
+    d = field_addresses_ex(widths, cluster_of, n_records, blocks, aligned)
+    buf = np.full(d["total"], fill, dtype=np.uint8)
+    for f in range(len(widths)):
+        buf[d["base"][f]: d["base"][f] + d["region_bytes"][f]] = 0
+    i = np.arange(n_records, dtype=np.int64)
+    for f, w in enumerate(widths):
+        if n_records == 0:
+            continue
+        a = addr_ex(d, f, i)
+        idx = (a[:, None] + np.arange(w, dtype=np.int64)[None, :]).reshape(-1)
+        buf[idx] = columns[f].reshape(-1)
+    return buf
+
+
+def unpack_ex(buf, widths, cluster_of, n_records, blocks=None, aligned=False):
+    d = field_addresses_ex(widths, cluster_of, n_records, blocks, aligned)
+    i = np.arange(n_records, dtype=np.int64)
+    cols = []
+    for f, w in enumerate(widths):
+        a = addr_ex(d, f, i)
+        idx = (a[:, None] + np.arange(w, dtype=np.int64)[None, :]).reshape(-1)
+        cols.append(buf[idx].reshape(n_records, w) if n_records else np.zeros((0, w), np.uint8))
+    return cols

@@ -23,6 +23,18 @@
  *     the buffer start (reading Q3);  bytes outside regions are never written;
  *   - the remap is a type-blind byte copy (reading Q6): NaN payloads survive.
  *
+ * Generalised layouts (beyond the paper, which "consider[s] only
+ * AoS and SoA"), in the *_ex functions:
+ *   - natural alignment (flags bit 0, C-struct rule): a field of width w starts at a
+ *     multiple of a(w) = the largest power of two dividing w, at most 8; the cluster
+ *     record stride is rounded up to the largest a(w) of its fields;
+ *   - AoSoA blocking: a cluster with block B (1, 2, 4, 8, 16 or 32) stores its records
+ *     in blocks of B, each field's B values contiguous inside the block:
+ *       addr(f, i) = base + (i / B) * (B * stride) + offset(f) * B + (i % B) * w_f ,
+ *     and its region holds ceil(N / B) whole blocks;
+ *   - every byte of a dst region that is not a field byte of a record < N (alignment
+ *     padding, slots past N in the last block) is written 0.
+ *
  * Everything is a plain loop of memcpy, in the order of the definition.
  */
 #include <stdint.h>
@@ -189,5 +201,101 @@ int oracle_remap_threads(const uint8_t* src, const int32_t* src_cluster_of,
     }
     free(jobs);
     free(th);
+    return rc;
+}
+
+/* ------------------------------------------------------------------ generalised layouts */
+
+typedef struct {
+    uint64_t base, stride, offset, block, width, region_bytes;
+} oracle_addr_ex;
+
+static uint64_t natural_align(uint64_t w)
+{
+    uint64_t a = 1;
+    while (a < 8 && w % (a * 2) == 0) a *= 2;
+    return a;
+}
+
+/*
+ * Generalised addresses.  block_of[f] (NULL = all 1) must be equal for the fields of one
+ * cluster; flags bit 0 = natural alignment.  Returns ORACLE_BAD on invalid input.
+ */
+int oracle_field_addresses_ex(int n_fields, const uint32_t* widths, const int32_t* cluster_of,
+                              const int32_t* block_of, uint32_t flags, int64_t n_records,
+                              oracle_addr_ex* addr, uint64_t* total_bytes)
+{
+    if (n_fields <= 0 || n_records < 0 || !widths || !cluster_of || !addr) return ORACLE_BAD;
+    int32_t* canon = (int32_t*)malloc(sizeof(int32_t) * (size_t)n_fields);
+    if (!canon) return ORACLE_BAD;
+    int n_clusters = canonical_clusters(n_fields, cluster_of, canon);
+    uint64_t base = 0;
+    int rc = ORACLE_OK;
+    for (int c = 0; c < n_clusters && rc == ORACLE_OK; ++c) {
+        uint64_t run = 0, maxa = 1, blk = 0;
+        for (int f = 0; f < n_fields; ++f) {
+            if (canon[f] != c) continue;
+            uint64_t b = block_of ? (uint64_t)block_of[f] : 1;
+            if (blk == 0) blk = b;
+            if (b != blk || !(b == 1 || b == 2 || b == 4 || b == 8 || b == 16 || b == 32)) rc = ORACLE_BAD;
+            if (flags & 1u) {
+                uint64_t a = natural_align(widths[f]);
+                if (a > maxa) maxa = a;
+                run = (run + a - 1) / a * a;
+            }
+            addr[f].offset = run;
+            addr[f].width = widths[f];
+            run += widths[f];
+        }
+        uint64_t stride = (run + maxa - 1) / maxa * maxa;
+        uint64_t nblocks = ((uint64_t)n_records + blk - 1) / blk;
+        if (c > 0) base = align_up_256(base);
+        for (int f = 0; f < n_fields; ++f) {
+            if (canon[f] != c) continue;
+            addr[f].base = base;
+            addr[f].stride = stride;
+            addr[f].block = blk;
+            addr[f].region_bytes = nblocks * blk * stride;
+        }
+        base += nblocks * blk * stride;
+    }
+    if (total_bytes) *total_bytes = base;
+    free(canon);
+    return rc;
+}
+
+static uint64_t addr_ex(const oracle_addr_ex* a, uint64_t i)
+{
+    return a->base + (i / a->block) * (a->block * a->stride) + a->offset * a->block + (i % a->block) * a->width;
+}
+
+/*
+ * Generalised remap of records [lo, hi): dst regions of the records' blocks are first set to
+ * zero (all of them when lo == 0 and hi == N), then every field byte is copied.
+ */
+int oracle_remap_ex(const uint8_t* src, const int32_t* src_cluster_of, const int32_t* src_block_of,
+                    uint32_t src_flags, uint8_t* dst, const int32_t* dst_cluster_of,
+                    const int32_t* dst_block_of, uint32_t dst_flags, int n_fields, const uint32_t* widths,
+                    int64_t n_records)
+{
+    if (!src || !dst) return ORACLE_BAD;
+    oracle_addr_ex* as = (oracle_addr_ex*)malloc(sizeof(oracle_addr_ex) * (size_t)n_fields);
+    oracle_addr_ex* ad = (oracle_addr_ex*)malloc(sizeof(oracle_addr_ex) * (size_t)n_fields);
+    int rc = ORACLE_BAD;
+    if (as && ad &&
+        oracle_field_addresses_ex(n_fields, widths, src_cluster_of, src_block_of, src_flags, n_records, as, NULL) ==
+            ORACLE_OK &&
+        oracle_field_addresses_ex(n_fields, widths, dst_cluster_of, dst_block_of, dst_flags, n_records, ad, NULL) ==
+            ORACLE_OK) {
+        /* 1. every byte of every dst region := 0 */
+        for (int f = 0; f < n_fields; ++f) memset(dst + ad[f].base, 0, ad[f].region_bytes);
+        /* 2. the field bytes of every record */
+        for (int64_t i = 0; i < n_records; ++i)
+            for (int f = 0; f < n_fields; ++f)
+                memcpy(dst + addr_ex(&ad[f], (uint64_t)i), src + addr_ex(&as[f], (uint64_t)i), widths[f]);
+        rc = ORACLE_OK;
+    }
+    free(as);
+    free(ad);
     return rc;
 }

@@ -235,3 +235,97 @@ def test_brute_force_all_layout_pairs_5_fields(n):
 def test_rejects_bad_arguments():
     with pytest.raises(ValueError):
         O.remap(np.zeros(4, np.uint8), [0, 0], np.zeros(100, np.uint8), [0, 1], [4, 4], 10)
+
+
+# ----------------------------------------------------------------------------- generalised layouts (N4)
+
+def _np_base(w):
+    """numpy element type for a w-byte field: the largest power of two dividing w (<= 8) as an
+    unsigned integer, repeated -- numpy's align=True then applies the C-struct rule."""
+    a = 1
+    while a < 8 and w % (a * 2) == 0:
+        a *= 2
+    t = {1: "u1", 2: "u2", 4: "u4", 8: "u8"}[a]
+    return (t, (w // a,)) if w // a > 1 else t
+
+
+def test_aligned_records_are_numpy_align_true_structs():
+    """Natural alignment == numpy's align=True struct layout (offsets, itemsize) -- the C rule."""
+    rng = np.random.default_rng(21)
+    for trial in range(40):
+        F = int(rng.integers(1, 8))
+        widths = [int(x) for x in rng.choice([1, 2, 3, 4, 6, 8, 12, 16], size=F)]
+        labels = [0] * F
+        d = O.field_addresses_ex(widths, labels, 5, aligned=True)
+        dt = np.dtype([(f"f{f}", _np_base(w)) for f, w in enumerate(widths)], align=True)
+        assert int(d["stride"][0]) == dt.itemsize, (widths, dt)
+        for f in range(F):
+            assert int(d["offset"][f]) == dt.fields[f"f{f}"][1]
+        # remap aligned AoS -> SoA -> aligned AoS: padding comes back as zeros, payload intact
+        n = int(rng.integers(1, 300))
+        cols = field_columns(trial, n, widths)
+        src = np.zeros(n, dtype=dt)
+        for f, w in enumerate(widths):
+            src[f"f{f}"] = cols[f].reshape(n, w).view(dt.fields[f"f{f}"][0].base if dt.fields[f"f{f}"][0].shape
+                                                     else dt.fields[f"f{f}"][0]).reshape(src[f"f{f}"].shape)
+        src_b = src.view(np.uint8).copy()
+        assert np.array_equal(src_b, O.pack_ex(cols, widths, labels, n, aligned=True))
+        soa = np.full(O.layout_bytes_ex(widths, list(range(F)), n), SENT, np.uint8)
+        O.remap_ex(src_b, labels, soa, list(range(F)), widths, n, src_aligned=True)
+        back = np.full(src_b.size, SENT, np.uint8)
+        O.remap_ex(soa, list(range(F)), back, labels, widths, n, dst_aligned=True)
+        assert np.array_equal(back, src_b)
+
+
+def test_aosoa_is_a_blocked_transpose():
+    """AoSoA(B) of a uniform 4-byte record == reshape (N/B, B, F) -> transpose (0, 2, 1)."""
+    for F, B, n in [(3, 8, 64), (5, 4, 37), (16, 32, 100), (2, 2, 9)]:
+        widths = [4] * F
+        x = np.random.default_rng(F * B).integers(0, 2 ** 32, size=(n, F), dtype=np.uint32)
+        src = x.view(np.uint8).reshape(-1).copy()
+        dst = np.full(O.layout_bytes_ex(widths, [0] * F, n, blocks=[B] * F), SENT, np.uint8)
+        O.remap_ex(src, [0] * F, dst, [0] * F, widths, n, dst_blocks=[B] * F)
+        nb = -(-n // B)
+        pad = np.zeros((nb * B, F), np.uint32)
+        pad[:n] = x
+        exp = pad.reshape(nb, B, F).transpose(0, 2, 1).reshape(-1)
+        assert np.array_equal(dst.view(np.uint32), exp)          # slots past N are zero
+
+
+def test_generalised_round_trips_and_zero_fill():
+    rng = np.random.default_rng(8)
+    for trial in range(60):
+        F = int(rng.integers(1, 7))
+        widths = [int(x) for x in rng.choice([1, 2, 3, 4, 8], size=F)]
+        ls = [int(x) for x in rng.integers(0, F, size=F)]
+        ld = [int(x) for x in rng.integers(0, F, size=F)]
+        cl_s = {lab: int(rng.choice([1, 2, 4, 8, 32])) for lab in set(ls)}
+        cl_d = {lab: int(rng.choice([1, 2, 4, 8, 32])) for lab in set(ld)}
+        bs, bd = [cl_s[l] for l in ls], [cl_d[l] for l in ld]
+        als, ald = bool(rng.integers(2)), bool(rng.integers(2))
+        n = int(rng.integers(0, 200))
+        cols = field_columns(trial, n, widths)
+        src = O.pack_ex(cols, widths, ls, n, bs, als)
+        dst = np.full(O.layout_bytes_ex(widths, ld, n, bd, ald), SENT, np.uint8)
+        O.remap_ex(src, ls, dst, ld, widths, n, bs, als, bd, ald)
+        assert np.array_equal(dst, O.pack_ex(cols, widths, ld, n, bd, ald, fill=SENT))   # payload + zero padding
+        back = np.full(src.size, 0x77, np.uint8)
+        O.remap_ex(dst, ld, back, ls, widths, n, bd, ald, bs, als)
+        assert np.array_equal(back, O.pack_ex(cols, widths, ls, n, bs, als, fill=0x77))
+        for f, c in enumerate(O.unpack_ex(dst, widths, ld, n, bd, ald)):
+            assert np.array_equal(c, cols[f])
+
+
+def test_plain_layouts_unchanged_by_ex():
+    """With blocks of 1 and no alignment the generalised oracle is the plain one."""
+    widths = [1, 2, 3, 4, 8]
+    for ls in set_partitions(5)[::7]:
+        for ld in set_partitions(5)[::5]:
+            n = 23
+            cols = tagged_columns(n, widths)
+            src = O.pack(cols, widths, ls, n)
+            a = np.full(O.layout_bytes(widths, ld, n), SENT, np.uint8)
+            b = a.copy()
+            O.remap(src, ls, a, ld, widths, n)
+            O.remap_ex(src, ls, b, ld, widths, n)
+            assert np.array_equal(a, b)
