@@ -104,6 +104,25 @@ ADHA_API void adha_free(void* p);
 ADHA_API adha_status adha_layout_create(const uint32_t* field_widths, int32_t n_fields,
                                const int32_t* cluster_of_field, adha_layout** out);
 
+/* Layout flags for adha_layout_create_ex. */
+#define ADHA_LAYOUT_ALIGNED 1u     /* natural (C-struct) alignment inside cluster records */
+
+/* Generalised layouts (beyond the paper, which considers "only AoS and
+ * SoA"):
+ *   flags & ADHA_LAYOUT_ALIGNED: a field of width w starts at a multiple of a(w), the largest
+ *     power of two dividing w (at most 8); a cluster record's stride is rounded up to the
+ *     largest a(w) of its fields (the C struct rule);
+ *   block_of_field[f] (NULL = all 1): AoSoA block B in {1,2,4,8,16,32}, equal for the fields
+ *     of a cluster.  Records are stored in blocks of B, each field's B values contiguous:
+ *       addr(f, i) = base + (i / B) * (B * stride) + offset(f) * B + (i % B) * w_f,
+ *     and the region holds ceil(N / B) whole blocks.
+ * A remap writes 0 into every byte of a dst region that is not a field byte of a record < N
+ * (alignment padding, block slots past N).  Strings: "aligned:" prefix, "{a,b}@8" suffix.
+ * Errors: as adha_layout_create; INVALID_ARG for a bad block or unequal blocks in a cluster. */
+ADHA_API adha_status adha_layout_create_ex(const uint32_t* field_widths, int32_t n_fields,
+                                           const int32_t* cluster_of_field, const int32_t* block_of_field,
+                                           uint32_t flags, adha_layout** out);
+
 /* Create a layout from its string form.  Accepts the canonical form of
  * SPEC.md:79 "{f,g,h}|{x}|{y}" and the paper's Table-2 notation
  * "V1,V2,V3,{U1,U2,U3},S" where a bare name is a singleton.
@@ -136,6 +155,11 @@ ADHA_API adha_status adha_layout_bytes(const adha_layout* layout, int64_t n_reco
  * region_offset = base(cluster(f)), stride = stride(cluster(f)), offset = offset(f). */
 ADHA_API adha_status adha_layout_field_address(const adha_layout* layout, int32_t field, int64_t n_records,
                                       uint64_t* region_offset, uint32_t* stride, uint32_t* offset);
+
+/* As adha_layout_field_address, plus the cluster's AoSoA block (1 for plain records). */
+ADHA_API adha_status adha_layout_field_address_ex(const adha_layout* layout, int32_t field, int64_t n_records,
+                                                  uint64_t* region_offset, uint32_t* stride, uint32_t* offset,
+                                                  uint32_t* block);
 
 /* Destroy a handle.  NULL is ok. */
 ADHA_API void adha_layout_destroy(adha_layout* layout);

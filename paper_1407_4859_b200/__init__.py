@@ -39,6 +39,10 @@ _SIGS = {
     "adha_free": (None, [_vp]),
     "adha_layout_create": (ctypes.c_int, [ctypes.POINTER(ctypes.c_uint32), _i32, ctypes.POINTER(_i32),
                                           ctypes.POINTER(_L)]),
+    "adha_layout_create_ex": (ctypes.c_int, [ctypes.POINTER(ctypes.c_uint32), _i32, ctypes.POINTER(_i32),
+                                             ctypes.POINTER(_i32), ctypes.c_uint32, ctypes.POINTER(_L)]),
+    "adha_layout_field_address_ex": (ctypes.c_int, [_L, _i32, _i64, ctypes.POINTER(_u64), ctypes.POINTER(ctypes.c_uint32),
+                                                    ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_uint32)]),
     "adha_layout_from_string": (ctypes.c_int, [_cp, ctypes.POINTER(_cp), ctypes.POINTER(ctypes.c_uint32), _i32,
                                                ctypes.POINTER(_L)]),
     "adha_layout_to_string": (ctypes.c_int, [_L, ctypes.POINTER(_cp), ctypes.c_char_p, ctypes.c_size_t,
@@ -106,11 +110,23 @@ def _names(names):
 class Layout:
     """Immutable layout descriptor: field widths + a partition into clusters (adha.h)."""
 
-    def __init__(self, widths: Sequence[int], cluster_of: Sequence[int], names: Optional[Sequence[str]] = None):
+    ALIGNED = 1          # ADHA_LAYOUT_ALIGNED: natural (C-struct) alignment inside records
+
+    def __init__(self, widths: Sequence[int], cluster_of: Sequence[int], names: Optional[Sequence[str]] = None,
+                 blocks: Optional[Sequence[int]] = None, aligned: bool = False):
+        """blocks[f]: AoSoA block of field f's cluster (1, 2, ..., 32; equal within a cluster);
+        aligned: C-struct field alignment (adha_layout_create_ex)."""
         if len(widths) != len(cluster_of):
             raise ValueError("widths and cluster_of differ in length")
         h = _L()
-        _check(_lib.adha_layout_create(_u32a(widths), len(widths), _i32a(cluster_of), ctypes.byref(h)))
+        if blocks is None and not aligned:
+            _check(_lib.adha_layout_create(_u32a(widths), len(widths), _i32a(cluster_of), ctypes.byref(h)))
+        else:
+            if blocks is not None and len(blocks) != len(widths):
+                raise ValueError("one block per field")
+            _check(_lib.adha_layout_create_ex(_u32a(widths), len(widths), _i32a(cluster_of),
+                                              None if blocks is None else _i32a(blocks),
+                                              Layout.ALIGNED if aligned else 0, ctypes.byref(h)))
         self._h = h
         self.names = list(names) if names is not None else None
 
@@ -187,6 +203,13 @@ class Layout:
                 cache.clear()
             cache[n] = out.value
         return cache[n]
+
+    def field_address_ex(self, field: int, n_records: int):
+        """(region_offset, stride, offset, block) of a field for an n_records instance."""
+        r, s, o, b = _u64(), ctypes.c_uint32(), ctypes.c_uint32(), ctypes.c_uint32()
+        _check(_lib.adha_layout_field_address_ex(self._h, int(field), int(n_records), ctypes.byref(r),
+                                                 ctypes.byref(s), ctypes.byref(o), ctypes.byref(b)))
+        return r.value, s.value, o.value, b.value
 
     def field_address(self, field: int, n_records: int):
         """(region_offset, stride, offset) of a field for an n_records instance."""

@@ -27,14 +27,23 @@ adha_status fail(adha_status s, const std::string& msg) {
 
 static std::atomic<uint64_t> g_next_id{1};
 
-std::unique_ptr<Layout> make_layout(const uint32_t* widths, int32_t n, const int32_t* labels) {
+static uint32_t natural_align(uint32_t w) {
+    uint32_t a = 1;
+    while (a < 8 && w % (a * 2) == 0) a *= 2;
+    return a;
+}
+
+std::unique_ptr<Layout> make_layout(const uint32_t* widths, int32_t n, const int32_t* labels,
+                                    const int32_t* block_of, bool aligned) {
     auto L = std::make_unique<Layout>();
     L->n_fields = n;
+    L->aligned = aligned;
     L->width.assign(widths, widths + n);
     L->cluster.assign(n, -1);
     L->offset.assign(n, 0);
     // number clusters by first sight in decl order == by minimum decl index
     std::unordered_map<int32_t, int32_t> seen;
+    std::vector<uint32_t> maxa;
     for (int32_t f = 0; f < n; ++f) {
         auto it = seen.find(labels[f]);
         int32_t c;
@@ -43,15 +52,23 @@ std::unique_ptr<Layout> make_layout(const uint32_t* widths, int32_t n, const int
             seen.emplace(labels[f], c);
             L->members.emplace_back();
             L->stride.push_back(0);
+            L->block.push_back(block_of ? (uint32_t)block_of[f] : 1u);
+            maxa.push_back(1);
         } else {
             c = it->second;
         }
         L->cluster[f] = c;
+        if (aligned) {   // C-struct rule: a field starts at a multiple of its natural alignment
+            const uint32_t a = natural_align(widths[f]);
+            maxa[c] = std::max(maxa[c], a);
+            L->stride[c] = (L->stride[c] + a - 1) / a * a;
+        }
         L->offset[f] = (uint32_t)L->stride[c];
         L->stride[c] += widths[f];
         L->members[c].push_back(f);
         L->record_bytes += widths[f];
     }
+    for (size_t c = 0; c < L->stride.size(); ++c) L->stride[c] = (L->stride[c] + maxa[c] - 1) / maxa[c] * maxa[c];
     L->id = g_next_id.fetch_add(1);
     return L;
 }
@@ -60,20 +77,22 @@ bool Layout::region_bases(int64_t n, std::vector<uint64_t>& base, uint64_t* tota
     const int32_t C = n_clusters();
     base.assign(C, 0);
     const uint64_t N = (uint64_t)n;
-    // overflow guard: N * record_bytes + 256 * C must fit in 63 bits
-    if (record_bytes != 0 && N > (uint64_t(INT64_MAX) - 256ull * (uint64_t)C) / record_bytes) return false;
+    // overflow guard: all regions (whole blocks) + 256 * C must fit in 63 bits
+    uint64_t per_rec = 0, per_blk = 0;
+    for (int32_t c = 0; c < C; ++c) { per_rec += stride[c]; per_blk += block[c] * stride[c]; }
+    if (per_rec != 0 && N > (uint64_t(INT64_MAX) - 256ull * (uint64_t)C - per_blk) / per_rec) return false;
     uint64_t b = 0;
     for (int32_t c = 0; c < C; ++c) {
         if (c > 0) b = align256(b);
         base[c] = b;
-        b += N * stride[c];
+        b += region_bytes(c, n);
     }
     if (total) *total = b;
     return true;
 }
 
 std::string layout_string(const Layout& l, const char* const* names) {
-    std::string s;
+    std::string s = l.aligned ? "aligned:" : "";
     for (int32_t c = 0; c < l.n_clusters(); ++c) {
         if (c) s += '|';
         s += '{';
@@ -84,6 +103,7 @@ std::string layout_string(const Layout& l, const char* const* names) {
             else s += "f" + std::to_string(f);
         }
         s += '}';
+        if (l.block[c] > 1) s += "@" + std::to_string(l.block[c]);
     }
     return s;
 }
@@ -129,20 +149,36 @@ static adha_status check_widths(const uint32_t* widths, int32_t n) {
     return ADHA_OK;
 }
 
-adha_status adha_layout_create(const uint32_t* widths, int32_t n, const int32_t* cluster_of,
-                               adha_layout** out) {
+adha_status adha_layout_create_ex(const uint32_t* widths, int32_t n, const int32_t* cluster_of,
+                                  const int32_t* block_of, uint32_t flags, adha_layout** out) {
     clear_error();
     if (!out || !cluster_of) return fail(ADHA_ERR_INVALID_ARG, "null argument");
     adha_status st = check_widths(widths, n);
     if (st != ADHA_OK) return st;
+    if (flags & ~uint32_t(ADHA_LAYOUT_ALIGNED)) return fail(ADHA_ERR_INVALID_ARG, "unknown layout flags");
+    if (block_of) {
+        std::unordered_map<int32_t, int32_t> blk;
+        for (int32_t f = 0; f < n; ++f) {
+            const int32_t b = block_of[f];
+            if (!(b == 1 || b == 2 || b == 4 || b == 8 || b == 16 || b == 32))
+                return fail(ADHA_ERR_INVALID_ARG, "block must be 1, 2, 4, 8, 16 or 32");
+            auto it = blk.emplace(cluster_of[f], b).first;
+            if (it->second != b) return fail(ADHA_ERR_INVALID_ARG, "fields of one cluster need one block size");
+        }
+    }
     try {
         auto* h = new adha_layout;
-        h->L = std::move(*make_layout(widths, n, cluster_of));
+        h->L = std::move(*make_layout(widths, n, cluster_of, block_of, (flags & ADHA_LAYOUT_ALIGNED) != 0));
         *out = h;
     } catch (const std::bad_alloc&) {
         return fail(ADHA_ERR_OOM, "out of host memory");
     }
     return ADHA_OK;
+}
+
+adha_status adha_layout_create(const uint32_t* widths, int32_t n, const int32_t* cluster_of,
+                               adha_layout** out) {
+    return adha_layout_create_ex(widths, n, cluster_of, nullptr, 0u, out);
 }
 
 adha_status adha_layout_from_string(const char* text, const char* const* names,
@@ -158,12 +194,31 @@ adha_status adha_layout_from_string(const char* text, const char* const* names,
             return fail(ADHA_ERR_INVALID_ARG, std::string("duplicate field name ") + names[f]);
     }
     std::vector<int32_t> label(n, -1);
+    std::vector<int32_t> blk(n, 1);
     int32_t next = 0;
     const char* p = text;
+    uint32_t flags = 0;
+    while (*p == ' ' || *p == '\t') ++p;
+    if (std::strncmp(p, "aligned:", 8) == 0) {
+        flags |= ADHA_LAYOUT_ALIGNED;
+        p += 8;
+    }
+    // an optional "@B" after a cluster sets its AoSoA block
+    auto take_block = [&](int32_t lab) -> adha_status {
+        if (*p != '@') return ADHA_OK;
+        ++p;
+        char* e = nullptr;
+        long b = std::strtol(p, &e, 10);
+        if (e == p) return fail(ADHA_ERR_PARSE, "missing block size after '@'");
+        p = e;
+        for (int32_t f = 0; f < n; ++f)
+            if (label[f] == lab) blk[f] = (int32_t)b;
+        return ADHA_OK;
+    };
     auto is_sep = [](char c) { return c == ',' || c == '|' || c == ' ' || c == '\t' || c == '\n'; };
     auto take_name = [&](const char*& q, std::string& nm) {
         const char* s = q;
-        while (*q && !is_sep(*q) && *q != '{' && *q != '}') ++q;
+        while (*q && !is_sep(*q) && *q != '{' && *q != '}' && *q != '@') ++q;
         nm.assign(s, q - s);
     };
     auto assign = [&](const std::string& nm, int32_t lab) -> adha_status {
@@ -190,17 +245,22 @@ adha_status adha_layout_from_string(const char* text, const char* const* names,
                 ++members;
             }
             if (members == 0) return fail(ADHA_ERR_PARSE, "empty cluster '{}'");
+            if ((st = take_block(lab)) != ADHA_OK) return st;
         } else if (*p == '}') {
             return fail(ADHA_ERR_PARSE, "unbalanced '}'");
         } else {
             std::string nm;
             take_name(p, nm);
-            if ((st = assign(nm, next++)) != ADHA_OK) return st;
+            const int32_t lab = next++;
+            if ((st = assign(nm, lab)) != ADHA_OK) return st;
+            if ((st = take_block(lab)) != ADHA_OK) return st;
         }
     }
     for (int32_t f = 0; f < n; ++f)
         if (label[f] < 0) return fail(ADHA_ERR_PARSE, std::string("field '") + names[f] + "' missing");
-    return adha_layout_create(widths, n, label.data(), out);
+    st = adha_layout_create_ex(widths, n, label.data(), blk.data(), flags, out);
+    if (st == ADHA_ERR_INVALID_ARG) st = ADHA_ERR_PARSE;
+    return st;
 }
 
 adha_status adha_layout_to_string(const adha_layout* h, const char* const* names, char* buf,
@@ -256,6 +316,13 @@ adha_status adha_layout_field_address(const adha_layout* h, int32_t f, int64_t n
     if (stride) *stride = (uint32_t)h->L.stride[c];
     if (offset) *offset = h->L.offset[f];
     return ADHA_OK;
+}
+
+adha_status adha_layout_field_address_ex(const adha_layout* h, int32_t f, int64_t n, uint64_t* region_offset,
+                                         uint32_t* stride, uint32_t* offset, uint32_t* block) {
+    adha_status st = adha_layout_field_address(h, f, n, region_offset, stride, offset);
+    if (st == ADHA_OK && block) *block = h->L.block[h->L.cluster[f]];
+    return st;
 }
 
 void adha_layout_destroy(adha_layout* h) { delete h; }

@@ -213,34 +213,53 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     uint32_t gstep[VMAX];
     uint32_t ne = 0, nv = 0;
 
-    // Tails first: records [n_tiles*T_k, N) of every component, spread over the consumer threads
-    // of ALL CTAs, four records in flight per thread.  Done while the producer's first tiles are
-    // still in flight, so the latency-bound scalar copies hide under the pipeline fill (one CTA
-    // copying a 48 KB tail alone took ~40 us).
+    // Tails first: records [n_tiles*T_k, N) of every component.  Plain components spread their
+    // tail over the consumer threads of ALL CTAs, four records in flight per thread, while the
+    // producer's first tiles are still in flight (one CTA copying a 48 KB tail alone took ~40 us).
+    // Components whose dst has padding or AoSoA blocks (CF_TAIL_ZERO) zero their dst tail area
+    // first, so their tail belongs to one CTA (zero, barrier, copy).
     {
         const int64_t gid = (int64_t)blockIdx.x * (NCONS * 32) + tid;
         const int64_t gstride = (int64_t)gridDim.x * (NCONS * 32);
         for (uint32_t kk = 0; kk < p.n_comp; ++kk) {
             const CompDesc& K = p.comp[kk];
-            if (K.skip) continue;
+            if (K.flags & CF_SKIP) continue;
             const int64_t lo = K.n_tiles * (int64_t)K.T;
             const int64_t n_tail = p.n_records - lo;
             if (n_tail <= 0) continue;
+            const bool own = (K.flags & CF_TAIL_ZERO) != 0;
+            if (own && gridDim.x - 1 - (kk % gridDim.x) != blockIdx.x) continue;
+            const int64_t first = own ? tid : gid, step = own ? (int64_t)(NCONS * 32) : gstride;
+            if (own) {
+                // every dst cluster of the component: bytes [lo*stride, ceil(N/B)*B*stride) := 0
+                for (uint32_t f = K.f_lo; f < K.f_hi; ++f) {
+                    const FieldDesc fd = et.fields[f];
+                    const uint64_t B = 1ull << fd.dbl, st = p.dstc[fd.dc].stride;
+                    const uint64_t a0 = p.dst + p.dstc[fd.dc].region + (uint64_t)lo * st;
+                    const uint64_t a1 = p.dst + p.dstc[fd.dc].region + ((uint64_t)p.n_records + B - 1) / B * B * st;
+                    for (uint64_t a = a0 + (uint64_t)tid * sizeof(U); a < a1; a += NCONS * 32 * sizeof(U))
+                        *reinterpret_cast<U*>(a) = U(0);
+                }
+                named_bar_sync(2, NCONS * 32);
+            }
             const int64_t total = n_tail * (int64_t)(K.f_hi - K.f_lo);
-            for (int64_t x0 = gid; x0 < total; x0 += 4 * gstride) {
+            for (int64_t x0 = first; x0 < total; x0 += 4 * step) {
                 const U* sp[4];
                 U* dp[4];
                 uint32_t nu[4];
 #pragma unroll
                 for (int m = 0; m < 4; ++m) {
-                    const int64_t x = x0 + m * gstride;
+                    const int64_t x = x0 + m * step;
                     nu[m] = 0;
                     if (x < total) {
                         const uint32_t f = K.f_lo + (uint32_t)(x / n_tail);
-                        const int64_t r = lo + (x % n_tail);
+                        const uint64_t r = (uint64_t)(lo + (x % n_tail));
                         const FieldDesc fd = et.fields[f];
-                        sp[m] = (const U*)(p.src + p.srcc[fd.sc].region + (uint64_t)r * p.srcc[fd.sc].stride + fd.soff);
-                        dp[m] = (U*)(p.dst + p.dstc[fd.dc].region + (uint64_t)r * p.dstc[fd.dc].stride + fd.doff);
+                        const uint64_t ss = p.srcc[fd.sc].stride, ds = p.dstc[fd.dc].stride;
+                        sp[m] = (const U*)(p.src + p.srcc[fd.sc].region + (r >> fd.sbl) * (ss << fd.sbl) +
+                                           ((uint64_t)fd.soff << fd.sbl) + (r & ((1u << fd.sbl) - 1)) * fd.width);
+                        dp[m] = (U*)(p.dst + p.dstc[fd.dc].region + (r >> fd.dbl) * (ds << fd.dbl) +
+                                     ((uint64_t)fd.doff << fd.dbl) + (r & ((1u << fd.dbl) - 1)) * fd.width);
                         nu[m] = fd.width / (uint32_t)sizeof(U);
                     }
                 }
@@ -267,7 +286,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         if ((int)k != k_cur) {
             // this warp's instructions of component k: i = warp + NCONS*e; lane's unit = entry i*32 + lane
             k_cur = (int)k;
-            nv = copy_plan(p, p.comp[k].dc_lo, T, p.comp[k].tile_bytes, tid, gofs, gstep);
+            nv = copy_plan(p, p.comp[k].dc_lo, T, p.comp[k].out_bytes, tid, gofs, gstep);
+            if (p.comp[k].flags & CF_ZERO_OUT) {
+                // dst records have padding the permutation never writes: zero both output buffers
+                // once for this component (the same positions stay untouched in every tile)
+                named_bar_sync(1, NCONS * 32);
+                const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+                for (uint32_t v = tid * 16; v < p.s_out * p.stage_bytes; v += NCONS * 32 * 16) sts128(out0 + v, z);
+                named_bar_sync(1, NCONS * 32);
+            }
             if constexpr (NG > 0) {
                 // G groups per period -> I instructions of 32 lanes; with I < NCONS the periods are
                 // split over P = NCONS / I warps per instruction (slot s -> instruction s % I,
@@ -416,6 +443,27 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
 }
 
+constexpr int ZMAX = 128;
+struct ZeroParams {
+    uint32_t n, pad;
+    uint64_t ptr[ZMAX];
+    uint64_t bytes[ZMAX];
+};
+// zero whole byte ranges (dst regions with padding, direct path); 16-byte stores where aligned
+__global__ void zero_kernel(const __grid_constant__ ZeroParams z) {
+    for (uint32_t i = 0; i < z.n; ++i) {
+        uint8_t* p = (uint8_t*)z.ptr[i];
+        const uint64_t nb = z.bytes[i];
+        const uint64_t head = ((16 - ((uintptr_t)p & 15)) & 15) < nb ? ((16 - ((uintptr_t)p & 15)) & 15) : nb;
+        const uint64_t nv = (nb - head) / 16;
+        for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < nv; k += (uint64_t)gridDim.x * blockDim.x)
+            reinterpret_cast<uint4*>(p + head)[k] = make_uint4(0u, 0u, 0u, 0u);
+        if (blockIdx.x == 0)
+            for (uint64_t k = threadIdx.x; k < head + (nb - head) % 16; k += blockDim.x)
+                p[k < head ? k : head + nv * 16 + (k - head)] = 0;
+    }
+}
+
 template <int NF>
 __global__ void remap_naive_kernel(const __grid_constant__ NaiveParamsT<NF> p) {
     const int64_t n = p.n_records;
@@ -424,8 +472,12 @@ __global__ void remap_naive_kernel(const __grid_constant__ NaiveParamsT<NF> p) {
         const uint32_t f = (uint32_t)(k / n);
         const int64_t r = p.lo + (k - (int64_t)f * n);
         const NaiveField& fd = p.f[f];
-        const uint8_t* s = (const uint8_t*)(p.src + fd.sbase + (uint64_t)r * fd.sstride + fd.soff);
-        uint8_t* d = (uint8_t*)(p.dst + fd.dbase + (uint64_t)r * fd.dstride + fd.doff);
+        const uint32_t sbl = fd.pad & 0xFF, dbl = (fd.pad >> 8) & 0xFF;
+        const uint64_t ur = (uint64_t)r;
+        const uint8_t* s = (const uint8_t*)(p.src + fd.sbase + (ur >> sbl) * ((uint64_t)fd.sstride << sbl) +
+                                            ((uint64_t)fd.soff << sbl) + (ur & ((1u << sbl) - 1)) * fd.width);
+        uint8_t* d = (uint8_t*)(p.dst + fd.dbase + (ur >> dbl) * ((uint64_t)fd.dstride << dbl) +
+                                ((uint64_t)fd.doff << dbl) + (ur & ((1u << dbl) - 1)) * fd.width);
         const uintptr_t a = (uintptr_t)s | (uintptr_t)d | fd.width;
         uint32_t j = 0;
         if ((a & 3) == 0) {
@@ -579,8 +631,11 @@ adha_status launch_naive_t(const uint8_t* src, const Layout& ls, const std::vect
         for (int k = 0; k < nf; ++k) {
             const int f = f0 + k;
             const int cs = ls.cluster[f], cd = ld.cluster[f];
+            uint32_t sbl = 0, dbl = 0;
+            while ((1u << sbl) < ls.block[cs]) ++sbl;
+            while ((1u << dbl) < ld.block[cd]) ++dbl;
             P->f[k] = {bs[cs], bd[cd], (uint32_t)ls.stride[cs], (uint32_t)ld.stride[cd], ls.offset[f], ld.offset[f],
-                       ls.width[f], 0};
+                       ls.width[f], sbl | (dbl << 8)};
         }
         const int64_t total = (hi - lo) * (int64_t)nf;
         const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, (int64_t)n_sm * 16));
@@ -594,6 +649,24 @@ adha_status launch_naive_t(const uint8_t* src, const Layout& ls, const std::vect
 adha_status launch_naive(const uint8_t* src, const Layout& ls, const std::vector<uint64_t>& bs, uint8_t* dst,
                          const Layout& ld, const std::vector<uint64_t>& bd, int64_t lo, int64_t hi,
                          cudaStream_t st) {
+    // dst clusters with padding or AoSoA blocks: zero their regions first (the copy fills the payload)
+    ZeroParams Z;
+    std::memset(&Z, 0, sizeof Z);
+    for (int c = 0; c < ld.n_clusters(); ++c) {
+        if (ld.stride[c] == ld.payload(c) && ld.block[c] == 1) continue;
+        if (Z.n == ZMAX) {
+            zero_kernel<<<256, 256, 0, st>>>(Z);
+            Z.n = 0;
+        }
+        Z.ptr[Z.n] = (uint64_t)(uintptr_t)dst + bd[c];
+        Z.bytes[Z.n] = ld.region_bytes(c, hi);
+        ++Z.n;
+    }
+    if (Z.n) {
+        zero_kernel<<<256, 256, 0, st>>>(Z);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return cuda_fail(e, "zero_kernel launch");
+    }
     if (ls.n_fields <= SMALL_NF) return launch_naive_t<SMALL_NF>(src, ls, bs, dst, ld, bd, lo, hi, st);
     return launch_naive_t<MAXF>(src, ls, bs, dst, ld, bd, lo, hi, st);
 }
@@ -668,10 +741,12 @@ adha_status remap_checked(const uint8_t* src, const Layout& ls, uint8_t* dst, co
         const RemapPlan::Comp& K = plan->comps[k];
         CompDesc& D = P->comp[k];
         D.T = call_tile(*plan, (int)k, n, n_sm);
-        D.tile_bytes = D.T * K.R;
+        D.tile_bytes = D.T * K.Rs;
+        D.out_bytes = D.T * K.Rd;
         // an identity component whose dst region is its src region moves nothing (NEXT N1)
-        D.skip = K.identity && P->src + ck.bs[K.src_clusters[0]] == P->dst + ck.bd[K.dst_clusters[0]];
-        D.n_tiles = D.skip ? 0 : n / D.T;
+        const bool skip = K.identity && P->src + ck.bs[K.src_clusters[0]] == P->dst + ck.bd[K.dst_clusters[0]];
+        D.flags = (uint16_t)((skip ? CF_SKIP : 0) | (K.zero_out ? CF_ZERO_OUT : 0) | (K.tail_zero ? CF_TAIL_ZERO : 0));
+        D.n_tiles = skip ? 0 : n / D.T;
         D.tile_base = tiles;
         tiles += D.n_tiles;
         D.identity = K.identity ? 1 : 0;
@@ -894,9 +969,13 @@ extern "C" adha_status adha_remap_host(const void* src_host, const adha_layout* 
     // region offsets lo*stride stay 16-byte aligned); each chunk is its own layout instance
     // (record locality).  PIPE_SLOTS chunks are in flight on PIPE_SLOTS internal streams.
     int slots = PIPE_SLOTS;
-    const uint64_t pad = 256ull * (ls.n_clusters() + ld.n_clusters() + 2);
-    const uint64_t R = ls.record_bytes;
-    const uint64_t per_rec = hybrid ? R : 2 * R;
+    uint64_t Rs = 0, Rd = 0;                   // bytes per record incl. alignment padding
+    for (int c = 0; c < ls.n_clusters(); ++c) Rs += ls.stride[c];
+    for (int c = 0; c < ld.n_clusters(); ++c) Rd += ld.stride[c];
+    // region alignment (256 B per region) and a partial last AoSoA block (< 32 records)
+    const uint64_t pad = 256ull * (ls.n_clusters() + ld.n_clusters() + 2) + 32 * (Rs + Rd);
+    const uint64_t R = Rs;
+    const uint64_t per_rec = hybrid ? Rs : Rs + Rd;
     uint64_t slot = 0;
     for (; slots >= 1; --slots) {
         slot = (scratch_bytes / slots) & ~uint64_t(255);
@@ -938,7 +1017,7 @@ extern "C" adha_status adha_remap_host(const void* src_host, const adha_layout* 
         ls.region_bases(m, ms, &mbs);
         ld.region_bases(m, md, &mbd);
         for (int c = 0; c < ls.n_clusters(); ++c) {
-            e = cudaMemcpyAsync(dsrc + ms[c], hsrc + ck.bs[c] + (uint64_t)lo * ls.stride[c], (uint64_t)m * ls.stride[c],
+            e = cudaMemcpyAsync(dsrc + ms[c], hsrc + ck.bs[c] + (uint64_t)lo * ls.stride[c], ls.region_bytes(c, m),
                                 cudaMemcpyHostToDevice, st);
             if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync H2D");
         }
@@ -956,7 +1035,7 @@ extern "C" adha_status adha_remap_host(const void* src_host, const adha_layout* 
             if ((s = remap_checked(dsrc, ls, ddst, ld, m, cm, st)) != ADHA_OK) return s;
             for (int c = 0; c < ld.n_clusters(); ++c) {
                 e = cudaMemcpyAsync(hdst + ck.bd[c] + (uint64_t)lo * ld.stride[c], ddst + md[c],
-                                    (uint64_t)m * ld.stride[c], cudaMemcpyDeviceToHost, st);
+                                    ld.region_bytes(c, m), cudaMemcpyDeviceToHost, st);
                 if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync D2H");
             }
         }

@@ -81,6 +81,24 @@ bool matched_order(const std::vector<Unit>& units, std::vector<uint32_t>& order)
 }
 }  // namespace
 
+static uint8_t log2u(uint32_t b) {
+    uint8_t l = 0;
+    while ((1u << l) < b) ++l;
+    return l;
+}
+
+static FieldDesc field_desc(const RemapPlan& P, const Layout& ls, const Layout& ld, int f) {
+    FieldDesc d;
+    d.sc = (uint8_t)P.src_slot[ls.cluster[f]];
+    d.dc = (uint8_t)P.dst_slot[ld.cluster[f]];
+    d.sbl = log2u(ls.block[ls.cluster[f]]);
+    d.dbl = log2u(ld.block[ld.cluster[f]]);
+    d.soff = ls.offset[f];
+    d.doff = ld.offset[f];
+    d.width = ls.width[f];
+    return d;
+}
+
 // Reorder a byte group's slots: source word m moves to slot ps[m], output word o to slot po[o];
 // the PRMT selectors are re-encoded for the new source slots.
 static void permute_group(ByteGroup& g, const int ps[4], const int po[4]) {
@@ -151,9 +169,11 @@ RemapPlan compile_plan(const Layout& ls, const Layout& ld) {
     uint64_t gall = 0;
     for (int f = 0; f < F; ++f) {
         gall = std::gcd(gall, (uint64_t)ls.width[f]);
-        gall = std::gcd(gall, (uint64_t)ls.offset[f]);
-        gall = std::gcd(gall, (uint64_t)ld.offset[f]);
+        gall = std::gcd(gall, (uint64_t)ls.offset[f] * ls.block[ls.cluster[f]]);
+        gall = std::gcd(gall, (uint64_t)ld.offset[f] * ld.block[ld.cluster[f]]);
     }
+    for (int c = 0; c < Cs; ++c) gall = std::gcd(gall, ls.stride[c]);
+    for (int c = 0; c < Cd; ++c) gall = std::gcd(gall, ld.stride[c]);
     P.unit = (gall % 4 == 0) ? 4 : (gall % 2 == 0) ? 2 : 1;
     const uint32_t g = P.unit;
 
@@ -200,8 +220,21 @@ RemapPlan compile_plan(const Layout& ls, const Layout& ld) {
     for (auto& K : P.comps) {
         for (int c : K.src_clusters) { P.src_slot[c] = (int)P.src_order.size(); P.src_order.push_back(c); }
         for (int c : K.dst_clusters) { P.dst_slot[c] = (int)P.dst_order.size(); P.dst_order.push_back(c); }
-        K.identity = K.src_clusters.size() == 1 && K.dst_clusters.size() == 1 &&
-                     ls.members[K.src_clusters[0]] == ld.members[K.dst_clusters[0]];
+        for (int c : K.src_clusters) K.Rs += (uint32_t)ls.stride[c];
+        for (int c : K.dst_clusters) {
+            K.Rd += (uint32_t)ld.stride[c];
+            const bool padded = ld.stride[c] != ld.payload(c);
+            K.zero_out = K.zero_out || padded;
+            K.tail_zero = K.tail_zero || padded || ld.block[c] > 1;
+        }
+        // identity: one cluster on each side with byte-identical records and no padding to zero
+        if (K.src_clusters.size() == 1 && K.dst_clusters.size() == 1) {
+            const int cs = K.src_clusters[0], cd = K.dst_clusters[0];
+            bool same = ls.members[cs] == ld.members[cd] && ls.block[cs] == ld.block[cd] &&
+                        ls.stride[cs] == ld.stride[cd] && ld.stride[cd] == ld.payload(cd);
+            for (int f : ls.members[cs]) same = same && ls.offset[f] == ld.offset[f];
+            K.identity = same;
+        }
     }
 
     // tile sizes and stages
@@ -213,10 +246,11 @@ RemapPlan compile_plan(const Layout& ls, const Layout& ld) {
     auto round128 = [](uint64_t x) { return (x + 127) / 128 * 128; };
     uint64_t stage = 0;
     for (auto& K : P.comps) {
-        uint64_t T = std::max<uint64_t>(32, (target / (32ull * K.R)) * 32);
+        const uint64_t Rmax = std::max(K.Rs, K.Rd);
+        uint64_t T = std::max<uint64_t>(32, (target / (32ull * Rmax)) * 32);
         T = std::min<uint64_t>(T, std::max<uint32_t>(32, t_cap / 32 * 32));
         K.T_max = (uint32_t)T;
-        stage = std::max<uint64_t>(stage, round128(T * K.R));
+        stage = std::max<uint64_t>(stage, round128(T * Rmax));
     }
     while (s_in > 2 && (s_in + S_OUT) * stage > budget) --s_in;
     if ((s_in + S_OUT) * stage > budget || stage > STAGE_MAX) {
@@ -224,10 +258,11 @@ RemapPlan compile_plan(const Layout& ls, const Layout& ld) {
         const uint64_t cap = std::min<uint64_t>(budget / (s_in + S_OUT) / 128 * 128, STAGE_MAX);
         stage = 0;
         for (auto& K : P.comps) {
-            uint64_t T = (cap / K.R) / 32 * 32;
+            const uint64_t Rmax = std::max(K.Rs, K.Rd);
+            uint64_t T = (cap / Rmax) / 32 * 32;
             if (T < 32) return naive("a 32-record tile does not fit in shared memory");
             K.T_max = (uint32_t)std::min<uint64_t>(K.T_max, T);
-            stage = std::max<uint64_t>(stage, round128((uint64_t)K.T_max * K.R));
+            stage = std::max<uint64_t>(stage, round128((uint64_t)K.T_max * Rmax));
         }
     }
     P.s_in = s_in;
@@ -264,23 +299,39 @@ RemapPlan compile_plan(const Layout& ls, const Layout& ld) {
             // the output words of one 32-record period with the source word of each byte
             std::vector<OW> ows;
             for (int cd : K.dst_clusters) {
-                const uint32_t sd = (uint32_t)ld.stride[cd];
-                std::vector<int> field_at(sd, -1);
+                // which (field, record, byte) lands on every byte of the chunk's 32-record period
+                const uint32_t pb = 32 * (uint32_t)ld.stride[cd];
+                std::vector<int> pf(pb, -1);
+                std::vector<uint32_t> pr(pb, 0), pj(pb, 0);
                 for (int f : ld.members[cd])
-                    for (uint32_t b = 0; b < ld.width[f]; ++b) field_at[ld.offset[f] + b] = f;
-                for (uint32_t w = 0; w < 8 * sd; ++w) {
+                    for (uint32_t r = 0; r < 32; ++r)
+                        for (uint32_t j = 0; j < ld.width[f]; ++j) {
+                            const uint64_t a = ld.local_addr(f, r) + j;
+                            pf[a] = f;
+                            pr[a] = r;
+                            pj[a] = j;
+                        }
+                for (uint32_t w = 0; w < pb / 4; ++w) {
                     OW o;
                     o.out = (uint16_t)(4 * w);
                     o.dc = (uint8_t)P.dst_slot[cd];
+                    bool any = false;
                     for (uint32_t j = 0; j < 4; ++j) {
-                        const uint32_t B = 4 * w + j, r = B / sd, b = B % sd;
-                        const int f = field_at[b];
-                        const int cs = ls.cluster[f];
-                        const uint64_t local = r * ls.stride[cs] + ls.offset[f] + (b - ld.offset[f]);
-                        o.src[j] = {P.src_slot[cs], (uint32_t)(local & ~uint64_t(3))};
-                        o.byte[j] = (uint8_t)(local & 3);
+                        const uint32_t B = 4 * w + j;
+                        const int f = pf[B];
+                        if (f < 0) {          // padding byte: the zero source (-1), an unloaded slot
+                            o.src[j] = {-1, 0};
+                            o.byte[j] = 0;
+                        } else {
+                            any = true;
+                            const int cs = ls.cluster[f];
+                            const uint64_t local = ls.local_addr(f, pr[B]) + pj[B];
+                            o.src[j] = {P.src_slot[cs], (uint32_t)(local & ~uint64_t(3))};
+                            o.byte[j] = (uint8_t)(local & 3);
+                        }
                         if (std::find(o.set.begin(), o.set.end(), o.src[j]) == o.set.end()) o.set.push_back(o.src[j]);
                     }
+                    if (!any) continue;       // all padding: the pre-zeroed output buffer already holds it
                     std::sort(o.set.begin(), o.set.end());
                     ows.push_back(o);
                 }
@@ -311,8 +362,12 @@ RemapPlan compile_plan(const Layout& ls, const Layout& ld) {
                 }
                 ByteGroup gr;
                 std::memset(&gr, 0, sizeof gr);
-                gr.n_src = (uint8_t)uni.size();
-                for (size_t m = 0; m < uni.size(); ++m) {
+                // real source words first, the zero source (padding) last: slots >= n_src read as 0
+                std::stable_partition(uni.begin(), uni.end(), [](const std::pair<int, uint32_t>& x) { return x.first >= 0; });
+                const size_t n_real = (size_t)std::count_if(uni.begin(), uni.end(),
+                                                            [](const std::pair<int, uint32_t>& x) { return x.first >= 0; });
+                gr.n_src = (uint8_t)n_real;
+                for (size_t m = 0; m < n_real; ++m) {
                     gr.src_sc[m] = (uint8_t)uni[m].first;
                     gr.src_off[m] = (uint16_t)uni[m].second;
                 }
@@ -428,7 +483,7 @@ RemapPlan compile_plan(const Layout& ls, const Layout& ld) {
             uint64_t stage2 = 0;
             for (auto& K : P.comps) {
                 K.T_max = std::max<uint32_t>(128, K.T_max / 128 * 128);
-                stage2 = std::max<uint64_t>(stage2, (uint64_t)K.T_max * K.R + 32 * max_chunks);   // + stagger
+                stage2 = std::max<uint64_t>(stage2, (uint64_t)K.T_max * std::max(K.Rs, K.Rd) + 32 * max_chunks);
             }
             stage2 = (stage2 + 127) / 128 * 128;
             if ((P.s_in + P.s_out) * stage2 > budget) gcls = -1;
@@ -451,9 +506,7 @@ RemapPlan compile_plan(const Layout& ls, const Layout& ld) {
             FieldDesc* fd = reinterpret_cast<FieldDesc*>(img + sizeof(ByteGroup) * ng);
             int fi = 0;
             for (auto& K : P.comps)
-                for (int f : K.fields)
-                    fd[fi++] = {(uint16_t)P.src_slot[ls.cluster[f]], (uint16_t)P.dst_slot[ld.cluster[f]],
-                                ls.offset[f], ld.offset[f], ls.width[f]};
+                for (int f : K.fields) fd[fi++] = field_desc(P, ls, ld, f);
             P.byte_groups = true;
             P.group_class = gcls;
             P.matched = false;
@@ -486,8 +539,8 @@ RemapPlan compile_plan(const Layout& ls, const Layout& ld) {
             for (int f : K.fields) {
                 const int cs = ls.cluster[f], cd = ld.cluster[f];
                 for (uint32_t j = 0; j < ls.width[f] / g; ++j) {
-                    const uint64_t ib = r * ls.stride[cs] + ls.offset[f] + j * g;
-                    const uint64_t ob = r * ld.stride[cd] + ld.offset[f] + j * g;
+                    const uint64_t ib = ls.local_addr(f, r) + j * g;
+                    const uint64_t ob = ld.local_addr(f, r) + j * g;
                     units.push_back({(uint32_t)(ib / g), (uint32_t)(ob / g), (uint8_t)P.src_slot[cs],
                                      (uint8_t)P.dst_slot[cd]});
                 }
@@ -527,9 +580,7 @@ RemapPlan compile_plan(const Layout& ls, const Layout& ld) {
     FieldDesc* fd = reinterpret_cast<FieldDesc*>(img + 6 * nent);
     int fi = 0;
     for (auto& K : P.comps)
-        for (int f : K.fields)
-            fd[fi++] = {(uint16_t)P.src_slot[ls.cluster[f]], (uint16_t)P.dst_slot[ld.cluster[f]], ls.offset[f],
-                        ld.offset[f], ls.width[f]};
+        for (int f : K.fields) fd[fi++] = field_desc(P, ls, ld, f);
     P.tiled = true;
     return P;
 }
@@ -564,7 +615,9 @@ std::string describe_plan(const RemapPlan& p, const Layout& ls, const Layout& ld
         const auto& K = p.comps[k];
         o += (k ? ",{" : "{");
         o += "\"src_clusters\":" + iarr(K.src_clusters) + ",\"dst_clusters\":" + iarr(K.dst_clusters) +
-             ",\"fields\":" + iarr(K.fields) + ",\"R\":" + std::to_string(K.R) + ",\"T\":" + std::to_string(K.T_max) +
+             ",\"fields\":" + iarr(K.fields) + ",\"R\":" + std::to_string(K.R) + ",\"Rs\":" + std::to_string(K.Rs) +
+             ",\"Rd\":" + std::to_string(K.Rd) + ",\"zero_out\":" + (K.zero_out ? "true" : "false") +
+             ",\"T\":" + std::to_string(K.T_max) +
              ",\"identity\":" + (K.identity ? "true" : "false") + ",\"instr_base\":" + std::to_string(K.instr_base) +
              ",\"n_instr\":" + std::to_string(K.n_instr) + "}";
     }

@@ -51,7 +51,8 @@ struct ClusterDesc {
 };
 
 struct FieldDesc {
-    uint16_t sc, dc;      // src / dst cluster (indices into srcc / dstc)
+    uint8_t sc, dc;       // src / dst cluster (indices into srcc / dstc)
+    uint8_t sbl, dbl;     // log2 of the src / dst cluster's AoSoA block
     uint32_t soff, doff;  // byte offset in the src / dst cluster record
     uint32_t width;
 };
@@ -60,14 +61,19 @@ struct CompDesc {
     int64_t tile_base;    // first global tile index of the component
     int64_t n_tiles;      // floor(N / T)
     uint32_t T;           // records per tile (multiple of 32)
-    uint32_t tile_bytes;  // T * R_k: TMA transaction bytes per tile
+    uint32_t tile_bytes;  // T * (sum of src strides): TMA transaction bytes per tile
+    uint32_t out_bytes;   // T * (sum of dst strides): bytes the copy-out writes per tile
     uint16_t sc_lo, sc_hi, dc_lo, dc_hi;   // cluster ranges (clusters are numbered by component)
     uint16_t f_lo, f_hi;                   // field range in the field table
     uint16_t identity;
-    uint16_t skip;        // 1: identity component whose dst region IS its src region (nothing moves)
+    uint16_t flags;       // CF_SKIP | CF_ZERO_OUT | CF_TAIL_ZERO
     uint32_t instr_base;  // first instruction (unit mode) / first group (byte-group mode) in the table
     uint32_t n_instr;     // unit mode: W_k = R_k / g; byte-group mode: groups per period
 };
+
+constexpr uint16_t CF_SKIP = 1;       // identity component whose dst region IS its src region (nothing moves)
+constexpr uint16_t CF_ZERO_OUT = 2;   // dst records have padding: output buffers pre-zeroed at component start
+constexpr uint16_t CF_TAIL_ZERO = 4;  // dst padding or AoSoA blocks: tail area zeroed before the tail copy
 
 struct TiledParams {
     uint64_t src;         // base address: src region c starts at src + srcc[c].region
@@ -119,7 +125,7 @@ constexpr int GCLASS_NG[2] = {128, 384};
 constexpr int GCLASS_GMAX[2] = {1, 2};    // slots per warp: ceil(instructions * period-split / NCONS)
 
 // Table size classes (entries per warp EMAX = instructions per warp per component).
-constexpr int CLASS_NENT[4] = {512, 1024, 2048, 3552};
+constexpr int CLASS_NENT[4] = {512, 1024, 2048, 3456};
 constexpr int CLASS_EMAX[4] = {2, 4, 8, 14};
 
 struct NaiveField {
@@ -145,7 +151,9 @@ using SmallParams = NaiveParamsT<SMALL_NF>;
 struct RemapPlan {
     struct Comp {
         std::vector<int> src_clusters, dst_clusters, fields;   // original (canonical) indices
-        uint32_t R = 0;               // bytes per record of the component
+        uint32_t R = 0;               // payload bytes per record of the component
+        uint32_t Rs = 0, Rd = 0;      // src / dst bytes per record (strides, padding included)
+        bool zero_out = false, tail_zero = false;
         uint32_t T_max = 0;           // records per tile at full size
         bool identity = false;
         uint32_t instr_base = 0, n_instr = 0;

@@ -416,3 +416,83 @@ def test_byte_group_plans_cover_every_byte():
         d = A.plan_describe(A.Layout(widths, ls), A.Layout(widths, ld))
         if d["unit"] < 4 and d["byte_groups"]:
             _check_byte_groups(widths, ls, ld)
+
+
+# ---------------------------------------------------------------- generalised layouts (N4)
+
+def _rand_general(rng, F):
+    widths = [rng.choice([1, 2, 3, 4, 6, 8, 12]) for _ in range(F)]
+    labels = [rng.randrange(F) for _ in range(F)]
+    cb = {lab: rng.choice([1, 1, 2, 4, 8, 16, 32]) for lab in set(labels)}
+    return widths, labels, [cb[l] for l in labels], rng.random() < 0.5
+
+
+def test_generalised_descriptor_matches_oracle():
+    rng = random.Random(13)
+    for _ in range(200):
+        F = rng.randint(1, 10)
+        widths, labels, blocks, aligned = _rand_general(rng, F)
+        L = A.Layout(widths, labels, blocks=blocks, aligned=aligned)
+        for n in (0, 1, 7, 33, 1000):
+            d = O.field_addresses_ex(widths, labels, n, blocks, aligned)
+            assert L.nbytes(n) == d["total"]
+            for f in range(F):
+                assert L.field_address_ex(f, n) == (d["base"][f], d["stride"][f], d["offset"][f], d["block"][f])
+        s = L.to_string()
+        names = [f"f{i}" for i in range(F)]
+        assert A.Layout.from_string(s, names, widths).to_string() == s
+    with pytest.raises(A.AdhaError):
+        A.Layout([4, 4], [0, 0], blocks=[2, 4])          # one block per cluster
+    with pytest.raises(A.AdhaError):
+        A.Layout([4], [0], blocks=[3])
+    names = ["a", "b", "c"]
+    L = A.Layout.from_string("aligned:{a,b}@8|{c}", names, [1, 4, 2])
+    assert L.field_address_ex(1, 10) == (0, 8, 4, 8) and L.to_string() == "aligned:{a,b}@8|{c}"
+
+
+def _gen_plan_checks(widths, ls, bs, als, ld, bd, ald):
+    """Unit-mode plan table of generalised layouts: every unit of one period moved exactly once,
+    to the generalised element address; padding units never written."""
+    Ls = A.Layout(widths, ls, blocks=bs, aligned=als)
+    Ld = A.Layout(widths, ld, blocks=bd, aligned=ald)
+    d = A.plan_describe(Ls, Ld)
+    assert d["tiled"], d
+    if d["byte_groups"]:
+        return d
+    g = d["unit"]
+    from tests.test_oracle_remap import clusters_in_order
+    cs, cd = clusters_in_order(ls), clusters_in_order(ld)
+    csrc = {f: k for k, c in enumerate(cs) for f in c}
+    cdst = {f: k for k, c in enumerate(cd) for f in c}
+    S = O.field_addresses_ex(widths, ls, 32, bs, als)
+    D = O.field_addresses_ex(widths, ld, 32, bd, ald)
+    ent_in, ent_out = np.array(d["ent_in"]), np.array(d["ent_out"])
+    ent_sc, ent_dc = np.array(d["ent_sc"]), np.array(d["ent_dc"])
+    for K in d["components"]:
+        if K["identity"]:
+            continue
+        lo, hi = 32 * K["instr_base"], 32 * (K["instr_base"] + K["n_instr"])
+        exp = set()
+        for r in range(32):
+            for f in K["fields"]:
+                for j in range(0, widths[f], g):
+                    a_s = O.addr_ex(S, f, r) - int(S["base"][f]) + j
+                    a_d = O.addr_ex(D, f, r) - int(D["base"][f]) + j
+                    exp.add((a_s // g, a_d // g, csrc[f], cdst[f]))
+        got = {(int(a), int(b), d["src_order"][c], d["dst_order"][e])
+               for a, b, c, e in zip(ent_in[lo:hi], ent_out[lo:hi], ent_sc[lo:hi], ent_dc[lo:hi])}
+        assert got == exp
+    return d
+
+
+def test_generalised_plan_tables():
+    _gen_plan_checks([4] * 8, [0] * 8, [1] * 8, False, [0] * 8, [8] * 8, False)            # AoS -> AoSoA8
+    _gen_plan_checks([4, 8, 4, 4], [0] * 4, [32] * 4, False, list(range(4)), [1] * 4, False)  # AoSoA32 -> SoA
+    _gen_plan_checks([4, 8, 4], list(range(3)), [1] * 3, False, [0] * 3, [1] * 3, True)      # SoA -> aligned AoS
+    rng = random.Random(17)
+    for _ in range(40):
+        F = rng.randint(1, 8)
+        widths = [rng.choice([4, 8, 12]) for _ in range(F)]
+        w2, ls, bs, als = _rand_general(rng, F)
+        _, ld, bd, ald = _rand_general(rng, F)
+        _gen_plan_checks(widths, ls, bs, als, ld, bd, ald)

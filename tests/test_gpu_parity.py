@@ -383,3 +383,52 @@ def test_remap_host_modes(mode, pinned, monkeypatch):
         A.remap_host(h_src, La, h_dst, Ld, n, scratch)
         torch.cuda.synchronize()
         assert np.array_equal(h_dst.numpy(), oracle_dst(src_np, ls, ld, widths, n)), (mode, pinned, widths[:4])
+
+
+# ----------------------------------------------------------------------------- generalised layouts (N4)
+
+def check_pair_ex(widths, ls, bs, als, ld, bd, ald, n, seed=0):
+    cols = field_columns(seed, n, widths)
+    src = O.pack_ex(cols, widths, ls, n, bs, als, fill=0x3C)
+    Ls = A.Layout(widths, ls, blocks=bs, aligned=als)
+    Ld = A.Layout(widths, ld, blocks=bd, aligned=ald)
+    got = run_remap(A, src, Ls, Ld, n)
+    exp = np.full(O.layout_bytes_ex(widths, ld, n, bd, ald), SENT, np.uint8)
+    O.remap_ex(src, ls, exp, ld, widths, n, bs, als, bd, ald)
+    if not np.array_equal(got, exp):
+        bad = np.nonzero(got != exp)[0]
+        raise AssertionError(f"mismatch at {bad.size} bytes, first {bad[:8]} (widths={widths} ls={ls} bs={bs} "
+                             f"als={als} ld={ld} bd={bd} ald={ald} n={n})")
+
+
+@pytest.mark.parametrize("case", [
+    ("AoS->AoSoA8", [4] * 8, [0] * 8, [1] * 8, False, [0] * 8, [8] * 8, False),
+    ("AoSoA32->SoA", config_widths(16), [0] * 16, [32] * 16, False, list(range(16)), [1] * 16, False),
+    ("SoA->aligned AoS", [1, 4, 2, 8, 4, 2], list(range(6)), [1] * 6, False, [0] * 6, [1] * 6, True),
+    ("aligned AoS->AoSoA4 hybrid", [1, 4, 2, 8, 4, 2], [0] * 6, [1] * 6, True, [0, 0, 1, 1, 2, 2], [4] * 6, True),
+    ("Medical AoSV@8 -> SoA", [4] * 9, [0, 0, 0, 1, 2, 3, 4, 5, 6], [8, 8, 8, 1, 1, 1, 1, 1, 1], False,
+     list(range(9)), [1] * 9, False),
+])
+def test_generalised_layouts(case, small_path):
+    _, widths, ls, bs, als, ld, bd, ald = case
+    T = A.plan_describe(A.Layout(widths, ls, blocks=bs, aligned=als), A.Layout(widths, ld, blocks=bd, aligned=ald))["T"]
+    for n in (1, 31, 33, T + 7, 5 * T + 19, 150 * T + 3):
+        check_pair_ex(widths, ls, bs, als, ld, bd, ald, n, seed=n)
+
+
+def test_generalised_random_pairs(monkeypatch):
+    import random as _r
+    monkeypatch.setenv("ADHA_SMALL_BYTES", "0")
+    rng = _r.Random(4859)
+    for trial in range(80):
+        F = rng.randint(1, 12)
+        widths = [rng.choice([1, 2, 3, 4, 4, 4, 6, 8, 8, 12]) for _ in range(F)]
+        ls = [rng.randrange(F) for _ in range(F)]
+        ld = [rng.randrange(F) for _ in range(F)]
+        cbs = {l: rng.choice([1, 1, 2, 4, 8, 32]) for l in set(ls)}
+        cbd = {l: rng.choice([1, 1, 2, 4, 8, 32]) for l in set(ld)}
+        bs, bd = [cbs[l] for l in ls], [cbd[l] for l in ld]
+        als, ald = rng.random() < 0.5, rng.random() < 0.5
+        T = A.plan_describe(A.Layout(widths, ls, blocks=bs, aligned=als), A.Layout(widths, ld, blocks=bd, aligned=ald))["T"]
+        n = rng.choice([T - 1, T + 5, 3 * T + rng.randrange(T), 160 * T + 11])
+        check_pair_ex(widths, ls, bs, als, ld, bd, ald, max(n, 1), seed=trial)
