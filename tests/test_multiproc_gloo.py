@@ -72,3 +72,21 @@ def test_two_rank_gloo_shards(scaling):
         assert np.array_equal(union, cols[f])                          # shard union == 1-process result
     assert ms == 2.5                                                   # max over ranks
     assert gbs == pytest.approx(2 * n_total * 80 * 10 / 2.5e-3 / 1e9)
+
+
+def test_bench_reference_arm_runs_on_cpu():
+    """bench.py --impl reference (the CPU oracle on the bench workload) prints one valid JSON line
+    with the contract's keys; no GPU needed."""
+    import json
+    import subprocess
+    import sys
+    from tests.conftest import ROOT
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
+                          "--warmup", "0"], capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    for key in ("impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+                "cpu_baseline", "e2e", "config"):
+        assert key in line, key
+    assert line["impl"] == "reference" and line["value"] > 0 and line["cpu_baseline"]["kind"] == "oracle"
+    assert line["e2e"]["h2d_bytes_per_step"] == 0
