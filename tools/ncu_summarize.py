@@ -1,0 +1,61 @@
+"""Export ncu --set full captures (gpurun_out/prof_<tag>_<cfg>.ncu-rep) into profiles/:
+<tag>_ncu_full_<cfg>_raw.csv, <tag>_ncu_full_<cfg>_details.csv, and the per-launch DRAM traffic
+table profiles/ncu_traffic.json that bench.py reports as roofline.traffic.
+
+usage: python tools/ncu_summarize.py <tag> [cfg ...]      (default cfgs: C2 C3 C4)
+"""
+import csv
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ALGO = {"C2": 2 * 10_000_000 * 80, "C3": 2 * 50_000_000 * 320, "C4": 2 * 59_652_323 * 36}
+SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-9, "us": 1e-6, "usecond": 1e-6,
+         "ms": 1e-3, "msecond": 1e-3, "nsecond": 1e-9, "s": 1.0, "%": 1.0}
+
+
+def export(rep, page):
+    return subprocess.run(["ncu", "-i", rep, "--page", page, "--csv"], capture_output=True, text=True,
+                          check=True).stdout
+
+
+def main():
+    tag = sys.argv[1]
+    cfgs = sys.argv[2:] or ["C2", "C3", "C4"]
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    table = json.load(open(path)) if os.path.exists(path) else {}
+    for cfg in cfgs:
+        rep = os.path.join(ROOT, "gpurun_out", f"prof_{tag}_{cfg}.ncu-rep")
+        raw = export(rep, "raw")
+        with open(os.path.join(ROOT, "profiles", f"{tag}_ncu_full_{cfg}_raw.csv"), "w") as f:
+            f.write(raw)
+        with open(os.path.join(ROOT, "profiles", f"{tag}_ncu_full_{cfg}_details.csv"), "w") as f:
+            f.write(export(rep, "details"))
+        rows = list(csv.reader(raw.splitlines()))
+        hdr, units, vals = rows[0], rows[1], rows[2]
+
+        def get(k):
+            i = hdr.index(k)
+            return float(vals[i].replace(",", "")) * SCALE.get(units[i], 1.0)
+
+        rd, wr = get("dram__bytes_read.sum"), get("dram__bytes_write.sum")
+        t = get("gpu__time_duration.sum")
+        table[cfg] = {
+            "kernel": vals[hdr.index("Kernel Name")],
+            "dram_bytes_read": rd, "dram_bytes_write": wr, "dram_bytes_per_launch": rd + wr,
+            "gpu_time_s": t,
+            "dram_pct_of_peak": get("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
+            "registers_per_thread": get("launch__registers_per_thread"),
+            "algorithmic_bytes_per_launch": ALGO[cfg],
+            "traffic_over_algorithmic": (rd + wr) / ALGO[cfg],
+            "source": f"profiles/{tag}_ncu_full_{cfg}_raw.csv (ncu --set full --clock-control none, one launch)",
+        }
+        print(cfg, json.dumps(table[cfg]))
+    with open(path, "w") as f:
+        json.dump(table, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()

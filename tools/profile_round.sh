@@ -8,7 +8,7 @@ out=gpurun_out
 timeout 900 python -m pytest tests -m gpu -q > $out/pytest_gpu_$tag.log 2>&1; echo "pytest=$?"
 python -c "import __graft_entry__ as g; g.smoke()" > $out/smoke_$tag.log 2>&1; echo "smoke=$?"
 python bench.py > $out/bench_$tag.json 2> $out/bench_$tag.err; echo "bench=$?"
-for c in C1 C3 C4 P1 P2; do
+for c in C1 C3 C4 C5 P1 P2; do
   python bench.py --config $c --no-cpu-baseline > $out/bench_${tag}_$c.json 2> $out/bench_${tag}_$c.err; echo "bench $c=$?"
 done
 python bench.py --impl reference --steps 3 --warmup 1 > $out/bench_${tag}_reference.json 2>&1; echo "reference=$?"
