@@ -173,6 +173,17 @@ def host_cores():
         return os.cpu_count() or 1
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 # ----------------------------------------------------------------------------------------- reference arm
 
 def run_reference(args, rank, world):
@@ -212,7 +223,7 @@ def run_reference(args, rank, world):
                    "note": "CPU oracle (oracle/remap_oracle.c, plain per-record per-field memcpy) on a bounded "
                            "sample of the workload; no GPU involved"},
         "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": cores, "kind": "oracle",
-                         "sample": f"first {sample} records of {name} per step"},
+                         "sample": f"first {sample} records of {name} per step", "cpu_model": cpu_model()},
         "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -321,6 +332,7 @@ def main():
 
     barrier()
     torch.cuda.synchronize(dev)
+    w0 = time.perf_counter()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record(stream)
@@ -329,10 +341,25 @@ def main():
     t1.record(stream)
     torch.cuda.synchronize(dev)
     barrier()
+    wall_ms = (time.perf_counter() - w0) * 1e3     # barrier-to-barrier host wall time (context only)
     clk = clocks.stop()
     ms_total = t0.elapsed_time(t1)
     ms_max = max_over_ranks(ms_total, dev)
+    wall_max = max_over_ranks(wall_ms, dev)
     value = aggregate_gbs(n_total, R, n_remaps, args.steps, ms_max)
+
+    # per-step spread, measured AFTER the timed region with an event pair around each step
+    # (not part of `value`; the per-step events would add their own gaps inside the timed loop)
+    reps = []
+    for _ in range(min(args.steps, 20)):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        step()
+        b.record(stream)
+        reps.append((a, b))
+    torch.cuda.synchronize(dev)
+    rep_ms = sorted(a.elapsed_time(b) for a, b in reps)
 
     # same-run torch copy_ of the same traffic (N*R bytes read + N*R written): the box's copy ceiling now
     copy_gbs = None
@@ -404,7 +431,7 @@ def main():
         cpu = {"value": v_all, "unit": "GB/s", "cores": cores, "kind": "oracle",
                "sample": f"first {sample} records of {name}, repeated for {s_all:.1f} s "
                          f"(oracle/remap_oracle.c, record-range split over {cores} threads)",
-               "single_thread_value": v_1}
+               "single_thread_value": v_1, "cpu_model": cpu_model()}
 
     if rank == 0:
         line = {
@@ -433,6 +460,9 @@ def main():
                                     "remap_tiled_kernel"),
                          "algorithmic_bytes_per_launch": 2 * n * R,
                          "avg_launch_ms": avg_launch_ms},
+            "step_ms_spread": {"median": statistics.median(rep_ms), "min": rep_ms[0], "max": rep_ms[-1],
+                               "reps": len(rep_ms), "note": "per-step events after the timed region, rank 0"},
+            "wall_ms_timed_region": wall_max,
             "gpu_launches": args.steps * n_remaps,
             "clocks": clk,
             "e2e": e2e,

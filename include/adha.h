@@ -229,6 +229,21 @@ ADHA_API adha_status adha_remap_sharded(const void* const* src_shards, const adh
                                int64_t n_records_total, int32_t n_shards,
                                const int32_t* device_ids, void* const* streams);
 
+/* Cross-device remap fused with the transfer (NEXT N2; the paper's
+ * remap edge crosses a device boundary; a device
+ * change moves all common fields).  src (bytes(Ls, N), device memory of src_device)
+ * is remapped into dst (bytes(Ld, N), device memory of dst_device) by ONE kernel
+ * running on src_device whose 16-byte stores go straight into dst_device's HBM over
+ * NVLink (peer access is enabled on first use and left enabled): no staging copy, the
+ * transfer overlaps the permutation tile by tile.  With src_device == dst_device it is
+ * adha_remap.  `stream` (void*, may be NULL) must belong to src_device.  The caller's
+ * current device is restored.  Ownership and asynchrony as adha_remap.
+ * Errors: as adha_remap; INVALID_ARG (device id out of range, a pointer not device
+ * memory of the stated device); CUDA (the two devices cannot access each other). */
+ADHA_API adha_status adha_remap_peer(const void* src, const adha_layout* src_layout, int32_t src_device,
+                                     void* dst, const adha_layout* dst_layout, int32_t dst_device,
+                                     int64_t n_records, void* stream);
+
 /* End-to-end remap of HOST buffers through the current device: src_host holds
  * bytes(Ls, N), dst_host receives bytes(Ld, N) (only payload bytes written).
  * Strategy (ADHA_HOST_MODE = auto | hybrid | zero | staged; auto = hybrid when dst_host

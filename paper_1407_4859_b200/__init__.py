@@ -60,6 +60,7 @@ _SIGS = {
     "adha_remap_sharded": (ctypes.c_int, [ctypes.POINTER(_vp), _L, ctypes.POINTER(_vp), _L, _i64, _i32,
                                           ctypes.POINTER(_i32), ctypes.POINTER(_vp)]),
     "adha_remap_host": (ctypes.c_int, [_vp, _L, _vp, _L, _i64, _vp, _u64, _vp]),
+    "adha_remap_peer": (ctypes.c_int, [_vp, _L, _i32, _vp, _L, _i32, _i64, _vp]),
     "adha_remap_plan_describe": (ctypes.c_int, [_L, _L, ctypes.POINTER(_vp)]),
     "adha_plan_ods": (ctypes.c_int, [_cp, _cp, _cp, _cp, ctypes.POINTER(_vp)]),
     "adha_plan_pdl": (ctypes.c_int, [_cp, _cp, _cp, ctypes.POINTER(_vp)]),
@@ -305,6 +306,22 @@ def remap_sharded(src_shards: Sequence, src_layout: Layout, dst_shards: Sequence
     st = (_vp * G)(*[_stream(x) for x in streams])
     _check(_lib.adha_remap_sharded(s, src_layout.handle, d, dst_layout.handle, int(n_records_total), G,
                                    _i32a(device_ids), st))
+
+
+def remap_peer(src, src_layout: Layout, dst, dst_layout: Layout, n_records: int, stream=None) -> None:
+    """Cross-device remap (adha_remap_peer): one kernel on src's device stores the records into
+    dst's device over NVLink.  `stream` (default: the current stream of src's device) must
+    belong to src's device."""
+    import torch
+    n = int(n_records)
+    if n > 0:
+        _check_size(src, src_layout.nbytes(n), "src")
+        _check_size(dst, dst_layout.nbytes(n), "dst")
+    sdev, ddev = src.device.index, dst.device.index
+    if stream is None:
+        stream = torch.cuda.current_stream(src.device)
+    _check(_lib.adha_remap_peer(_ptr(src), src_layout.handle, sdev, _ptr(dst), dst_layout.handle, ddev, n,
+                                _stream(stream)))
 
 
 def remap_host(src_host, src_layout: Layout, dst_host, dst_layout: Layout, n_records: int, scratch,

@@ -422,6 +422,72 @@ extern "C" adha_status adha_remap_sharded(const void* const* src_shards, const a
     return out;
 }
 
+// ---------------------------------------------------------------------------- cross-device (N2)
+// Push design: the kernel runs on the src device and its copy-out STG.128s address the
+// peer's HBM through the unified address space (NVLink 5 / NVSwitch).  Loads stay local
+// (TMA bulk copies from local HBM); only the dst bytes cross the link, once.
+namespace {
+
+std::mutex g_peer_mu;
+std::set<std::pair<int, int>> g_peer_enabled;
+
+adha_status check_device_pointer(const void* p, int device, const char* what) {
+    cudaPointerAttributes a{};
+    cudaError_t e = cudaPointerGetAttributes(&a, p);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaPointerGetAttributes");
+    if (a.type != cudaMemoryTypeDevice || a.device != device)
+        return fail(ADHA_ERR_INVALID_ARG, std::string(what) + " is not device memory of device " +
+                                              std::to_string(device));
+    return ADHA_OK;
+}
+
+adha_status enable_peer(int from, int to) {
+    std::lock_guard<std::mutex> lk(g_peer_mu);
+    if (g_peer_enabled.count({from, to})) return ADHA_OK;
+    int can = 0;
+    cudaError_t e = cudaDeviceCanAccessPeer(&can, from, to);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceCanAccessPeer");
+    if (!can)
+        return fail(ADHA_ERR_CUDA, "device " + std::to_string(from) + " cannot access device " +
+                                       std::to_string(to) + " (no P2P path)");
+    e = cudaDeviceEnablePeerAccess(to, 0);           // current device is `from`
+    if (e == cudaErrorPeerAccessAlreadyEnabled) {
+        cudaGetLastError();
+    } else if (e != cudaSuccess) {
+        return cuda_fail(e, "cudaDeviceEnablePeerAccess");
+    }
+    g_peer_enabled.insert({from, to});
+    return ADHA_OK;
+}
+
+}  // namespace
+
+extern "C" adha_status adha_remap_peer(const void* src, const adha_layout* hs, int32_t src_device, void* dst,
+                                       const adha_layout* hd, int32_t dst_device, int64_t n, void* stream) {
+    clear_error();
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
+    if (src_device < 0 || src_device >= count || dst_device < 0 || dst_device >= count)
+        return fail(ADHA_ERR_INVALID_ARG, "device id out of range (" + std::to_string(count) + " devices)");
+    int prev = 0;
+    e = cudaGetDevice(&prev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    e = cudaSetDevice(src_device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+    adha_status out = ADHA_OK;
+    if (n > 0 && src && dst) {
+        out = check_device_pointer(src, src_device, "src");
+        if (out == ADHA_OK) out = check_device_pointer(dst, dst_device, "dst");
+    }
+    if (out == ADHA_OK && src_device != dst_device) out = enable_peer(src_device, dst_device);
+    if (out == ADHA_OK) out = adha_remap(src, hs, dst, hd, n, stream);
+    std::string msg = adha_last_error();
+    cudaSetDevice(prev);
+    if (out != ADHA_OK) set_error(msg);
+    return out;
+}
+
 // ---------------------------------------------------------------------------- host end-to-end
 extern "C" adha_status adha_remap_plan_describe(const adha_layout* hs, const adha_layout* hd, char** json_out) {
     clear_error();

@@ -432,3 +432,44 @@ def test_generalised_random_pairs(monkeypatch):
         T = A.plan_describe(A.Layout(widths, ls, blocks=bs, aligned=als), A.Layout(widths, ld, blocks=bd, aligned=ald))["T"]
         n = rng.choice([T - 1, T + 5, 3 * T + rng.randrange(T), 160 * T + 11])
         check_pair_ex(widths, ls, bs, als, ld, bd, ald, max(n, 1), seed=trial)
+
+
+# ----------------------------------------------------------------------------- cross-device (NEXT N2)
+
+def test_remap_peer_same_device_and_errors():
+    """adha_remap_peer with src and dst on one device is adha_remap (bit-exact vs the oracle);
+    bad device ids and non-device pointers are rejected before any launch."""
+    widths = config_widths(16)
+    n = 300_001
+    aos, soa = [0] * 16, list(range(16))
+    cols = field_columns(5, n, widths)
+    src = O.pack(cols, widths, aos, n)
+    La, Ls = A.Layout(widths, aos), A.Layout(widths, soa)
+    d_src = to_dev(src)
+    d_dst = sentinel_dev(Ls.nbytes(n))
+    A.remap_peer(d_src, La, d_dst, Ls, n)
+    torch.cuda.synchronize()
+    assert np.array_equal(d_dst.cpu().numpy(), oracle_dst(src, aos, soa, widths, n))
+    lib = A._lib
+    nd = torch.cuda.device_count()
+    rc = lib.adha_remap_peer(d_src.data_ptr(), La.handle, 0, d_dst.data_ptr(), Ls.handle, nd, n, None)
+    assert A.STATUS[rc] == "ADHA_ERR_INVALID_ARG"
+    h = torch.empty(Ls.nbytes(n), dtype=torch.uint8).pin_memory()
+    rc = lib.adha_remap_peer(d_src.data_ptr(), La.handle, 0, h.data_ptr(), Ls.handle, 0, n, None)
+    assert A.STATUS[rc] == "ADHA_ERR_INVALID_ARG" and b"not device memory" in lib.adha_last_error()
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs two GPUs (peer access)")
+def test_remap_peer_two_devices():
+    """One kernel on cuda:0 stores the remapped records into cuda:1's HBM; bit-exact vs the oracle."""
+    widths = config_widths(16)
+    n = 1_000_003
+    aos, hyb = [0] * 16, [0, 0, 1, 1, 2, 2, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11]
+    cols = field_columns(6, n, widths)
+    src = O.pack(cols, widths, aos, n)
+    La, Lh = A.Layout(widths, aos), A.Layout(widths, hyb)
+    d_src = torch.from_numpy(src).to("cuda:0")
+    d_dst = torch.full((Lh.nbytes(n),), SENT, dtype=torch.uint8, device="cuda:1")
+    A.remap_peer(d_src, La, d_dst, Lh, n)
+    torch.cuda.synchronize(0)
+    assert np.array_equal(d_dst.cpu().numpy(), oracle_dst(src, aos, hyb, widths, n))
