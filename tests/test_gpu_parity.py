@@ -184,8 +184,10 @@ def test_c2_full_size_every_byte():
     assert np.array_equal(dst.cpu().numpy(), exp)
 
 
-def sampled_check(src, Ls_lab, dst, Ld_lab, widths, n, T, seed=0):
+def sampled_check(src, Ls_lab, dst, Ld_lab, widths, n, T, seed=0, extra=()):
     recs = sample_records(n, T, seed=seed)
+    if len(extra):
+        recs = np.unique(np.concatenate([recs, np.asarray([r for r in extra if 0 <= r < n], np.int64)]))
     bs, ss, os_, _ = O.field_addresses(widths, Ls_lab, n)
     bd, sd, od, tot = O.field_addresses(widths, Ld_lab, n)
     a = gather_fields_dev(src, widths, bs, ss, os_, recs)
@@ -212,6 +214,29 @@ def test_full_size_sampled(cfg):
     A.remap(src, Ls, dst, Ld, n)
     torch.cuda.synchronize()
     sampled_check(src, ls, dst, ld, widths, n, plan_T(widths, ls, ld))
+    del src, dst
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("widths", [[4, 4], [1, 2, 1]], ids=["unit4", "byte-groups"])
+def test_max_size_beyond_2_31_records(widths):
+    """Maximum sizes: N > 2^31 records, so record indices need 64 bits and region offsets pass
+    2^32 bytes (unit-4 permute path and byte-group path).  Sampled records around every 2^k
+    boundary that a 32-bit index or byte offset would break at."""
+    n = 2 ** 31 + 4099
+    F = len(widths)
+    aos, soa = [0] * F, list(range(F))
+    La, Ls = A.Layout(widths, aos), A.Layout(widths, soa)
+    src = torch.empty(La.nbytes(n), dtype=torch.uint8, device="cuda")
+    fill_random_device(src, SEED_BASE + 9)
+    dst = sentinel_dev(Ls.nbytes(n))
+    A.remap(src, La, dst, Ls, n)
+    torch.cuda.synchronize()
+    R = sum(widths)
+    edges = []
+    for b in (2 ** 30, 2 ** 31, 2 ** 32 // R, 2 ** 31 // R, 2 ** 32 // widths[0]):
+        edges += list(range(b - 40, b + 40))
+    sampled_check(src, aos, dst, soa, widths, n, plan_T(widths, aos, soa), extra=edges)
     del src, dst
     torch.cuda.empty_cache()
 
