@@ -91,57 +91,90 @@ def ncu_traffic(config):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 100 ms while running."""
+    """SM clock, power and clock-event (throttle) reasons sampled every ~2 ms through NVML while
+    running, so that a timed region of a few ms still gets samples; nvidia-smi (100 ms) if NVML
+    is unavailable."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap", "hw_power_brake")
 
-    def __init__(self, device_index):
+    def __init__(self, device_index, period_s=0.002):
         self.dev = device_index
-        self.proc = None
-        self.lines = []
+        self.period = period_s
+        self.samples = []          # (sm_mhz, power_w, set(reasons))
+        self.stop_ev = threading.Event()
+        self.max_mhz = None
+        self.source = None
+        self.t = None
+
+    def _nvml_handle(self):
+        import pynvml
+        pynvml.nvmlInit()
+        try:
+            import torch
+            pr = torch.cuda.get_device_properties(self.dev)
+            bus = "%08X:%02X:%02X.0" % (pr.pci_domain_id, pr.pci_bus_id, pr.pci_device_id)
+            return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.dev)
+
+    def _run_nvml(self, nv, h):
+        bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
+                "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
+                "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
+                "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap,
+                "hw_power_brake": nv.nvmlClocksEventReasonHwPowerBrakeSlowdown}
+        while not self.stop_ev.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                pw = nv.nvmlDeviceGetPowerUsage(h) / 1000.0
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append((float(sm), pw, {k for k, b in bits.items() if r & b}))
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def _run_smi(self):
+        q = ("clocks.sm,power.draw,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,"
+             "clocks_event_reasons.hw_power_brake_slowdown")
+        p = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms", "100",
+                              "-i", str(self.dev)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        for ln in p.stdout:
+            if self.stop_ev.is_set():
+                break
+            parts = [x.strip() for x in ln.split(",")]
+            try:
+                self.samples.append((float(parts[0]), float(parts[1]),
+                                     {n for n, v in zip(self.NAMES, parts[2:7]) if v.lower() == "active"}))
+            except (ValueError, IndexError):
+                continue
+        p.terminate()
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                                          "-lms", "100", "-i", str(self.dev)],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
+            nv, h = self._nvml_handle()
+            self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+            self.source = "nvml, 2 ms"
+            self.t = threading.Thread(target=self._run_nvml, args=(nv, h), daemon=True)
         except Exception:
-            self.proc = None
+            self.source = "nvidia-smi, 100 ms"
+            self.t = threading.Thread(target=self._run_smi, daemon=True)
+        self.t.start()
 
-    def _read(self):
-        for ln in self.proc.stdout:
-            self.lines.append(ln.strip())
+    def count(self):
+        return len(self.samples)
 
     def stop(self):
-        if self.proc is None:
+        self.stop_ev.set()
+        if self.t is not None:
+            self.t.join(timeout=5)
+        if not self.samples:
             return None
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except Exception:
-            self.proc.kill()
-        self.t.join(timeout=2)
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [x.strip() for x in ln.split(",")]
-            if len(parts) < 9:
-                continue
-            try:
-                sm.append(float(parts[1]))
-                mx = float(parts[2])
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[5:9]):
-                if v.lower() == "active":
-                    reasons.add(nm)
-        if not sm:
-            return None
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        sm = [x[0] for x in self.samples]
+        reasons = set().union(*[x[2] for x in self.samples])
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": self.max_mhz, "sm_min_mhz": min(sm),
+                "power_w_median": statistics.median(x[1] for x in self.samples),
+                "reasons": sorted(reasons), "samples": len(sm), "source": self.source}
 
 
 def oracle_rate(widths, chain, sample_records, seconds, threads):
@@ -244,7 +277,11 @@ def main():
     ap.add_argument("--no-copy-ref", action="store_true")
     ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
                     help="replay the step as a CUDA graph (auto: when a step moves < 256 MB, i.e. launch-bound)")
-    ap.add_argument("--soak-s", type=float, default=1.5, help="untimed load before the timed region (clock sampling)")
+    ap.add_argument("--soak-s", type=float, default=0.0,
+                    help="untimed load before the timed region (0: burst regime, like the burst copy peak)")
+    ap.add_argument("--sustained-s", type=float, default=3.0,
+                    help="after the main measurement: this long untimed under load, then K steps timed again "
+                         "(power-capped sustained regime, reported as `sustained`; 0 disables)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -322,16 +359,17 @@ def main():
         step()
     torch.cuda.synchronize(dev)
 
-    clocks = ClockSampler(local)
-    clocks.start()
     t_end = time.perf_counter() + args.soak_s
-    while time.perf_counter() < t_end:              # untimed soak so the sampler sees the load
+    while time.perf_counter() < t_end:              # optional untimed soak (default 0: burst regime)
         for _ in range(10):
             step()
         torch.cuda.synchronize(dev)
 
     barrier()
     torch.cuda.synchronize(dev)
+    clocks = ClockSampler(local)                    # samples DURING the timed region
+    clocks.start()
+    time.sleep(0.005)
     w0 = time.perf_counter()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
@@ -342,7 +380,15 @@ def main():
     torch.cuda.synchronize(dev)
     barrier()
     wall_ms = (time.perf_counter() - w0) * 1e3     # barrier-to-barrier host wall time (context only)
+    n_in_region = clocks.count()
+    extend_t = time.perf_counter() + 0.5
+    while clocks.count() < 5 and time.perf_counter() < extend_t:   # region too short for 5 samples:
+        for _ in range(10):                                        # keep the same load on, untimed
+            step()
+        torch.cuda.synchronize(dev)
     clk = clocks.stop()
+    if clk is not None:
+        clk["samples_in_timed_region"] = n_in_region
     ms_total = t0.elapsed_time(t1)
     ms_max = max_over_ranks(ms_total, dev)
     wall_max = max_over_ranks(wall_ms, dev)
@@ -363,6 +409,7 @@ def main():
 
     # same-run torch copy_ of the same traffic (N*R bytes read + N*R written): the box's copy ceiling now
     copy_gbs = None
+    ca = cb = None
     if n > 0 and not args.no_copy_ref:
         ca = torch.empty(n * R, dtype=torch.uint8, device=dev)
         cb = torch.empty_like(ca)
@@ -376,7 +423,41 @@ def main():
         c1.record(stream)
         torch.cuda.synchronize(dev)
         copy_gbs = 2 * n * R * args.steps / (c0.elapsed_time(c1) * 1e-3) / 1e9
-        del ca, cb
+
+    def sustained_leg(fn, bytes_per_call):
+        """fn back to back for --sustained-s seconds (untimed; the board reaches its power-capped
+        steady state), then K calls timed with events while NVML samples the clocks."""
+        t_end = time.perf_counter() + args.sustained_s
+        while time.perf_counter() < t_end:
+            for _ in range(10):
+                fn()
+            torch.cuda.synchronize(dev)
+        barrier()
+        cs = ClockSampler(local)
+        cs.start()
+        time.sleep(0.005)
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.steps):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize(dev)
+        barrier()
+        ms = max_over_ranks(a.elapsed_time(b), dev)
+        return bytes_per_call * args.steps * world / (ms * 1e-3) / 1e9, cs.stop()
+
+    sustained = None
+    if args.sustained_s > 0 and n > 0:
+        v_s, clk_s = sustained_leg(step, 2 * n * R * n_remaps)
+        sustained = {"value": v_s, "unit": "GB/s", "clocks": clk_s,
+                     "note": f"after {args.sustained_s:.1f} s of untimed load (board power cap engaged); "
+                             "K steps timed with events, max over ranks"}
+        if ca is not None:
+            c_s, cclk_s = sustained_leg(lambda: cb.copy_(ca), 2 * n * R)
+            sustained["copy_gbs"] = c_s / world
+            sustained["copy_clocks"] = cclk_s
+    del ca, cb
 
     # roofline of the dominant kernel (the remap kernel is the only kernel in the step)
     peak, peak_src = measured_peak()
@@ -444,7 +525,12 @@ def main():
                 "record_bytes": R, "remaps_per_step": n_remaps,
                 "layouts": [l.to_string() for l in layouts],
                 "bytes_per_step_total": 2 * n_total * R * n_remaps,
-                "l2": f"inputs larger than L2 ({2 * n * R / 1e9:.2f} GB moved per remap per GPU vs 126 MB L2); no flush",
+                "l2": (f"inputs larger than L2 ({2 * n * R / 1e9:.2f} GB moved per remap per GPU vs 126 MB L2); no flush"
+                       if 2 * n * R > (252 << 20) else
+                       f"inputs fit in L2 ({2 * n * R} B per remap; no flush): latency-bound config, not a "
+                       "bandwidth claim"),
+                "timing_regime": ("burst: timed right after the warm-up, like the burst copy peak"
+                                  if args.soak_s <= 0 else f"after a {args.soak_s:.1f} s untimed soak"),
                 "parallelism": f"shard by contiguous record range over {world} GPU(s), no data-path collective",
                 "kernel": {k: plan[k] for k in ("tiled", "unit", "T", "s_in", "s_out", "smem_bytes", "matched")},
                 "cuda_graph": use_graph,
@@ -460,6 +546,7 @@ def main():
                                     "remap_tiled_kernel"),
                          "algorithmic_bytes_per_launch": 2 * n * R,
                          "avg_launch_ms": avg_launch_ms},
+            "sustained": sustained,
             "step_ms_spread": {"median": statistics.median(rep_ms), "min": rep_ms[0], "max": rep_ms[-1],
                                "reps": len(rep_ms), "note": "per-step events after the timed region, rank 0"},
             "wall_ms_timed_region": wall_max,

@@ -1,0 +1,65 @@
+"""bench.py on a GPU: the JSON line keeps the driver's contract (keys, units, clocks sampled in the
+timed region, roofline, e2e, gpu_launches), and the torchrun multi-rank path (ranks sharing the one
+GPU through ADHA_BENCH_SHARE_GPU; their kernels never wait on one another) reports the max over
+ranks with weak scaling."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+from tests.conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+KEYS = ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+        "vs_baseline", "dtype", "data", "config", "roofline", "gpu_launches", "clocks", "e2e", "cpu_baseline")
+
+
+def run_bench(args, env=None, torchrun=0):
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py")] + args
+    if torchrun:
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={torchrun}",
+               "--master-addr", "127.0.0.1", "--master-port", "29571", os.path.join(ROOT, "bench.py")] + args
+    e = dict(os.environ)
+    e.update(env or {})
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=e)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    return json.loads(lines[0])
+
+
+def test_bench_c2_contract():
+    d = run_bench(["--steps", "20", "--warmup", "3", "--sustained-s", "0.3", "--no-cpu-baseline"])
+    for k in KEYS:
+        assert k in d, k
+    assert d["metric"] == "remap GB/s (read+write)" and d["unit"] == "GB/s" and d["dtype"] == "u8"
+    assert d["n_gpus"] == 1 and d["steps"] == 20 and d["higher_is_better"] is True
+    assert d["config"]["workload"].startswith("C2") and d["vs_baseline"] is None
+    r = d["roofline"]
+    assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0 < r["frac"] < 1.2
+    assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
+    assert d["gpu_launches"] == 20
+    assert d["clocks"]["samples"] >= 5 and d["clocks"]["sm_mhz"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] == 10_000_000 * 80 == d["e2e"]["d2h_bytes_per_step"]
+    assert d["sustained"]["value"] > 0 and d["sustained"]["copy_gbs"] > 0
+    assert d["value"] > 1000          # a B200 moves well over 1 TB/s through the remap
+
+
+def test_bench_c1_graph():
+    d = run_bench(["--config", "C1", "--steps", "50", "--warmup", "3", "--sustained-s", "0", "--no-cpu-baseline"])
+    assert d["config"]["cuda_graph"] is True and d["gpu_launches"] == 100
+    assert "fit in L2" in d["config"]["l2"]
+
+
+def test_bench_two_ranks_share_gpu():
+    d = run_bench(["--gpus", "2", "--steps", "5", "--warmup", "3", "--sustained-s", "0", "--no-e2e",
+                   "--no-copy-ref"], env={"ADHA_BENCH_SHARE_GPU": "1"}, torchrun=2)
+    assert d["n_gpus"] == 2 and d["scaling"] == "weak"
+    assert d["config"]["n_records_total"] == 2 * d["config"]["n_records_per_rank"]
