@@ -206,6 +206,28 @@ def host_cores():
         return os.cpu_count() or 1
 
 
+def planner_times():
+    """Host planner cost, off the timed path: the C++ ODS of the C3 program
+    (64 fields, 2016 pairs, cap 128 B) and the C++ PDL of the Medical fixture (7 sections x 2
+    devices, 56 run nodes); median of 20 calls each, in ms, with the JSON passed as text."""
+    import paper_1407_4859_b200 as A
+    from tests.conftest import golden
+
+    def med(fn):
+        ts = []
+        for _ in range(20):
+            a = time.perf_counter()
+            fn()
+            ts.append((time.perf_counter() - a) * 1e3)
+        return statistics.median(ts)
+    c3p, b200 = json.dumps(golden("c3_program.json")), json.dumps(golden("b200_arch.json"))
+    mp, ma, mprof = (json.dumps(golden(x)) for x in ("medical_program.json", "medical_arch.json",
+                                                      "medical_profile.json"))
+    return {"ods_c3_ms": med(lambda: A.plan_ods(c3p, b200, "c3", "b200")),
+            "pdl_medical_ms": med(lambda: A.plan_pdl(mp, ma, mprof)),
+            "note": "C++ planner in libadha, host only, off the timed path"}
+
+
 def cpu_model():
     try:
         with open("/proc/cpuinfo") as f:
@@ -547,6 +569,7 @@ def main():
                          "algorithmic_bytes_per_launch": 2 * n * R,
                          "avg_launch_ms": avg_launch_ms},
             "sustained": sustained,
+            "planner": planner_times(),
             "step_ms_spread": {"median": statistics.median(rep_ms), "min": rep_ms[0], "max": rep_ms[-1],
                                "reps": len(rep_ms), "note": "per-step events after the timed region, rank 0"},
             "wall_ms_timed_region": wall_max,
