@@ -10,6 +10,7 @@
 #include <array>
 #include <cstdlib>
 #include <climits>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <numeric>
@@ -291,10 +292,9 @@ RemapPlan compile_plan(const Layout& ls, const Layout& ld) {
             for (size_t i = 0; i < K.dst_clusters.size(); ++i) dpad[P.dst_slot[K.dst_clusters[i]]] = 32 * i;
             max_chunks = std::max(max_chunks, std::max(K.src_clusters.size(), K.dst_clusters.size()));
         }
+        std::vector<std::vector<ByteGroup>> cgs(P.comps.size());
         for (size_t ki = 0; ki < P.comps.size(); ++ki) {
             auto& K = P.comps[ki];
-            base[ki] = (uint32_t)groups.size();
-            count[ki] = 0;
             if (K.identity) continue;
             // the output words of one 32-record period with the source word of each byte
             std::vector<OW> ows;
@@ -390,46 +390,65 @@ RemapPlan compile_plan(const Layout& ls, const Layout& ld) {
                 }
                 comp_groups.push_back(gr);
             }
-            // instruction order: fill each 32-lane instruction greedily with groups whose source
-            // words and output words can be put in slots (the m-th load / o-th store of all lanes)
-            // whose banks (period 0) are still unused in that instruction -- the slot order inside a
-            // group is free, so try every permutation of it
-            auto sbank = [&](const ByteGroup& x, int m) { return ((spad[x.src_sc[m]] + x.src_off[m]) / 4) % 32; };
-            auto obank = [&](const ByteGroup& x, int o) { return ((dpad[x.out_dc[o]] + x.out_off[o]) / 4) % 32; };
-            // one greedy pass over the remaining groups in `cand` order: picks conflict-free groups
-            // (with their slot permutations) until 32 or the candidates run out
-            auto greedy = [&](const std::vector<size_t>& cand, std::vector<size_t>& pick,
-                              std::vector<std::array<int, 8>>& perms) {
-                uint32_t used_s[4] = {0, 0, 0, 0}, used_o[4] = {0, 0, 0, 0};
-                for (size_t i : cand) {
-                    if (pick.size() == 32) break;
-                    const ByteGroup& gr = comp_groups[i];
-                    int ps[4] = {0, 1, 2, 3}, po[4] = {0, 1, 2, 3};
-                    bool ok_s = false, ok_o = false;
-                    do {
-                        bool ok = true;
-                        for (int m = 0; m < gr.n_src && ok; ++m) ok = !(used_s[ps[m]] >> sbank(gr, m) & 1u);
-                        if (ok) { ok_s = true; break; }
-                    } while (std::next_permutation(ps, ps + gr.n_src));
-                    if (!ok_s) continue;
-                    do {
-                        bool ok = true;
-                        for (int o = 0; o < gr.n_out && ok; ++o) ok = !(used_o[po[o]] >> obank(gr, o) & 1u);
-                        if (ok) { ok_o = true; break; }
-                    } while (std::next_permutation(po, po + gr.n_out));
-                    if (!ok_o) continue;
-                    for (int m = 0; m < gr.n_src; ++m) used_s[ps[m]] |= 1u << sbank(gr, m);
-                    for (int o = 0; o < gr.n_out; ++o) used_o[po[o]] |= 1u << obank(gr, o);
-                    pick.push_back(i);
-                    perms.push_back({ps[0], ps[1], ps[2], ps[3], po[0], po[1], po[2], po[3]});
-                }
-            };
-            std::vector<char> taken(comp_groups.size(), 0);
-            size_t left = comp_groups.size();
+            cgs[ki] = std::move(comp_groups);
+        }
+        // instruction order: fill each 32-lane instruction greedily with groups whose source
+        // words and output words can be put in slots (the m-th load / o-th store of all lanes)
+        // whose banks are still unused in that instruction -- the slot order inside a group is
+        // free, so try every permutation of it.  All lanes of an instruction are at the same
+        // period q, and a word's bank moves by 8 * stride words per period, so banks are
+        // checked at every phase q = 0..3 (the shift pattern repeats with period 4): clusters
+        // of stride 2 (mod 4) and 0 (mod 4) in one instruction collide on odd periods otherwise.
+        auto sbank = [&](const ByteGroup& x, int m, int q) {
+            const uint32_t h = (8u * (uint32_t)ls.stride[P.src_order[x.src_sc[m]]]) & 31u;
+            return ((spad[x.src_sc[m]] + x.src_off[m]) / 4 + q * h) % 32;
+        };
+        auto obank = [&](const ByteGroup& x, int o, int q) {
+            const uint32_t h = (8u * (uint32_t)ld.stride[P.dst_order[x.out_dc[o]]]) & 31u;
+            return ((dpad[x.out_dc[o]] + x.out_off[o]) / 4 + q * h) % 32;
+        };
+        // one greedy pass over the remaining groups in `cand` order: picks conflict-free groups
+        // (with their slot permutations) until 32 or the candidates run out
+        auto greedy = [&](const std::vector<ByteGroup>& cg, const std::vector<size_t>& cand, std::vector<size_t>& pick,
+                          std::vector<std::array<int, 8>>& perms) {
+            uint32_t used_s[4][4] = {}, used_o[4][4] = {};     // [slot][phase] bank masks
+            for (size_t i : cand) {
+                if (pick.size() == 32) break;
+                const ByteGroup& gr = cg[i];
+                int ps[4] = {0, 1, 2, 3}, po[4] = {0, 1, 2, 3};
+                bool ok_s = false, ok_o = false;
+                do {
+                    bool ok = true;
+                    for (int m = 0; m < gr.n_src && ok; ++m)
+                        for (int q = 0; q < 4 && ok; ++q) ok = !(used_s[ps[m]][q] >> sbank(gr, m, q) & 1u);
+                    if (ok) { ok_s = true; break; }
+                } while (std::next_permutation(ps, ps + gr.n_src));
+                if (!ok_s) continue;
+                do {
+                    bool ok = true;
+                    for (int o = 0; o < gr.n_out && ok; ++o)
+                        for (int q = 0; q < 4 && ok; ++q) ok = !(used_o[po[o]][q] >> obank(gr, o, q) & 1u);
+                    if (ok) { ok_o = true; break; }
+                } while (std::next_permutation(po, po + gr.n_out));
+                if (!ok_o) continue;
+                for (int m = 0; m < gr.n_src; ++m)
+                    for (int q = 0; q < 4; ++q) used_s[ps[m]][q] |= 1u << sbank(gr, m, q);
+                for (int o = 0; o < gr.n_out; ++o)
+                    for (int q = 0; q < 4; ++q) used_o[po[o]][q] |= 1u << obank(gr, o, q);
+                pick.push_back(i);
+                perms.push_back({ps[0], ps[1], ps[2], ps[3], po[0], po[1], po[2], po[3]});
+            }
+        };
+        // Dense packing (the fallback when the balanced tables below exceed the parameter space):
+        // the largest conflict-free pick of each instruction is topped up with the next groups.
+        auto pack = [&](std::vector<ByteGroup> cg, size_t ki) {
+            std::vector<ByteGroup> out;
+            std::vector<char> taken(cg.size(), 0);
+            size_t left = cg.size();
             uint64_t rng = 0x9E3779B97F4A7C15ull ^ (uint64_t)ki;
             while (left) {
                 std::vector<size_t> remaining;
-                for (size_t i = 0; i < comp_groups.size(); ++i)
+                for (size_t i = 0; i < cg.size(); ++i)
                     if (!taken[i]) remaining.push_back(i);
                 // natural order first, then seeded shuffles; keep the largest conflict-free pick
                 std::vector<size_t> best_pick;
@@ -448,20 +467,158 @@ RemapPlan compile_plan(const Layout& ls, const Layout& ld) {
                     }
                     std::vector<size_t> pick;
                     std::vector<std::array<int, 8>> perms;
-                    greedy(cand, pick, perms);
+                    greedy(cg, cand, pick, perms);
                     if (pick.size() > best_pick.size()) { best_pick = pick; best_perms = perms; }
                 }
                 for (size_t t = 0; t < best_pick.size(); ++t) {
                     const auto& pp = best_perms[t];
-                    permute_group(comp_groups[best_pick[t]], pp.data(), pp.data() + 4);
+                    permute_group(cg[best_pick[t]], pp.data(), pp.data() + 4);
                     taken[best_pick[t]] = 1;
                 }
                 for (size_t i : remaining)
                     if (best_pick.size() < 32 && !taken[i]) { best_pick.push_back(i); taken[i] = 1; }
-                for (size_t i : best_pick) groups.push_back(comp_groups[i]);
+                for (size_t i : best_pick) out.push_back(cg[i]);
                 left -= best_pick.size();
             }
-            count[ki] = (uint32_t)comp_groups.size();
+            return out;
+        };
+        // Packing into exactly I instructions: groups go one by one to the instruction (and slot
+        // permutation) that adds the fewest shared-memory wavefronts over the four period phases;
+        // lanes an instruction cannot use conflict-free may stay idle (empty groups).  Returns
+        // the groups in instruction order and the wavefronts per 4 periods in *cost.
+        auto pack_fixed = [&](std::vector<ByteGroup> cg, size_t ki, uint32_t I, uint64_t* cost) {
+            uint64_t rng = 0xD1B54A32D192ED03ull ^ (uint64_t)ki ^ ((uint64_t)I << 32);
+            std::vector<size_t> order(cg.size());
+            std::iota(order.begin(), order.end(), size_t(0));
+            std::vector<ByteGroup> best;
+            uint64_t best_cost = ~uint64_t(0);
+            for (int attempt = 0; attempt < 4; ++attempt) {
+                if (attempt) {
+                    for (size_t i = order.size(); i > 1; --i) {       // Fisher-Yates with splitmix64
+                        rng += 0x9E3779B97F4A7C15ull;
+                        uint64_t z = rng;
+                        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+                        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+                        z ^= z >> 31;
+                        std::swap(order[i - 1], order[z % i]);
+                    }
+                }
+                // per instruction: bank counts [slot][phase][bank] and their maxima [slot][phase]
+                std::vector<std::array<uint8_t, 512>> cs(I), co(I);
+                std::vector<std::array<uint8_t, 16>> ms(I), mo(I);
+                for (uint32_t i = 0; i < I; ++i) { cs[i].fill(0); co[i].fill(0); ms[i].fill(0); mo[i].fill(0); }
+                std::vector<std::vector<ByteGroup>> lanes(I);
+                bool ok = true;
+                for (size_t gi : order) {
+                    const ByteGroup& gr = cg[gi];
+                    int bi = -1, bps[4] = {0, 1, 2, 3}, bpo[4] = {0, 1, 2, 3};
+                    uint32_t bd = ~0u;
+                    for (uint32_t i = 0; i < I; ++i) {
+                        if (lanes[i].size() >= 32) continue;
+                        uint32_t ds = ~0u, dout = ~0u;
+                        int ps[4] = {0, 1, 2, 3}, po[4] = {0, 1, 2, 3}, ps_b[4] = {0, 1, 2, 3}, po_b[4] = {0, 1, 2, 3};
+                        do {
+                            uint32_t d = 0;
+                            for (int m = 0; m < gr.n_src; ++m)
+                                for (int q = 0; q < 4; ++q)
+                                    d += cs[i][(ps[m] * 4 + q) * 32 + sbank(gr, m, q)] >= ms[i][ps[m] * 4 + q];
+                            if (d < ds) { ds = d; std::copy(ps, ps + 4, ps_b); }
+                        } while (ds && std::next_permutation(ps, ps + gr.n_src));
+                        do {
+                            uint32_t d = 0;
+                            for (int o = 0; o < gr.n_out; ++o)
+                                for (int q = 0; q < 4; ++q)
+                                    d += co[i][(po[o] * 4 + q) * 32 + obank(gr, o, q)] >= mo[i][po[o] * 4 + q];
+                            if (d < dout) { dout = d; std::copy(po, po + 4, po_b); }
+                        } while (dout && std::next_permutation(po, po + gr.n_out));
+                        // fewest added wavefronts, then the emptier instruction
+                        const uint32_t key = ((ds + dout) << 8) | (uint32_t)lanes[i].size();
+                        if (key < bd) {
+                            bd = key;
+                            bi = (int)i;
+                            std::copy(ps_b, ps_b + 4, bps);
+                            std::copy(po_b, po_b + 4, bpo);
+                        }
+                    }
+                    if (bi < 0) { ok = false; break; }
+                    ByteGroup h = gr;
+                    permute_group(h, bps, bpo);
+                    for (int m = 0; m < h.n_src; ++m)
+                        for (int q = 0; q < 4; ++q) {
+                            uint8_t& c = cs[bi][(m * 4 + q) * 32 + sbank(h, m, q)];
+                            ms[bi][m * 4 + q] = std::max<uint8_t>(ms[bi][m * 4 + q], ++c);
+                        }
+                    for (int o = 0; o < h.n_out; ++o)
+                        for (int q = 0; q < 4; ++q) {
+                            uint8_t& c = co[bi][(o * 4 + q) * 32 + obank(h, o, q)];
+                            mo[bi][o * 4 + q] = std::max<uint8_t>(mo[bi][o * 4 + q], ++c);
+                        }
+                    lanes[bi].push_back(h);
+                }
+                if (!ok) continue;
+                uint64_t c = 0;
+                for (uint32_t i = 0; i < I; ++i)
+                    for (int x = 0; x < 16; ++x) c += ms[i][x] + mo[i][x];
+                if (c < best_cost) {
+                    best_cost = c;
+                    best.clear();
+                    ByteGroup idle;
+                    std::memset(&idle, 0, sizeof idle);
+                    for (uint32_t i = 0; i < I; ++i) {
+                        best.insert(best.end(), lanes[i].begin(), lanes[i].end());
+                        if (i + 1 < I) best.resize(best.size() + (32 - lanes[i].size()), idle);
+                    }
+                }
+            }
+            *cost = best_cost;
+            return best;
+        };
+        {
+            // per component: the instruction count with the smallest estimated busiest-warp time;
+            // if the tables do not fit the parameter space, the dense packing instead
+            groups.clear();
+            bool fits = true;
+            for (size_t ki = 0; ki < P.comps.size() && fits; ++ki) {
+                base[ki] = (uint32_t)groups.size();
+                count[ki] = 0;
+                if (cgs[ki].empty()) continue;
+                // Per tile, the kernel gives instruction i's periods to gP = NCONS*GMAX / I warp
+                // slots; the busiest warp holds ceil(I*gP / NCONS) slots of P/gP periods each.
+                // Estimated busiest-warp time per period: slots/gP * (wavefronts per instruction-
+                // period + an issue term for the PRMT/address work), minimised over I.
+                const uint32_t I_min = (uint32_t)((cgs[ki].size() + 31) / 32);
+                const uint32_t S = (uint32_t)(NCONS * GCLASS_GMAX[1]);
+                std::vector<ByteGroup> v;
+                double vt = 1e300;
+                auto busy = [&](uint32_t I) {
+                    const uint32_t gP = std::max<uint32_t>(1, S / I);
+                    return (double)((I * gP + NCONS - 1) / NCONS) / gP;
+                };
+                for (uint32_t I = I_min; I <= S; ++I) {
+                    const double busiest = busy(I);
+                    // same busiest-warp load with more instructions = more room for conflict-free
+                    // lanes: only the largest I of each load class is tried
+                    if (I < S && busy(I + 1) == busiest) continue;
+                    if (busiest * 8.0 >= vt) continue;     // >= 1 load + 1 store wavefront: cannot win
+                    uint64_t c = 0;
+                    std::vector<ByteGroup> w = pack_fixed(cgs[ki], ki, I, &c);
+                    if (w.empty() || groups.size() + w.size() > (size_t)GCLASS_NG[1]) continue;
+                    const double t = busiest * ((double)c / (4.0 * I) + 6.0);
+                    if (t < vt) { vt = t; v = std::move(w); }
+                }
+                if (v.empty()) { fits = false; break; }
+                count[ki] = (uint32_t)v.size();
+                groups.insert(groups.end(), v.begin(), v.end());
+            }
+            if (!fits || groups.size() > (size_t)GCLASS_NG[1]) {
+                groups.clear();
+                for (size_t ki = 0; ki < P.comps.size(); ++ki) {
+                    base[ki] = (uint32_t)groups.size();
+                    std::vector<ByteGroup> v = pack(cgs[ki], ki);
+                    count[ki] = (uint32_t)v.size();
+                    groups.insert(groups.end(), v.begin(), v.end());
+                }
+            }
         }
         // class: all groups fit, and every component's slots fit GMAX per warp
         int gcls = -1;
