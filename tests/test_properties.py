@@ -1,0 +1,139 @@
+"""Property-based checks (hypothesis, CPU only) of the oracle and the C ABI's host logic, over
+random widths, partitions, AoSoA blocks, alignment and record counts.  Each property is one the
+paper's data model fixes: the remap is a bijection on payload bytes,
+composes, round-trips, equals a structured-array view, and the C ABI's descriptor places every
+field where the (independently written) oracle address model does."""
+import numpy as np
+import pytest
+from hypothesis import HealthCheck, given, settings
+from hypothesis import strategies as st
+
+from oracle import remap as O
+
+A = pytest.importorskip("paper_1407_4859_b200")
+
+SET = settings(max_examples=60, deadline=None, suppress_health_check=[HealthCheck.too_slow])
+
+
+@st.composite
+def layouts(draw, max_fields=7):
+    F = draw(st.integers(1, max_fields))
+    widths = draw(st.lists(st.sampled_from([1, 2, 3, 4, 6, 8, 12, 16]), min_size=F, max_size=F))
+    return widths
+
+
+@st.composite
+def partition(draw, F):
+    labels = draw(st.lists(st.integers(0, F - 1), min_size=F, max_size=F))
+    return labels
+
+
+@st.composite
+def layout_triple(draw):
+    widths = draw(layouts())
+    F = len(widths)
+    parts = [draw(partition(F)) for _ in range(3)]
+    n = draw(st.sampled_from([0, 1, 2, 31, 32, 33, 100, 257]))
+    return widths, parts, n
+
+
+def _random_src(widths, labels, n, seed):
+    rng = np.random.default_rng(seed)
+    cols = [rng.integers(0, 256, size=(n, w), dtype=np.uint8) for w in widths]
+    return cols, O.pack(cols, widths, labels, n)
+
+
+@SET
+@given(layout_triple(), st.integers(0, 2 ** 31))
+def test_oracle_round_trip_and_composition(t, seed):
+    widths, (l1, l2, l3), n = t
+    cols, src = _random_src(widths, l1, n, seed)
+    b2 = np.zeros(O.layout_bytes(widths, l2, n), np.uint8)
+    b3 = np.zeros(O.layout_bytes(widths, l3, n), np.uint8)
+    O.remap(src, l1, b2, l2, widths, n)
+    O.remap(b2, l2, b3, l3, widths, n)
+    direct = np.zeros_like(b3)
+    O.remap(src, l1, direct, l3, widths, n)
+    assert np.array_equal(b3, direct)                       # L1 -> L2 -> L3 == L1 -> L3
+    back = np.zeros(O.layout_bytes(widths, l1, n), np.uint8)
+    O.remap(b2, l2, back, l1, widths, n)
+    mask = O.payload_mask(widths, l1, n)
+    assert np.array_equal(back[mask], src[mask])           # round trip restores every payload byte
+    for f, c in enumerate(O.unpack(b3, widths, l3, n)):
+        assert np.array_equal(c, cols[f])                   # fields land where the layout says
+
+
+@SET
+@given(layouts(), st.data())
+def test_oracle_is_a_numpy_structured_view(widths, data):
+    """A packed cluster record is a numpy structured dtype with V<w> fields at the packed offsets;
+    its region is the contiguous array of those records (SURVEY 8(c) pin (i))."""
+    F = len(widths)
+    labels = data.draw(partition(F))
+    n = data.draw(st.integers(0, 50))
+    cols, buf = _random_src(widths, labels, n, data.draw(st.integers(0, 999)))
+    base, stride, off, _ = O.field_addresses(widths, labels, n)
+    for f in range(F):
+        members = [g for g in range(F) if labels[g] == labels[f]]
+        dt = np.dtype({"names": [f"f{g}" for g in members], "formats": [f"V{widths[g]}" for g in members],
+                       "offsets": [int(off[g]) for g in members], "itemsize": int(stride[f])})
+        region = buf[int(base[f]): int(base[f]) + n * int(stride[f])].view(dt) if n else np.zeros(0, dt)
+        got = np.frombuffer(np.ascontiguousarray(region[f"f{f}"]).tobytes(), np.uint8).reshape(n, widths[f])
+        assert np.array_equal(got, cols[f])
+
+
+@SET
+@given(layouts(max_fields=9), st.data())
+def test_capi_descriptor_matches_oracle_address_model(widths, data):
+    F = len(widths)
+    labels = data.draw(partition(F))
+    blocks = data.draw(st.one_of(st.none(), st.lists(st.sampled_from([1, 2, 4, 8, 16, 32]), min_size=F,
+                                                     max_size=F)))
+    aligned = data.draw(st.booleans())
+    n = data.draw(st.integers(0, 5000))
+    if blocks is not None:
+        # one block size per cluster (the first field's)
+        first = {}
+        for f, c in enumerate(labels):
+            first.setdefault(c, blocks[f])
+        blocks = [first[c] for c in labels]
+    L = A.Layout(widths, labels, blocks=blocks, aligned=aligned)
+    d = O.field_addresses_ex(widths, labels, n, blocks, aligned)
+    assert L.nbytes(n) == O.layout_bytes_ex(widths, labels, n, blocks, aligned)
+    for f in range(F):
+        r, s, o, b = L.field_address_ex(f, n)
+        for i in sorted({0, 1, n // 2, max(0, n - 1)}):
+            if i < n:
+                assert r + (i // b) * (b * s) + o * b + (i % b) * widths[f] == O.addr_ex(d, f, i)
+
+
+@SET
+@given(layouts(max_fields=8), st.data())
+def test_capi_layout_string_round_trip(widths, data):
+    F = len(widths)
+    labels = data.draw(partition(F))
+    names = [f"x{i}" for i in range(F)]
+    blocks = None
+    if data.draw(st.booleans()):
+        per = {c: data.draw(st.sampled_from([1, 2, 4, 8, 16, 32])) for c in sorted(set(labels))}
+        blocks = [per[c] for c in labels]
+    L = A.Layout(widths, labels, names=names, blocks=blocks, aligned=data.draw(st.booleans()))
+    text = L.to_string()
+    L2 = A.Layout.from_string(text, names, widths)
+    assert L2.to_string() == text
+    for f in range(F):
+        assert L.field_address_ex(f, 77) == L2.field_address_ex(f, 77)
+    assert L.nbytes(1001) == L2.nbytes(1001)
+
+
+@SET
+@given(st.integers(0, 10 ** 12), st.integers(1, 64))
+def test_capi_shard_ranges_cover_and_balance(n, G):
+    prev_hi = 0
+    sizes = []
+    for g in range(G):
+        lo, hi = A.shard_range(n, G, g)
+        assert lo == prev_hi and lo == g * n // G and hi == (g + 1) * n // G
+        prev_hi = hi
+        sizes.append(hi - lo)
+    assert prev_hi == n and max(sizes) - min(sizes) <= 1
