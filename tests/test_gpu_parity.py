@@ -498,3 +498,41 @@ def test_remap_peer_two_devices():
     A.remap_peer(d_src, La, d_dst, Lh, n)
     torch.cuda.synchronize(0)
     assert np.array_equal(d_dst.cpu().numpy(), oracle_dst(src, aos, hyb, widths, n))
+
+
+def test_concurrent_host_threads():
+    """Several host threads call adha_remap at once (ctypes drops the GIL), each on its own stream
+    with its own layout pair, so plan compilation and the plan cache run concurrently; every
+    result is bit-exact vs the oracle."""
+    import threading
+    widths = config_widths(16)
+    n = 50_001
+    pairs = [([0] * 16, list(range(16))), (list(range(16)), [0] * 16),
+             ([i // 4 for i in range(16)], [i % 4 for i in range(16)]),
+             ([i % 2 for i in range(16)], [i // 8 for i in range(16)])]
+    results, errors = {}, []
+
+    def work(k):
+        try:
+            ls, ld = pairs[k % len(pairs)]
+            cols = field_columns(100 + k, n, widths)
+            src = O.pack(cols, widths, ls, n)
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                d_src = to_dev(src)
+                d_dst = sentinel_dev(A.Layout(widths, ld).nbytes(n))
+                for _ in range(3):
+                    A.remap(d_src, A.Layout(widths, ls), d_dst, A.Layout(widths, ld), n, stream=s)
+            s.synchronize()
+            results[k] = (src, ls, ld, d_dst.cpu().numpy())
+        except Exception as e:  # surfaced below
+            errors.append(e)
+
+    threads = [threading.Thread(target=work, args=(k,)) for k in range(8)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    for k, (src, ls, ld, got) in results.items():
+        assert np.array_equal(got, oracle_dst(src, ls, ld, widths, n)), k
