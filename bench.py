@@ -39,8 +39,13 @@ CONFIGS = {
 }
 
 
+def golden(name):
+    """A committed planner-input fixture (tests/golden/*.json): program / arch documents only."""
+    with open(os.path.join(ROOT, "tests", "golden", name)) as fh:
+        return json.load(fh)
+
+
 def c3_labels():
-    from tests.conftest import golden  # fixture file only (the planner's expected output, cited)
     import paper_1407_4859_b200 as A
     layout = A.plan_ods(golden("c3_program.json"), golden("b200_arch.json"), "c3", "b200")
     names = [f"f{i}" for i in range(64)]
@@ -211,7 +216,6 @@ def planner_times():
     (64 fields, 2016 pairs, cap 128 B) and the C++ PDL of the Medical fixture (7 sections x 2
     devices, 56 run nodes); median of 20 calls each, in ms, with the JSON passed as text."""
     import paper_1407_4859_b200 as A
-    from tests.conftest import golden
 
     def med(fn):
         ts = []
