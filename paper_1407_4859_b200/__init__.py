@@ -1,7 +1,7 @@
 """paper_1407_4859_b200 -- B200-native ADHA data-layout remap (arXiv 1407.4859).
 
 Thin Python binding over the C ABI in ``include/adha.h`` (``libadha.so``, built
-in-tree by ``python -m paper_1407_4859_b200.build``).  Argument marshalling only:
+in-tree by ``python paper_1407_4859_b200/build.py`` or ``__graft_entry__.build()``).  Argument marshalling only:
 every step of the remap runs in the library's sm_100a kernels, the planner in its
 C++ host code.  There is no Python or CPU fallback: importing this package
 raises if the library is missing.
@@ -21,7 +21,7 @@ from typing import List, Optional, Sequence
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libadha.so")
 if not os.path.exists(LIB_PATH):
-    raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_1407_4859_b200.build` "
+    raise ImportError(f"{LIB_PATH} is missing: build it with `python paper_1407_4859_b200/build.py` "
                       "(there is no fallback path)")
 _lib = ctypes.CDLL(LIB_PATH)
 

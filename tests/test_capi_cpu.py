@@ -511,3 +511,15 @@ def test_byte_group_packing_is_phase_aware():
         F = len(w)
         _check_byte_groups(w, [0] * F, list(range(F)))
         _check_byte_groups(w, list(range(F)), [0] * F)
+
+
+def test_package_refuses_to_import_without_its_library(tmp_path):
+    """No fallback: a copy of the binding next to no libadha.so raises ImportError on import."""
+    import shutil
+    import subprocess
+    import sys
+    pkg = tmp_path / "adha_copy"
+    pkg.mkdir()
+    shutil.copy(os.path.join(ROOT, "paper_1407_4859_b200", "__init__.py"), pkg / "__init__.py")
+    out = subprocess.run([sys.executable, "-c", "import adha_copy"], cwd=tmp_path, capture_output=True, text=True)
+    assert out.returncode != 0 and "ImportError" in out.stderr and "no fallback" in out.stderr
