@@ -241,6 +241,48 @@ def test_max_size_beyond_2_31_records(widths):
     torch.cuda.empty_cache()
 
 
+@pytest.mark.parametrize("cfg", ["P1", "P2"])
+def test_paper_shaped_chains_full_size_sampled(cfg):
+    """The extra paper-shaped bench configs at their bench sizes (P1 Medical 256^3 AoS->AoSV->SoA,
+    P2 K-Means 2^23 SoA->4xAoS8->AoS), through adha_remap_chain; sampled records per edge."""
+    if cfg == "P1":
+        widths, n, labs = [4] * 9, 256 ** 3, [[0] * 9, AOSV, list(range(9))]
+    else:
+        widths, n, labs = [4] * 32, 2 ** 23, [list(range(32)), [i // 8 for i in range(32)], [0] * 32]
+    lays = [A.Layout(widths, l) for l in labs]
+    bufs = [torch.empty(l.nbytes(n), dtype=torch.uint8, device="cuda") for l in lays]
+    fill_random_device(bufs[0], SEED_BASE + 11)
+    for b in bufs[1:]:
+        b.fill_(SENT)
+    A.remap_chain(bufs, lays, n)
+    torch.cuda.synchronize()
+    for k in range(len(labs) - 1):
+        sampled_check(bufs[k], labs[k], bufs[k + 1], labs[k + 1], widths, n,
+                      plan_T(widths, labs[k], labs[k + 1]), seed=k)
+    del bufs
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("widths,kind", [([2, 4, 6, 4] * 4, "aos2soa"), ([2, 4, 6, 4] * 4, "soa2aos"),
+                                         ([1] * 24 + [8], "aos2soa"), ([1, 3, 4, 8] * 4, "soa2aos")])
+def test_byte_groups_large_n_sampled(widths, kind):
+    """The byte-group path (1/2-byte units) at the narrow-probe size N = 20M, in the tile
+    configuration it runs there; sampled records around tile and tail boundaries."""
+    n = 20_000_003
+    F = len(widths)
+    ls, ld = ([0] * F, list(range(F))) if kind == "aos2soa" else (list(range(F)), [0] * F)
+    Ls, Ld = A.Layout(widths, ls), A.Layout(widths, ld)
+    assert A.plan_describe(Ls, Ld)["byte_groups"]
+    src = torch.empty(Ls.nbytes(n), dtype=torch.uint8, device="cuda")
+    fill_random_device(src, SEED_BASE + 12)
+    dst = sentinel_dev(Ld.nbytes(n))
+    A.remap(src, Ls, dst, Ld, n)
+    torch.cuda.synchronize()
+    sampled_check(src, ls, dst, ld, widths, n, plan_T(widths, ls, ld))
+    del src, dst
+    torch.cuda.empty_cache()
+
+
 def test_c4_pdl_chain_full_size():
     widths, n = [4] * 9, (2 ** 31) // 36
     labs = [[0] * 9, AOSV, list(range(9)), [0] * 9]
