@@ -17,7 +17,7 @@ python bench.py --steps 2 --warmup 1 --soak-s 0 --no-cpu-baseline > $out/plain_$
   ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $out/launches_$tag.csv \
       python bench.py --steps 2 --warmup 1 --soak-s 0 --no-cpu-baseline > $out/ncu_launch_$tag.log 2>&1
 echo "ncu launches=$?"
-for c in C2 C3 C4; do
+for c in C2 C3 C4 C5 P1 P2; do
   python bench.py --config $c --steps 2 --warmup 1 --soak-s 0 --no-cpu-baseline --no-e2e --no-copy-ref > $out/plainf_${tag}_$c.log 2>&1 && \
     ncu --set full --clock-control none --import-source on -k regex:remap_tiled -s 3 -c 1 -o $out/prof_${tag}_$c \
         python bench.py --config $c --steps 2 --warmup 1 --soak-s 0 --no-cpu-baseline --no-e2e --no-copy-ref > $out/ncu_full_${tag}_$c.log 2>&1
