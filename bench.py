@@ -564,6 +564,11 @@ def main():
             "records_per_s": n_total * n_remaps * args.steps / (ms_max * 1e-3) / max(n_remaps, 1),
             "pct_of_spec_8000": value / world / 8000.0 * 100.0,
             "same_run_copy_gbs_per_gpu": copy_gbs,
+            "frac_of_same_run_copy": (value / world / copy_gbs) if copy_gbs else None,
+            "speedup_vs_oracle": ({"all_cores": value / cpu["value"], "single_thread": value / cpu["single_thread_value"],
+                                   "paper_context": "PAPER.md:16 reports up to 6.92x from layout choice alone on "
+                                                    "X5660 + M2050 (a different quantity; context only)"}
+                                  if cpu else None),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "peak_source": peak_src,
