@@ -25,7 +25,8 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-FALLBACK_HBM_GBS = 6650.0      # /opt/skills/guides/B200_PROFILING.md fallback, used only without MEASURED_PEAKS.json
+FALLBACK_HBM_GBS = 6650.0
+GRAPH_STEPS = 16               # steps per CUDA-graph launch for launch-bound (< 256 MB) steps      # /opt/skills/guides/B200_PROFILING.md fallback, used only without MEASURED_PEAKS.json
 
 CONFIGS = {
     # name: (description, widths, src labels, dst labels chain, n_records, scaling)
@@ -353,8 +354,10 @@ def main():
     plan = A.plan_describe(layouts[0], layouts[1])
 
     def step_direct():
-        for k in range(n_remaps):
-            A.remap(bufs[k], layouts[k], bufs[k + 1], layouts[k + 1], n, stream=None)   # torch's current stream
+        if n_remaps == 1:
+            A.remap(bufs[0], layouts[0], bufs[1], layouts[1], n, stream=None)       # torch's current stream
+        else:       # a PDL chain: adha_remap_chain (one launch for latency-bound chains like C1)
+            A.remap_chain(bufs, layouts, n, stream=None)
 
     use_graph = args.graph == "on" or (args.graph == "auto" and bytes_step_rank < (256 << 20))
     step = step_direct
@@ -370,9 +373,26 @@ def main():
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph):
             step_direct()
+        # launch-bound steps are also captured GRAPH_STEPS at a time, so the timed loop pays one
+        # graph launch per GRAPH_STEPS steps (every step still runs its full remap(s))
+        graph_n = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph_n):
+            for _ in range(GRAPH_STEPS):
+                step_direct()
 
         def step():
             graph.replay()
+
+    def run_steps(k):
+        """k steps back to back: the multi-step graph where it applies, single steps otherwise."""
+        if use_graph:
+            for _ in range(k // GRAPH_STEPS):
+                graph_n.replay()
+            for _ in range(k % GRAPH_STEPS):
+                graph.replay()
+        else:
+            for _ in range(k):
+                step()
 
     def barrier():
         if world > 1:
@@ -400,8 +420,7 @@ def main():
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record(stream)
-    for i in range(args.steps):
-        step()
+    run_steps(args.steps)
     t1.record(stream)
     torch.cuda.synchronize(dev)
     barrier()
@@ -465,8 +484,11 @@ def main():
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        for _ in range(args.steps):
-            fn()
+        if fn is step:
+            run_steps(args.steps)
+        else:
+            for _ in range(args.steps):
+                fn()
         b.record(stream)
         torch.cuda.synchronize(dev)
         barrier()
@@ -487,10 +509,18 @@ def main():
 
     # roofline of the dominant kernel (the remap kernel is the only kernel in the step)
     peak, peak_src = measured_peak()
-    # the step is n_remaps back-to-back launches of the remap kernel and nothing else, so the
-    # kernel's average launch duration is this rank's event time over the K steps / (K * n_remaps)
-    avg_launch_ms = ms_total / (args.steps * n_remaps)
-    achieved = 2 * n * R / (avg_launch_ms * 1e-3) / 1e9
+    # launches per step: one per remap, except a chain of latency-bound hops, which
+    # adha_remap_chain runs as ONE fused launch (remap.cu chain_small: every hop <= ADHA_SMALL_BYTES,
+    # <= 16 fields, <= 4 hops, packed layouts, disjoint buffers -- all true for C1)
+    small = int(os.environ.get("ADHA_SMALL_BYTES", 65536))
+    fused_chain = (n_remaps > 1 and os.environ.get("ADHA_CHAIN_FUSE", "1") != "0" and n * R <= small
+                   and len(widths) <= 16 and n_remaps <= 4)
+    launches_per_step = 1 if fused_chain else n_remaps
+    # the step is those back-to-back launches and nothing else, so the kernel's average launch
+    # duration is this rank's event time over the K steps / (K * launches per step)
+    avg_launch_ms = ms_total / (args.steps * launches_per_step)
+    bytes_per_launch = 2 * n * R * n_remaps // launches_per_step
+    achieved = bytes_per_launch / (avg_launch_ms * 1e-3) / 1e9
     traffic = ncu_traffic(name)
 
     # end-to-end through the public API with host buffers (pinned), H2D + D2H inside the timed region
@@ -560,6 +590,7 @@ def main():
                 "parallelism": f"shard by contiguous record range over {world} GPU(s), no data-path collective",
                 "kernel": {k: plan[k] for k in ("tiled", "unit", "T", "s_in", "s_out", "smem_bytes", "matched")},
                 "cuda_graph": use_graph,
+                "graph_steps_per_launch": GRAPH_STEPS if use_graph else None,
             },
             "records_per_s": n_total * n_remaps * args.steps / (ms_max * 1e-3) / max(n_remaps, 1),
             "pct_of_spec_8000": value / world / 8000.0 * 100.0,
@@ -572,17 +603,17 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "peak_source": peak_src,
-                         "kernel": ("remap_naive_kernel (direct path for remaps <= ADHA_SMALL_BYTES)"
-                                    if n * R <= int(os.environ.get("ADHA_SMALL_BYTES", 65536)) else
-                                    "remap_tiled_kernel"),
-                         "algorithmic_bytes_per_launch": 2 * n * R,
+                         "kernel": ("remap_chain_small_kernel (fused chain of latency-bound hops)" if fused_chain
+                                    else "remap_naive_kernel (direct path for remaps <= ADHA_SMALL_BYTES)"
+                                    if n * R <= small else "remap_tiled_kernel"),
+                         "algorithmic_bytes_per_launch": bytes_per_launch,
                          "avg_launch_ms": avg_launch_ms},
             "sustained": sustained,
             "planner": planner_times(),
             "step_ms_spread": {"median": statistics.median(rep_ms), "min": rep_ms[0], "max": rep_ms[-1],
                                "reps": len(rep_ms), "note": "per-step events after the timed region, rank 0"},
             "wall_ms_timed_region": wall_max,
-            "gpu_launches": args.steps * n_remaps,
+            "gpu_launches": args.steps * launches_per_step,
             "clocks": clk,
             "e2e": e2e,
             "cpu_baseline": cpu,

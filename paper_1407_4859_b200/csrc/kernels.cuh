@@ -463,5 +463,31 @@ __global__ void remap_naive_kernel(const __grid_constant__ NaiveParamsT<NF> p) {
     }
 }
 
+__global__ void __launch_bounds__(256) remap_chain_small_kernel(const __grid_constant__ ChainParams p) {
+    const int64_t n = p.n_records;
+    const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+    const int64_t lo = (int64_t)blockIdx.x * per;
+    const int64_t m = lo < n ? min(per, n - lo) : 0;
+    const int64_t total = m * (int64_t)p.n_fields;
+    for (uint32_t h = 0; h < p.n_hops; ++h) {
+        const uint8_t* src = (const uint8_t*)p.buf[h];
+        uint8_t* dst = (uint8_t*)p.buf[h + 1];
+        for (int64_t k = threadIdx.x; k < total; k += blockDim.x) {
+            const uint32_t f = (uint32_t)(k / m);
+            const uint64_t r = (uint64_t)(lo + (k - (int64_t)f * m));
+            const NaiveField& fd = p.f[h][f];
+            const uint8_t* s = src + fd.sbase + r * fd.sstride + fd.soff;
+            uint8_t* d = dst + fd.dbase + r * fd.dstride + fd.doff;
+            uint32_t j = 0;
+            if ((((uintptr_t)s | (uintptr_t)d | fd.width) & 3) == 0) {
+                for (; j < fd.width; j += 4) *reinterpret_cast<uint32_t*>(d + j) = *reinterpret_cast<const uint32_t*>(s + j);
+            } else {
+                for (; j < fd.width; ++j) d[j] = s[j];
+            }
+        }
+        __syncthreads();     // hop h's stores by this block are visible to the whole block
+    }
+}
+
 }  // namespace dev
 }  // namespace adha

@@ -386,10 +386,70 @@ extern "C" adha_status adha_remap_regions(const void* const* src_regions, const 
     return remap_checked(nullptr, ls, nullptr, ld, n, ck, (cudaStream_t)stream);
 }
 
+namespace adha {
+namespace detail {
+// One launch for a chain of latency-bound hops (every hop <= ADHA_SMALL_BYTES of payload, packed
+// unblocked layouts, <= CHAIN_NF fields, <= CHAIN_NH hops, pairwise disjoint buffers).  Returns
+// ADHA_ERR_UNSUPPORTED (no error recorded) when the chain does not qualify.
+adha_status chain_small(void* const* buffers, const adha_layout* const* layouts, int32_t n_layouts, int64_t n,
+                        cudaStream_t st) {
+    const char* e = std::getenv("ADHA_CHAIN_FUSE");
+    if ((e && *e == '0') || n <= 0 || n_layouts - 1 > CHAIN_NH) return ADHA_ERR_UNSUPPORTED;
+    const Layout& l0 = layouts[0]->L;
+    if (l0.n_fields > CHAIN_NF || (uint64_t)n * l0.record_bytes > small_bytes()) return ADHA_ERR_UNSUPPORTED;
+    std::vector<Checked> ck(n_layouts - 1);
+    for (int32_t k = 0; k + 1 < n_layouts; ++k) {
+        adha_status s = validate(buffers[k], layouts[k], buffers[k + 1], layouts[k + 1], n, &ck[k], true);
+        if (s != ADHA_OK) return s;
+    }
+    std::vector<std::pair<uintptr_t, uintptr_t>> ranges;
+    for (int32_t k = 0; k < n_layouts; ++k) {
+        const Layout& L = layouts[k]->L;
+        for (int c = 0; c < L.n_clusters(); ++c)
+            if (L.block[c] != 1 || L.stride[c] != L.payload(c)) return ADHA_ERR_UNSUPPORTED;
+        const uint64_t bytes = k + 1 < n_layouts ? ck[k].bytes_s : ck[k - 1].bytes_d;
+        ranges.push_back({(uintptr_t)buffers[k], (uintptr_t)buffers[k] + bytes});
+    }
+    for (size_t a = 0; a < ranges.size(); ++a)
+        for (size_t b = a + 1; b < ranges.size(); ++b)
+            if (ranges[a].first < ranges[b].second && ranges[b].first < ranges[a].second) return ADHA_ERR_UNSUPPORTED;
+    int n_sm = 0;
+    adha_status s = device_setup(nullptr, &n_sm);
+    if (s != ADHA_OK) return s;
+    auto P = std::make_unique<ChainParams>();
+    std::memset(P.get(), 0, sizeof(ChainParams));
+    P->n_records = n;
+    P->n_fields = (uint32_t)l0.n_fields;
+    P->n_hops = (uint32_t)(n_layouts - 1);
+    for (int32_t k = 0; k < n_layouts; ++k) P->buf[k] = (uint64_t)(uintptr_t)buffers[k];
+    for (int32_t k = 0; k + 1 < n_layouts; ++k) {
+        const Layout& ls = layouts[k]->L;
+        const Layout& ld = layouts[k + 1]->L;
+        for (int f = 0; f < ls.n_fields; ++f) {
+            const int cs = ls.cluster[f], cd = ld.cluster[f];
+            P->f[k][f] = {ck[k].bs[cs], ck[k].bd[cd], (uint32_t)ls.stride[cs], (uint32_t)ld.stride[cd], ls.offset[f],
+                          ld.offset[f], ls.width[f], 0u};
+        }
+    }
+    // ~256 (record, field) items per block and hop: enough blocks to spread the latency
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((n * l0.n_fields + 255) / 256, n_sm));
+    remap_chain_small_kernel<<<(unsigned)blocks, 256, 0, st>>>(*P);
+    cudaError_t ce = cudaGetLastError();
+    if (ce != cudaSuccess) return cuda_fail(ce, "remap_chain_small_kernel launch");
+    return ADHA_OK;
+}
+}  // namespace detail
+}  // namespace adha
+
 extern "C" adha_status adha_remap_chain(void* const* buffers, const adha_layout* const* layouts, int32_t n_layouts,
                                         int64_t n, void* stream) {
     clear_error();
     if (!buffers || !layouts || n_layouts < 2) return fail(ADHA_ERR_INVALID_ARG, "need at least two layouts");
+    for (int32_t k = 0; k < n_layouts; ++k)
+        if (!layouts[k]) return fail(ADHA_ERR_INVALID_ARG, "null layout");
+    const adha_status fused = detail::chain_small(buffers, layouts, n_layouts, n, (cudaStream_t)stream);
+    if (fused != ADHA_ERR_UNSUPPORTED) return fused;
+    clear_error();
     for (int32_t k = 0; k + 1 < n_layouts; ++k) {
         adha_status s = adha_remap(buffers[k], layouts[k], buffers[k + 1], layouts[k + 1], n, stream);
         if (s != ADHA_OK) return s;

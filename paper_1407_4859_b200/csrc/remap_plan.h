@@ -143,6 +143,17 @@ struct NaiveParamsT {
 };
 using NaiveParams = NaiveParamsT<MAXF>;
 constexpr int SMALL_NF = 32;                  // direct kernel with small parameters (latency path)
+
+// Fused small chain (adha_remap_chain when every hop is a latency-bound remap): one launch runs
+// every hop; block b owns a contiguous record range in every buffer and a __syncthreads()
+// separates the hops, so hop h+1 reads exactly the bytes block b wrote in hop h.
+constexpr int CHAIN_NF = 16, CHAIN_NH = 4;
+struct ChainParams {
+    uint64_t buf[CHAIN_NH + 1];
+    int64_t n_records;
+    uint32_t n_fields, n_hops;
+    NaiveField f[CHAIN_NH][CHAIN_NF];   // per hop; packed, unblocked layouts only (pad = 0)
+};
 using SmallParams = NaiveParamsT<SMALL_NF>;
 
 }  // namespace dev

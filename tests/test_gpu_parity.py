@@ -283,6 +283,36 @@ def test_byte_groups_large_n_sampled(widths, kind):
     torch.cuda.empty_cache()
 
 
+@pytest.mark.parametrize("fuse", ["1", "0"])
+def test_small_chain_fused_single_launch(fuse, monkeypatch):
+    """adha_remap_chain over latency-bound hops runs as ONE launch (block-local record ranges,
+    a barrier between hops) when every hop is <= ADHA_SMALL_BYTES and the layouts are packed;
+    every intermediate is materialised and bit-exact vs the oracle, fused or not.  Includes C1
+    (xyz AoS -> SoA -> AoS, 1024 records) and random 2-4 hop chains with ragged N."""
+    monkeypatch.setenv("ADHA_CHAIN_FUSE", fuse)
+    rng = np.random.default_rng(77)
+    cases = [([4, 4, 4], [[0, 0, 0], [0, 1, 2], [0, 0, 0]], 1024)]
+    for _ in range(12):
+        F = int(rng.integers(1, 12))
+        widths = [int(x) for x in rng.choice([1, 2, 4, 8, 3], size=F)]
+        hops = int(rng.integers(2, 5))
+        labs = [[int(x) for x in rng.integers(0, F, size=F)] for _ in range(hops + 1)]
+        n = int(rng.integers(1, max(2, 60000 // sum(widths))))
+        cases.append((widths, labs, n))
+    for widths, labs, n in cases:
+        cols = field_columns(n % 1000, n, widths)
+        lays = [A.Layout(widths, l) for l in labs]
+        bufs = [to_dev(O.pack(cols, widths, labs[0], n))] + [sentinel_dev(l.nbytes(n)) for l in lays[1:]]
+        A.remap_chain(bufs, lays, n)
+        torch.cuda.synchronize()
+        exp = O.pack(cols, widths, labs[0], n)
+        for k in range(1, len(labs)):
+            e = np.full(O.layout_bytes(widths, labs[k], n), SENT, np.uint8)
+            O.remap(exp, labs[k - 1], e, labs[k], widths, n)
+            assert np.array_equal(bufs[k].cpu().numpy()[: e.size], e), (widths, labs, n, k)
+            exp = e
+
+
 def test_c4_pdl_chain_full_size():
     widths, n = [4] * 9, (2 ** 31) // 36
     labs = [[0] * 9, AOSV, list(range(9)), [0] * 9]
