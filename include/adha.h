@@ -207,7 +207,11 @@ ADHA_API adha_status adha_remap_regions(const void* const* src_regions, const ad
 /* A chain of remaps on one stream (a PDL plan with several remap edges,
  * PAPER.md:146): buffers[k] holds the records in layouts[k];
  * for k = 0..n_layouts-2: remap buffers[k] (layouts[k]) -> buffers[k+1]
- * (layouts[k+1]).  Every intermediate is materialised.  Same rules as adha_remap. */
+ * (layouts[k+1]).  Every intermediate is materialised.  Same rules as adha_remap.
+ * A chain of latency-bound hops (each <= ADHA_SMALL_BYTES of payload, <= 16 fields, <= 4 hops,
+ * packed unblocked layouts, pairwise disjoint buffers) runs as ONE kernel launch with a
+ * block-level barrier between hops (ADHA_CHAIN_FUSE=0 disables this); otherwise one remap per
+ * hop, in order, on `stream`. */
 ADHA_API adha_status adha_remap_chain(void* const* buffers, const adha_layout* const* layouts,
                              int32_t n_layouts, int64_t n_records, void* stream);
 
