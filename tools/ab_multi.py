@@ -15,7 +15,12 @@ import bench  # noqa: E402
 ROUNDS = int(os.environ.get("ROUNDS", "5"))
 variants = [dict(kv.split("=") for kv in v.split(",") if kv) for v in (sys.argv[1:] or [""])]
 edges = []
-for cfg in os.environ.get("CFGS", "C2,P1,P2,C4").split(","):
+if os.environ.get("NARROW") == "1":          # the narrow-field / generalised cases of narrow_probe.py
+    for name, w in (("g2", [2, 4, 6, 4] * 4), ("g1", [1, 3, 4, 8] * 4), ("b24", [1] * 24 + [8])):
+        F = len(w)
+        edges.append((name + "a2s", w, [0] * F, list(range(F)), 20_000_000))
+        edges.append((name + "s2a", w, list(range(F)), [0] * F, 20_000_000))
+for cfg in [c for c in os.environ.get("CFGS", "C2,P1,P2,C4").split(",") if c]:
     desc, kind, n, _ = bench.CONFIGS[cfg]
     widths, chain = bench.chain_for(kind)
     for k in range(len(chain) - 1):
