@@ -10,7 +10,6 @@ Each test checks the oracle against something other than itself:
   (iv)  brute force over all 52^2 ordered layout pairs of 5 fields;
   (v)   tagged data names a misplaced slot; NaN payloads survive bit for bit.
 """
-import itertools
 
 import numpy as np
 import pytest

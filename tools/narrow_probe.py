@@ -1,5 +1,5 @@
 """Narrow fields: GB/s of AoS<->SoA remaps for records whose unit g is 4, 2 or 1 byte."""
-import os, sys, statistics
+import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_1407_4859_b200 as A
