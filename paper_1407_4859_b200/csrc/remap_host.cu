@@ -23,6 +23,7 @@ constexpr int PIPE_SLOTS = 4;        // chunks in flight through the device scra
 struct HostPipe {
     cudaStream_t s[PIPE_SLOTS] = {};
     cudaEvent_t start = nullptr, done[PIPE_SLOTS] = {};
+    std::mutex* mu = nullptr;      // held while one call enqueues (the events are shared state)
 };
 std::mutex g_pipe_mu;
 std::map<int, HostPipe> g_pipes;
@@ -43,6 +44,7 @@ adha_status get_pipe(HostPipe** out) {
         }
         if ((e = cudaEventCreateWithFlags(&hp.start, cudaEventDisableTiming)) != cudaSuccess)
             return cuda_fail(e, "cudaEventCreate");
+        hp.mu = new std::mutex();      // lives as long as the process, like the pipe's streams
         it = g_pipes.emplace(dev, hp).first;
     }
     *out = &it->second;
@@ -130,6 +132,8 @@ extern "C" adha_status adha_remap_host(const void* src_host, const adha_layout* 
 
     HostPipe* hp = nullptr;
     if ((s = get_pipe(&hp)) != ADHA_OK) return s;
+    // concurrent calls on one device share the pipe's streams and events: enqueue one at a time
+    std::lock_guard<std::mutex> pipe_lock(*hp->mu);
     cudaError_t e = cudaEventRecord(hp->start, user);
     if (e != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
     for (int i = 0; i < slots; ++i)

@@ -608,3 +608,39 @@ def test_concurrent_host_threads():
     assert not errors, errors
     for k, (src, ls, ld, got) in results.items():
         assert np.array_equal(got, oracle_dst(src, ls, ld, widths, n)), k
+
+
+def test_concurrent_remap_host_threads(monkeypatch):
+    """adha_remap_host from 4 host threads at once (own streams, own scratch, own pinned buffers):
+    the per-device pipe is shared, so its enqueue is serialised; every result is bit-exact."""
+    import threading
+    monkeypatch.setenv("ADHA_HOST_MODE", "hybrid")
+    monkeypatch.setenv("ADHA_HOST_CHUNK_BYTES", str(1 << 20))
+    widths = config_widths(16)
+    n = 120_001
+    ls, ld = [0] * 16, list(range(16))
+    La, Ld = A.Layout(widths, ls), A.Layout(widths, ld)
+    out, errors = {}, []
+
+    def work(k):
+        try:
+            src_np = O.pack(field_columns(200 + k, n, widths), widths, ls, n)
+            h_src = torch.from_numpy(src_np).pin_memory()
+            h_dst = torch.full((Ld.nbytes(n),), SENT, dtype=torch.uint8).pin_memory()
+            scratch = torch.empty(16 << 20, dtype=torch.uint8, device="cuda")
+            s = torch.cuda.Stream()
+            for _ in range(3):
+                A.remap_host(h_src, La, h_dst, Ld, n, scratch, stream=s)
+            s.synchronize()
+            out[k] = (src_np, h_dst.numpy().copy())
+        except Exception as e:  # surfaced below
+            errors.append(e)
+
+    threads = [threading.Thread(target=work, args=(k,)) for k in range(4)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    for k, (src_np, got) in out.items():
+        assert np.array_equal(got, oracle_dst(src_np, ls, ld, widths, n)), k
