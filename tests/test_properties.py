@@ -137,3 +137,52 @@ def test_capi_shard_ranges_cover_and_balance(n, G):
         prev_hi = hi
         sizes.append(hi - lo)
     assert prev_hi == n and max(sizes) - min(sizes) <= 1
+
+
+@settings(max_examples=300, deadline=None)
+@given(st.text(max_size=80))
+def test_capi_layout_parser_never_crashes(text):
+    """Arbitrary text into adha_layout_from_string: a layout or ADHA_ERR_PARSE / INVALID_ARG,
+    never a crash."""
+    names, widths = ["a", "b", "c", "V1"], [4, 4, 8, 2]
+    try:
+        L = A.Layout.from_string(text, names, widths)
+    except A.AdhaError as e:
+        assert e.name in ("ADHA_ERR_PARSE", "ADHA_ERR_INVALID_ARG"), e
+    else:
+        assert sorted(f for c in L.to_string().strip("{}").split("}|{") for f in c.split(",")) == sorted(names)
+
+
+def _mutations(doc: str):
+    return st.one_of(
+        st.just(doc),
+        st.builds(lambda i, j: doc[:i] + doc[j:], st.integers(0, len(doc)), st.integers(0, len(doc))),
+        st.builds(lambda i, c: doc[:i] + c + doc[i:], st.integers(0, len(doc)), st.sampled_from(list('{}[]",:0-1e'))),
+        st.text(max_size=60))
+
+
+_PROGRAM = None
+
+
+def _medical():
+    global _PROGRAM
+    if _PROGRAM is None:
+        import json
+        from tests.conftest import golden
+        _PROGRAM = (json.dumps(golden("medical_program.json")), json.dumps(golden("medical_arch.json")))
+    return _PROGRAM
+
+
+@settings(max_examples=200, deadline=None)
+@given(st.data())
+def test_capi_planner_rejects_malformed_json_cleanly(data):
+    """Truncated, spliced or random planner documents: adha_plan_ods / adha_plan_pdl return a plan or
+    a PARSE / PLANNER / CAPACITY / INVALID_ARG status, never a crash."""
+    prog, arch = _medical()
+    p = data.draw(_mutations(prog))
+    a = data.draw(_mutations(arch))
+    for call in (lambda: A.plan_pdl(p, a), lambda: A.plan_ods(p, a, "s1", "cpu")):
+        try:
+            call()
+        except A.AdhaError as e:
+            assert e.name in ("ADHA_ERR_PARSE", "ADHA_ERR_PLANNER", "ADHA_ERR_CAPACITY", "ADHA_ERR_INVALID_ARG"), e
