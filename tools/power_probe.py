@@ -78,7 +78,18 @@ def run(name, fn):
     time.sleep(2.0)          # cool-down between variants
 
 
+def remap_env(env):
+    def fn():
+        os.environ.update(env)
+        A.remap(src, La, dst, Ls, N)
+        for k in env:
+            del os.environ[k]
+    return fn
+
+
 variants = [("copy_", lambda: cb.copy_(ca)), ("remap C2", lambda: A.remap(src, La, dst, Ls, N))]
+for extra in sys.argv[2:]:              # e.g. ADHA_STAGE_BYTES=40960,ADHA_OUT_BUFFERS=1
+    variants.append((f"remap C2 {extra}", remap_env(dict(kv.split("=") for kv in extra.split(",")))))
 for _ in range(2):
     for name, fn in variants:
         run(name, fn)
