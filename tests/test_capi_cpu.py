@@ -523,3 +523,17 @@ def test_package_refuses_to_import_without_its_library(tmp_path):
     shutil.copy(os.path.join(ROOT, "paper_1407_4859_b200", "__init__.py"), pkg / "__init__.py")
     out = subprocess.run([sys.executable, "-c", "import adha_copy"], cwd=tmp_path, capture_output=True, text=True)
     assert out.returncode != 0 and "ImportError" in out.stderr and "no fallback" in out.stderr
+
+
+def test_status_strings_and_version():
+    """adha_status_string names every status the header declares (and never returns NULL);
+    adha_version is MAJOR*10000 + MINOR*100 + PATCH with MAJOR >= 1 or MINOR >= 1."""
+    import re
+    text = open(os.path.join(ROOT, "include", "adha.h")).read()
+    codes = {int(v): k for k, v in re.findall(r"(ADHA_(?:OK|ERR_[A-Z_]+)) = (\d+)", text)}
+    assert len(codes) == 12
+    for v, k in codes.items():
+        assert A._lib.adha_status_string(v).decode() == k == A.STATUS[v]
+    assert A._lib.adha_status_string(999) is not None and A._lib.adha_status_string(-1) is not None
+    v = A.version()
+    assert v >= 100 and 0 <= v % 100 < 100
