@@ -24,7 +24,12 @@
 //     distinct banks and writes 32 distinct banks (conflict-free LDS and STS by
 //     construction, independent of T_k);
 //   * identity components (one src cluster == one dst cluster, same fields)
-//     skip the permutation: the staged chunk is written straight back.
+//     skip the permutation: the staged chunk moves to the output buffer with
+//     16-byte shared copies (releasing the input stage early) and is written back;
+//   * g = 1 or 2 (byte-group mode): a lane assembles up to 4 output WORDS from
+//     up to 4 source words with PRMT (ByteGroup below); groups are packed into
+//     instructions conflict-free at every period phase where possible
+//     (remap_plan.cpp), and chunk starts are staggered by 32 bytes per cluster.
 #pragma once
 
 #include <cstdint>
