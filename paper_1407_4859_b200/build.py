@@ -43,19 +43,22 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(f) <= t for f in _deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
-        return LIB
-    os.makedirs(BUILD, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, defines=(), lib: str = LIB) -> str:
+    """Compile every csrc/ source for sm_100a and link `lib`.  `defines` (e.g. ADHA_PHASE_TIMING
+    for the instrumented diagnostic library) go to every compile; such variants are linked to
+    their own file under _build/, never to the product libadha.so."""
+    if not force and not defines and up_to_date():
+        return lib
+    tag = "_".join(d.lower() for d in defines)
+    bdir = os.path.join(BUILD, tag) if tag else BUILD
+    os.makedirs(bdir, exist_ok=True)
     objs = []
     procs = []
     for src in sources():
-        obj = os.path.join(BUILD, os.path.basename(src) + ".o")
-        cmd = [NVCC] + ARCH + COMMON + ["-c", src, "-o", obj]
-        if src.endswith(".cu"):
-            cmd += ["-Xptxas", "-v"] if verbose else []
-        else:
-            cmd += ["-x", "cu"] if False else []
+        obj = os.path.join(bdir, os.path.basename(src) + ".o")
+        cmd = [NVCC] + ARCH + COMMON + [f"-D{d}" for d in defines] + ["-c", src, "-o", obj]
+        if src.endswith(".cu") and verbose:
+            cmd += ["-Xptxas", "-v"]
         objs.append(obj)
         procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
     for cmd, p in procs:
@@ -64,13 +67,22 @@ def build(force: bool = False, verbose: bool = False) -> str:
             sys.stderr.write(out.decode())
         if p.returncode != 0:
             raise RuntimeError("nvcc failed: " + " ".join(cmd))
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     link = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", tmp] + objs + ["-lpthread", "-lrt", "-ldl"]
     subprocess.check_call(link)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
+
+
+def build_phase_timing() -> str:
+    """The diagnostic library with per-phase clock64() counters in the tiled kernel
+    (tools/phase_probe.py); not used by the package, the tests or the bench."""
+    return build(force=True, defines=("ADHA_PHASE_TIMING",), lib=os.path.join(BUILD, "libadha_phase.so"))
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB)
+    if "--phase-timing" in sys.argv:
+        print(build_phase_timing())
+    else:
+        build(force="--force" in sys.argv, verbose="-v" in sys.argv)
+        print(LIB)

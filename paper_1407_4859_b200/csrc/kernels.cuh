@@ -74,6 +74,17 @@ __device__ __forceinline__ void copy_out(uint8_t* dst, uint32_t sm_base, uint32_
     }
 }
 
+// Diagnostic build only (-DADHA_PHASE_TIMING, tools/phase_probe.py): clock64() time per phase of
+// the tiled kernel, summed over warps and tiles.  [0] consumer wait on `full`, [1] permutation,
+// [2] output-tile barrier, [3] copy-out, [4] consumer tiles, [5] producer wait on `empty`,
+// [6] producer issue, [7] tails.  Off in the product library.
+#ifdef ADHA_PHASE_TIMING
+__device__ unsigned long long g_phase[8];
+#define ADHA_PT(...) __VA_ARGS__
+#else
+#define ADHA_PT(...)
+#endif
+
 // Tile order of a CTA: interleaved (t = b, b+G, ...: the GPU sweeps the arrays as one front)
 // or blocked (CTA b takes the contiguous range [b*M/G, (b+1)*M/G)).
 __device__ __forceinline__ int64_t t_first(const TiledParams& p) {
@@ -125,6 +136,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         uint32_t np = 0;
         int kp = -1;
         uint32_t stage = 0, phase = 0, k = 0;
+        ADHA_PT(long long pw = 0; long long pi = 0);
         for (int64_t t = t_first(p), te = t_end(p); t < te; t += t_step(p)) {
             while (t >= p.comp[k].tile_base + p.comp[k].n_tiles) ++k;
             const int64_t lt = t - p.comp[k].tile_base;
@@ -160,7 +172,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     }
                 }
             }
+            ADHA_PT(const long long pt0 = clock64());
             mbar_wait(empty0 + 8 * stage, phase ^ 1);
+            ADHA_PT(const long long pt1 = clock64(); pw += pt1 - pt0);
             if (lane == 0) mbar_arrive_expect_tx(full0 + 8 * stage, p.comp[k].tile_bytes);
             __syncwarp();
             const uint32_t ib = in0 + stage * p.stage_bytes;
@@ -172,8 +186,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     else bulk_load(ib + psm[q], g, pbytes[q], full0 + 8 * stage);
                 }
             }
+            ADHA_PT(pi += clock64() - pt1);
             if (++stage == p.s_in) { stage = 0; phase ^= 1; }
         }
+        ADHA_PT(if (lane == 0) { atomicAdd(&g_phase[5], (unsigned long long)pw); atomicAdd(&g_phase[6], (unsigned long long)pi); });
         return;
     }
 
@@ -188,6 +204,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     uint32_t gstep[VMAX];
     uint32_t ne = 0, nv = 0;
 
+    ADHA_PT(const long long tt0 = clock64());
     // Tails first: records [n_tiles*T_k, N) of every component.  Plain components spread their
     // tail over the consumer threads of ALL CTAs, four records in flight per thread, while the
     // producer's first tiles are still in flight (one CTA copying a 48 KB tail alone took ~40 us).
@@ -252,8 +269,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
     }
 
+    ADHA_PT(long long ph[5] = {0, 0, 0, 0, 0}; ph[4] = clock64() - tt0);
     int k_cur = -1;
     uint32_t stage = 0, phase = 0, oslot = 0, k = 0;
+    ADHA_PT(long long ntile = 0);
     for (int64_t t = t_first(p), te = t_end(p); t < te; t += t_step(p)) {
         while (t >= p.comp[k].tile_base + p.comp[k].n_tiles) ++k;
         const int64_t lt = t - p.comp[k].tile_base;
@@ -322,7 +341,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             }
             }
         }
+        ADHA_PT(const long long c0 = clock64());
         mbar_wait(full0 + 8 * stage, phase);
+        ADHA_PT(const long long c1 = clock64(); ph[0] += c1 - c0; ++ntile);
         const uint32_t ib = in0 + stage * p.stage_bytes;
         {
             const uint32_t ob = out0 + oslot * p.stage_bytes;
@@ -408,13 +429,21 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(empty0 + 8 * stage);    // input stage free for the producer
+            ADHA_PT(const long long c2 = clock64(); ph[1] += c2 - c1);
             named_bar_sync(1, NCONS * 32);                      // output tile complete
+            ADHA_PT(const long long c3 = clock64(); ph[2] += c3 - c2);
             if (p.l2_hints & 2) copy_out<true>((uint8_t*)p.dst, ob, tid, lt, nv, gofs, gstep, spol);
             else copy_out<false>((uint8_t*)p.dst, ob, tid, lt, nv, gofs, gstep, spol);
+            ADHA_PT(ph[3] += clock64() - c3);
             if (p.s_out == 2) oslot ^= 1;
         }
         if (++stage == p.s_in) { stage = 0; phase ^= 1; }
     }
+    ADHA_PT(if (lane == 0) {
+        for (int i = 0; i < 4; ++i) atomicAdd(&g_phase[i], (unsigned long long)ph[i]);
+        atomicAdd(&g_phase[4], (unsigned long long)ntile);
+        atomicAdd(&g_phase[7], (unsigned long long)ph[4]);
+    });
 
 }
 

@@ -548,6 +548,18 @@ extern "C" adha_status adha_remap_peer(const void* src, const adha_layout* hs, i
     return out;
 }
 
+#ifdef ADHA_PHASE_TIMING
+// diagnostic build only: read (and optionally reset) the tiled kernel's phase counters
+extern "C" __attribute__((visibility("default"))) int adha_debug_phase(unsigned long long* out8, int reset) {
+    cudaError_t e = cudaMemcpyFromSymbol(out8, adha::dev::g_phase, 8 * sizeof(unsigned long long));
+    if (e == cudaSuccess && reset) {
+        unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        e = cudaMemcpyToSymbol(adha::dev::g_phase, z, sizeof z);
+    }
+    return (int)e;
+}
+#endif
+
 // ---------------------------------------------------------------------------- host end-to-end
 extern "C" adha_status adha_remap_plan_describe(const adha_layout* hs, const adha_layout* hd, char** json_out) {
     clear_error();

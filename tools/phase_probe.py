@@ -1,0 +1,78 @@
+"""Where does a tile's time go?  Loads the DIAGNOSTIC library (built with -DADHA_PHASE_TIMING by
+`python paper_1407_4859_b200/build.py --phase-timing`, never used by the package) and reports the
+tiled kernel's clock64() phase sums per tile and consumer warp: wait for the TMA data (`full`),
+permutation, output-tile barrier, copy-out; and the producer's wait for a free stage.
+usage: python tools/phase_probe.py"""
+import ctypes
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+lib = ctypes.CDLL(os.path.join(ROOT, "paper_1407_4859_b200", "_build", "libadha_phase.so"))
+lib.adha_layout_create.argtypes = [ctypes.POINTER(ctypes.c_uint32), ctypes.c_int32, ctypes.POINTER(ctypes.c_int32),
+                                   ctypes.POINTER(ctypes.c_void_p)]
+lib.adha_layout_bytes.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.POINTER(ctypes.c_uint64)]
+lib.adha_remap.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                           ctypes.c_void_p]
+lib.adha_debug_phase.argtypes = [ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_int]
+
+
+def layout(widths, labels):
+    h = ctypes.c_void_p()
+    rc = lib.adha_layout_create((ctypes.c_uint32 * len(widths))(*widths), len(widths),
+                                (ctypes.c_int32 * len(labels))(*labels), ctypes.byref(h))
+    assert rc == 0
+    return h
+
+
+def nbytes(h, n):
+    b = ctypes.c_uint64()
+    assert lib.adha_layout_bytes(h, n, ctypes.byref(b)) == 0
+    return b.value
+
+
+def phases(reset=True):
+    out = (ctypes.c_ulonglong * 8)()
+    assert lib.adha_debug_phase(out, 1 if reset else 0) == 0
+    return list(out)
+
+
+w16 = [8 if i % 4 == 3 else 4 for i in range(16)]
+cases = [
+    ("C2 AoS->SoA", w16, [0] * 16, list(range(16)), 10_000_000),
+    ("C2 SoA->AoS", w16, list(range(16)), [0] * 16, 10_000_000),
+    ("P2 4xAoS8->AoS", [4] * 32, [i // 8 for i in range(32)], [0] * 32, 2 ** 23),
+    ("g2 AoS->SoA (byte groups)", [2, 4, 6, 4] * 4, [0] * 16, list(range(16)), 20_000_000),
+    ("b24 SoA->AoS (byte groups)", [1] * 24 + [8], list(range(25)), [0] * 25, 20_000_000),
+]
+stream = torch.cuda.current_stream().cuda_stream
+for name, w, ls, ld, n in cases:
+    Ls, Ld = layout(w, ls), layout(w, ld)
+    a = torch.empty(nbytes(Ls, n), dtype=torch.uint8, device="cuda")
+    b = torch.empty(nbytes(Ld, n), dtype=torch.uint8, device="cuda")
+    for _ in range(3):
+        assert lib.adha_remap(a.data_ptr(), Ls, b.data_ptr(), Ld, n, stream) == 0
+    torch.cuda.synchronize()
+    phases(reset=True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    reps = 10
+    for _ in range(reps):
+        lib.adha_remap(a.data_ptr(), Ls, b.data_ptr(), Ld, n, stream)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    p = phases(reset=True)
+    tiles = max(1, p[4])                        # summed over the 8 consumer warps
+    R = sum(w)
+    per = [x / tiles for x in p[:4]]
+    tot = sum(per)
+    print(f"{name:28s} {2 * n * R / ms / 1e6:6.0f} GB/s  per tile & warp (clk): wait_full {per[0]:7.0f}  "
+          f"permute {per[1]:6.0f}  barrier {per[2]:6.0f}  copy_out {per[3]:6.0f}  (sum {tot:6.0f}; "
+          f"{100 * per[0] / tot:4.1f}% waiting for data)  producer wait_empty/tile {p[5] / (tiles / 8):7.0f}  "
+          f"tails/warp {p[7] / 8 / 148 / reps:6.0f}", flush=True)
+    del a, b
+    torch.cuda.empty_cache()
