@@ -1,3 +1,5 @@
+"""Host cost per call: adha_remap and adha_remap_regions launched back to back from Python with the
+GPU queue kept full (time.perf_counter per call), plus a cProfile of the regions call."""
 import os, sys, time, cProfile, pstats
 sys.path.insert(0, "/root/repo")
 import torch

@@ -1,3 +1,5 @@
+"""Single-shot (synchronised, host launch latency included) vs back-to-back per-launch time of
+C2 and the P1/P2 chain edges, with tile-order and L2-hint variants."""
 import os, sys, statistics
 sys.path.insert(0, "/root/repo")
 import torch, paper_1407_4859_b200 as A, bench
