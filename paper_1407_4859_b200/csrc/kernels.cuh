@@ -103,9 +103,12 @@ using TableOf = typename std::conditional<(NG > 0), GroupTable<NG>, EntryTable<N
 
 // NG = 0: unit mode (EntryTable<NENT>, EMAX instructions per warp); NG > 0: byte-group mode
 // (GroupTable<NG>, GMAX slots per warp, U = uint8_t for the tails).
-template <typename U, int NENT, int EMAX, int NG = 0, int GMAX = 1>
-__global__ void __launch_bounds__(NTHREADS, 1)
+// TMAC (unit mode only): a 10th warp writes the permuted tiles back with TMA bulk stores
+// (TiledParams::tma_copy); otherwise the consumers write them back with STG.
+template <typename U, int NENT, int EMAX, int NG = 0, int GMAX = 1, bool TMAC = false>
+__global__ void __launch_bounds__(TMAC ? NTHREADS_TMA : NTHREADS, 1)
     remap_tiled_kernel(const __grid_constant__ TiledParams p, const __grid_constant__ TableOf<NENT, NG> et) {
+    static_assert(!TMAC || NG == 0, "TMA write-back is a unit-mode instantiation");
     extern __shared__ __align__(1024) uint8_t smem[];
     const uint32_t warp = threadIdx.x >> 5;
     const uint32_t lane = threadIdx.x & 31;
@@ -115,14 +118,58 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const uint32_t in0 = sbase + HDR_BYTES;
     const uint32_t out0 = in0 + p.s_in * p.stage_bytes;
 
+    const uint32_t ofull0 = sbase + 16 * MAX_S_IN;     // s_out mbarriers: output tile permuted (tma_copy)
+    const uint32_t oempty0 = ofull0 + 8 * S_OUT_MAX;   // s_out mbarriers: output tile read by its bulk store
     if (threadIdx.x == 0) {
         for (uint32_t s = 0; s < p.s_in; ++s) {
             mbar_init(full0 + 8 * s, 1);
             mbar_init(empty0 + 8 * s, NCONS);
         }
+        for (uint32_t o = 0; o < S_OUT_MAX; ++o) {
+            mbar_init(ofull0 + 8 * o, NCONS * 32);
+            mbar_init(oempty0 + 8 * o, 1);
+        }
         fence_mbarrier_init();
     }
     __syncthreads();
+
+    if (TMAC && warp == NCONS + 1) {
+        // ------------------------------------------------------------ TMA write-back (tma_copy)
+        // Lane 0 writes every permuted tile back with one bulk store per dst chunk once the
+        // consumers arrive on out_full[o]; tile i-1's buffer is released (out_empty) as soon as its
+        // bulk group has finished reading shared memory, so the store overlaps the next
+        // permutation.  Chosen per launch for components with one large dst chunk per tile.
+        if (lane != 0) return;
+        const uint64_t pol = policy_evict_first();
+        uint32_t i = 0, k = 0;
+        int prev_o = -1;
+        for (int64_t t = t_first(p), te = t_end(p); t < te; t += t_step(p), ++i) {
+            while (t >= p.comp[k].tile_base + p.comp[k].n_tiles) ++k;
+            const CompDesc& K = p.comp[k];
+            const uint32_t o = p.s_out == 2 ? (i & 1u) : 0u;
+            const uint32_t j = p.s_out == 2 ? (i >> 1) : i;
+            mbar_wait(ofull0 + 8 * o, j & 1u);
+            const uint32_t ob = out0 + o * p.stage_bytes;
+            const int64_t lt = t - K.tile_base;
+            for (uint32_t c = K.dc_lo; c < K.dc_hi; ++c) {
+                const uint32_t bytes = K.T * p.dstc[c].stride;
+                uint8_t* g = (uint8_t*)p.dst + p.dstc[c].region + (uint64_t)lt * bytes;
+                if (p.l2_hints & 2) bulk_store_hint(g, ob + p.dstc[c].smem, bytes, pol);
+                else bulk_store(g, ob + p.dstc[c].smem, bytes);
+            }
+            bulk_commit();
+            if (p.s_out == 2) {
+                bulk_wait_read<1>();                       // tile i-1's group has read its buffer
+                if (prev_o >= 0) mbar_arrive(oempty0 + 8 * prev_o);
+            } else {
+                bulk_wait_read<0>();
+                mbar_arrive(oempty0 + 8 * o);
+            }
+            prev_o = (int)o;
+        }
+        bulk_wait_all();
+        return;
+    }
 
     if (warp == NCONS) {
         // ------------------------------------------------------------ TMA producer
@@ -273,6 +320,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     int k_cur = -1;
     uint32_t stage = 0, phase = 0, oslot = 0, k = 0;
     ADHA_PT(long long ntile = 0);
+    constexpr bool tmac = TMAC;      // compile-time: the STG instantiations are the plain kernel
+    uint32_t i_t = 0, zeroed = 0;
     for (int64_t t = t_first(p), te = t_end(p); t < te; t += t_step(p)) {
         while (t >= p.comp[k].tile_base + p.comp[k].n_tiles) ++k;
         const int64_t lt = t - p.comp[k].tile_base;
@@ -280,8 +329,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         if ((int)k != k_cur) {
             // this warp's instructions of component k: i = warp + NCONS*e; lane's unit = entry i*32 + lane
             k_cur = (int)k;
-            nv = copy_plan(p, p.comp[k].dc_lo, T, p.comp[k].out_bytes, tid, gofs, gstep);
-            if (p.comp[k].flags & CF_ZERO_OUT) {
+            zeroed = 0;
+            if (!tmac) nv = copy_plan(p, p.comp[k].dc_lo, T, p.comp[k].out_bytes, tid, gofs, gstep);
+            if (!tmac && (p.comp[k].flags & CF_ZERO_OUT)) {
                 // dst records have padding the permutation never writes: zero both output buffers
                 // once for this component (the same positions stay untouched in every tile)
                 named_bar_sync(1, NCONS * 32);
@@ -342,12 +392,25 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             }
         }
         ADHA_PT(const long long c0 = clock64());
+        if (tmac) {
+            // output buffer o of this tile: wait until the bulk store of its previous tile read it
+            const uint32_t o = p.s_out == 2 ? (i_t & 1u) : 0u;
+            const uint32_t j = p.s_out == 2 ? (i_t >> 1) : i_t;
+            if (j > 0) mbar_wait(oempty0 + 8 * o, (j - 1) & 1u);
+            oslot = o;
+            if ((p.comp[k].flags & CF_ZERO_OUT) && !((zeroed >> o) & 1u)) {
+                const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+                for (uint32_t v = tid * 16; v < p.stage_bytes; v += NCONS * 32 * 16) sts128(out0 + o * p.stage_bytes + v, z);
+                named_bar_sync(1, NCONS * 32);
+                zeroed |= 1u << o;
+            }
+        }
         mbar_wait(full0 + 8 * stage, phase);
         ADHA_PT(const long long c1 = clock64(); ph[0] += c1 - c0; ++ntile);
         const uint32_t ib = in0 + stage * p.stage_bytes;
         {
             const uint32_t ob = out0 + oslot * p.stage_bytes;
-            if (p.s_out == 1) named_bar_sync(1, NCONS * 32);   // previous copy-out done with the buffer
+            if (!tmac && p.s_out == 1) named_bar_sync(1, NCONS * 32);   // previous copy-out done with the buffer
             if (p.comp[k].identity) {
                 // same cluster on both sides: the staged chunk is already the output chunk; move it
                 // to the output buffer with 16-byte shared copies so the input stage is released as
@@ -430,12 +493,18 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(empty0 + 8 * stage);    // input stage free for the producer
             ADHA_PT(const long long c2 = clock64(); ph[1] += c2 - c1);
-            named_bar_sync(1, NCONS * 32);                      // output tile complete
-            ADHA_PT(const long long c3 = clock64(); ph[2] += c3 - c2);
-            if (p.l2_hints & 2) copy_out<true>((uint8_t*)p.dst, ob, tid, lt, nv, gofs, gstep, spol);
-            else copy_out<false>((uint8_t*)p.dst, ob, tid, lt, nv, gofs, gstep, spol);
-            ADHA_PT(ph[3] += clock64() - c3);
-            if (p.s_out == 2) oslot ^= 1;
+            if (tmac) {
+                fence_proxy_async_smem();                       // this thread's smem writes -> the bulk store
+                mbar_arrive(ofull0 + 8 * oslot);
+                ++i_t;
+            } else {
+                named_bar_sync(1, NCONS * 32);                  // output tile complete
+                ADHA_PT(const long long c3 = clock64(); ph[2] += c3 - c2);
+                if (p.l2_hints & 2) copy_out<true>((uint8_t*)p.dst, ob, tid, lt, nv, gofs, gstep, spol);
+                else copy_out<false>((uint8_t*)p.dst, ob, tid, lt, nv, gofs, gstep, spol);
+                ADHA_PT(ph[3] += clock64() - c3);
+                if (p.s_out == 2) oslot ^= 1;
+            }
         }
         if (++stage == p.s_in) { stage = 0; phase ^= 1; }
     }

@@ -48,27 +48,28 @@ namespace detail {
 
 typedef void (*TiledLauncher)(dim3, dim3, size_t, cudaStream_t, const TiledParams&, const void* table);
 
-template <typename U, int CLS>
+template <typename U, int CLS, bool TMAC>
 void launch_tiled(dim3 grid, dim3 block, size_t smem, cudaStream_t st, const TiledParams& p, const void* table) {
     constexpr int NENT = CLASS_NENT[CLS];
     constexpr int EMAX = CLASS_EMAX[CLS];
-    remap_tiled_kernel<U, NENT, EMAX><<<grid, block, smem, st>>>(p, *static_cast<const EntryTable<NENT>*>(table));
+    remap_tiled_kernel<U, NENT, EMAX, 0, 1, TMAC><<<grid, block, smem, st>>>(
+        p, *static_cast<const EntryTable<NENT>*>(table));
 }
 
-template <typename U, int CLS>
+template <typename U, int CLS, bool TMAC>
 const void* tiled_fn() {
     constexpr int NENT = CLASS_NENT[CLS];
     constexpr int EMAX = CLASS_EMAX[CLS];
-    return (const void*)&remap_tiled_kernel<U, NENT, EMAX>;
+    return (const void*)&remap_tiled_kernel<U, NENT, EMAX, 0, 1, TMAC>;
 }
 
-template <typename U>
+template <typename U, bool TMAC>
 TiledLauncher pick_cls(int cls, const void** fn) {
     switch (cls) {
-        case 0: *fn = tiled_fn<U, 0>(); return &launch_tiled<U, 0>;
-        case 1: *fn = tiled_fn<U, 1>(); return &launch_tiled<U, 1>;
-        case 2: *fn = tiled_fn<U, 2>(); return &launch_tiled<U, 2>;
-        default: *fn = tiled_fn<U, 3>(); return &launch_tiled<U, 3>;
+        case 0: *fn = tiled_fn<U, 0, TMAC>(); return &launch_tiled<U, 0, TMAC>;
+        case 1: *fn = tiled_fn<U, 1, TMAC>(); return &launch_tiled<U, 1, TMAC>;
+        case 2: *fn = tiled_fn<U, 2, TMAC>(); return &launch_tiled<U, 2, TMAC>;
+        default: *fn = tiled_fn<U, 3, TMAC>(); return &launch_tiled<U, 3, TMAC>;
     }
 }
 
@@ -89,10 +90,15 @@ TiledLauncher pick_groups(int gcls, const void** fn) {
     return &launch_groups<1>;
 }
 
-TiledLauncher pick(uint32_t unit, int cls, const void** fn) {
-    if (unit == 4) return pick_cls<uint32_t>(cls, fn);
-    if (unit == 2) return pick_cls<uint16_t>(cls, fn);
-    return pick_cls<uint8_t>(cls, fn);
+TiledLauncher pick(uint32_t unit, int cls, bool tma, const void** fn) {
+    if (tma) {
+        if (unit == 4) return pick_cls<uint32_t, true>(cls, fn);
+        if (unit == 2) return pick_cls<uint16_t, true>(cls, fn);
+        return pick_cls<uint8_t, true>(cls, fn);
+    }
+    if (unit == 4) return pick_cls<uint32_t, false>(cls, fn);
+    if (unit == 2) return pick_cls<uint16_t, false>(cls, fn);
+    return pick_cls<uint8_t, false>(cls, fn);
 }
 
 struct PlanCache {
@@ -123,7 +129,7 @@ adha_status cuda_fail(cudaError_t e, const char* what) {
 }
 
 // per-device setup: SM count and the kernel's dynamic shared memory opt-in
-adha_status device_setup(const void* fn, int* n_sm) {
+adha_status device_setup(const void* fn, int* n_sm, int threads = NTHREADS) {
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
@@ -143,9 +149,9 @@ adha_status device_setup(const void* fn, int* n_sm) {
         cudaFuncAttributes fa;
         e = cudaFuncGetAttributes(&fa, fn);
         if (e != cudaSuccess) return cuda_fail(e, "cudaFuncGetAttributes");
-        if (fa.maxThreadsPerBlock < NTHREADS)      // register budget regression guard
+        if (fa.maxThreadsPerBlock < threads)       // register budget regression guard
             return fail(ADHA_ERR_UNSUPPORTED, "remap_tiled_kernel uses " + std::to_string(fa.numRegs) +
-                                                  " registers: cannot launch " + std::to_string(NTHREADS) + " threads");
+                                                  " registers: cannot launch " + std::to_string(threads) + " threads");
         c.attr_done.insert({dev, fn});
     }
     return ADHA_OK;
@@ -248,11 +254,8 @@ adha_status remap_checked(const uint8_t* src, const Layout& ls, uint8_t* dst, co
     if (!plan->tiled || (uint64_t)n * ls.record_bytes <= small_bytes())
         return launch_naive(src, ls, ck.bs, dst, ld, ck.bd, 0, n, st);
 
-    const void* fn = nullptr;
-    TiledLauncher launch = plan->byte_groups ? pick_groups(plan->group_class, &fn)
-                                             : pick(plan->unit, plan->table_class, &fn);
     int n_sm = 0;
-    adha_status s = device_setup(fn, &n_sm);
+    adha_status s = device_setup(nullptr, &n_sm);
     if (s != ADHA_OK) return s;
 
     auto P = std::make_unique<TiledParams>();
@@ -314,10 +317,43 @@ adha_status remap_checked(const uint8_t* src, const Layout& ls, uint8_t* dst, co
         D.f_hi = (uint16_t)fi;
     }
     P->total_tiles = tiles;
+    // Write-back mode (unit mode).  TMA bulk stores by a 10th warp when every component with
+    // tiles has ONE dst chunk of >= 32 KB per tile and at most 8 src chunks: K-Means SoA->4xAoS8
+    // +1.3 %, 4xAoS8->AoS +3 % (profiles/r01_notes.md).  Many small dst chunks queue behind the
+    // loads in the per-SM TMA engine (C2 AoS->SoA -26 % if forced) and more src chunks gain
+    // nothing (Medical SoA->AoS, 9), so those keep the consumers' STG write-back.  Only for dst
+    // in this device's HBM.  ADHA_COPYOUT = stg | tma overrides (tests, A/B).
+    {
+        const char* cm = std::getenv("ADHA_COPYOUT");
+        bool tma = false;
+        if (ck.dst_local && !plan->byte_groups) {
+            if (cm && std::strcmp(cm, "tma") == 0) {
+                tma = true;
+            } else if (!(cm && std::strcmp(cm, "stg") == 0)) {
+                bool any = false;
+                tma = true;
+                for (size_t k = 0; k < plan->comps.size(); ++k) {
+                    if (P->comp[k].n_tiles == 0) continue;
+                    any = true;
+                    const RemapPlan::Comp& K = plan->comps[k];
+                    if (K.dst_clusters.size() != 1 || K.src_clusters.size() > 8 || P->comp[k].out_bytes < 32768)
+                        tma = false;
+                }
+                tma = tma && any;
+            }
+        }
+        P->tma_copy = tma ? 1u : 0u;
+    }
+    const void* fn = nullptr;
+    TiledLauncher launch = plan->byte_groups ? pick_groups(plan->group_class, &fn)
+                                             : pick(plan->unit, plan->table_class, P->tma_copy != 0, &fn);
+    const int threads = P->tma_copy ? NTHREADS_TMA : NTHREADS;
+    s = device_setup(fn, &n_sm, threads);
+    if (s != ADHA_OK) return s;
     // a tail-only call still needs one CTA per component tail
     const int64_t grid = std::max<int64_t>(std::min<int64_t>((int64_t)plan->comps.size(), n_sm),
                                            std::min<int64_t>(tiles, n_sm));
-    launch(dim3((unsigned)std::max<int64_t>(grid, 1)), dim3(NTHREADS), plan->smem_bytes, st, *P, plan->table.data());
+    launch(dim3((unsigned)std::max<int64_t>(grid, 1)), dim3(threads), plan->smem_bytes, st, *P, plan->table.data());
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "remap_tiled_kernel launch");
     return ADHA_OK;
@@ -329,12 +365,16 @@ adha_status remap_checked(const uint8_t* src, const Layout& ls, uint8_t* dst, co
 using namespace adha;
 using namespace adha::detail;
 
+// set by adha_remap_peer around its adha_remap call: dst is another device's memory
+static thread_local bool g_dst_remote = false;
+
 extern "C" adha_status adha_remap(const void* src, const adha_layout* hs, void* dst, const adha_layout* hd,
                                   int64_t n, void* stream) {
     clear_error();
     Checked ck;
     adha_status s = validate(src, hs, dst, hd, n, &ck, true);
     if (s != ADHA_OK) return s;
+    ck.dst_local = !g_dst_remote;
     return remap_checked((const uint8_t*)src, hs->L, (uint8_t*)dst, hd->L, n, ck, (cudaStream_t)stream);
 }
 
@@ -541,7 +581,11 @@ extern "C" adha_status adha_remap_peer(const void* src, const adha_layout* hs, i
         if (out == ADHA_OK) out = check_device_pointer(dst, dst_device, "dst");
     }
     if (out == ADHA_OK && src_device != dst_device) out = enable_peer(src_device, dst_device);
-    if (out == ADHA_OK) out = adha_remap(src, hs, dst, hd, n, stream);
+    if (out == ADHA_OK) {
+        g_dst_remote = src_device != dst_device;    // no TMA write-back into peer memory
+        out = adha_remap(src, hs, dst, hd, n, stream);
+        g_dst_remote = false;
+    }
     std::string msg = adha_last_error();
     cudaSetDevice(prev);
     if (out != ADHA_OK) set_error(msg);

@@ -95,7 +95,10 @@ extern "C" adha_status adha_remap_host(const void* src_host, const adha_layout* 
     if (mode == "auto") mode = (dst_pinned && aligned && scratch) ? "hybrid" : "staged";
     if ((mode == "zero" && !(src_pinned && dst_pinned && aligned)) || (mode == "hybrid" && !(dst_pinned && aligned)))
         mode = "staged";
-    if (mode == "zero") return remap_checked((const uint8_t*)src_host, ls, (uint8_t*)dst_host, ld, n, ck, user);
+    if (mode == "zero") {
+        ck.dst_local = false;                // dst is pinned host memory: STG write-back
+        return remap_checked((const uint8_t*)src_host, ls, (uint8_t*)dst_host, ld, n, ck, user);
+    }
 
     if (!scratch || ((uintptr_t)scratch & 255)) return fail(ADHA_ERR_ALIGNMENT, "scratch must be 256-byte aligned");
     const bool hybrid = mode == "hybrid";
@@ -164,6 +167,7 @@ extern "C" adha_status adha_remap_host(const void* src_host, const adha_layout* 
             // dst regions of this chunk inside the host buffer: base_c(N) + lo * stride_c
             cm.bd.resize(ld.n_clusters());
             for (int c = 0; c < ld.n_clusters(); ++c) cm.bd[c] = ck.bd[c] + (uint64_t)lo * ld.stride[c];
+            cm.dst_local = false;            // the kernel stores into pinned host memory
             if ((s = remap_checked(dsrc, ls, hdst, ld, m, cm, st)) != ADHA_OK) return s;
         } else {
             cm.bd = md;

@@ -41,6 +41,7 @@ namespace dev {
 
 constexpr int NCONS = 8;                       // consumer warps per CTA
 constexpr int NTHREADS = (NCONS + 1) * 32;     // + one TMA producer warp
+constexpr int NTHREADS_TMA = (NCONS + 2) * 32; // + a TMA write-back warp (tma_copy instantiations)
 constexpr int MAXC = 128;                      // clusters per side (tiled kernel)
 constexpr int MAXF = 256;                      // fields (tiled kernel tail table, naive chunk)
 constexpr int MAXK = 64;                       // components
@@ -93,7 +94,7 @@ struct TiledParams {
     uint32_t l2_hints;    // bit 0: TMA loads with L2 evict_first; bit 1: stores with L2 evict_first
     uint32_t blocked;     // 1: CTA b processes a contiguous tile range, 0: tiles b, b+G, b+2G, ...
     uint32_t tma_split;   // 0: one bulk load per src chunk; else pieces of at most this many bytes
-    uint32_t pad1;
+    uint32_t tma_copy;    // 1: tiles written back by the write-back warp with TMA bulk stores, else STG by the consumers
     CompDesc comp[MAXK];
     ClusterDesc srcc[MAXC];
     ClusterDesc dstc[MAXC];

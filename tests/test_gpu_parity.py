@@ -644,3 +644,23 @@ def test_concurrent_remap_host_threads(monkeypatch):
     assert not errors, errors
     for k, (src_np, got) in out.items():
         assert np.array_equal(got, oracle_dst(src_np, ls, ld, widths, n)), k
+
+
+@pytest.mark.parametrize("mode", ["tma", "stg", "auto"])
+def test_write_back_modes(mode, monkeypatch):
+    """Both write-back paths of the tiled kernel (consumer STG, or the TMA bulk-store warp chosen per
+    launch for one large dst chunk per tile) are bit-exact, forced either way: K-Means chain edges,
+    AoS->SoA (many small chunks), C-aligned and AoSoA dst (pre-zeroed padding), ragged N."""
+    if mode != "auto":
+        monkeypatch.setenv("ADHA_COPYOUT", mode)
+    monkeypatch.setenv("ADHA_SMALL_BYTES", "0")
+    w32 = [4] * 32
+    cases = [
+        (w32, list(range(32)), None, False, [i // 8 for i in range(32)], None, False, 200_003),
+        (w32, [i // 8 for i in range(32)], None, False, [0] * 32, None, False, 100_001),
+        (config_widths(16), [0] * 16, None, False, list(range(16)), None, False, 70_001),
+        ([4, 8, 4, 4, 8], list(range(5)), None, False, [0] * 5, None, True, 50_017),
+        ([4, 4, 8, 4], list(range(4)), None, False, [0] * 4, [8] * 4, False, 33_333),
+    ]
+    for w, ls, bs, als, ld, bd, ald, n in cases:
+        check_pair_ex(w, ls, bs, als, ld, bd, ald, n, seed=n % 97)

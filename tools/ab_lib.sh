@@ -8,7 +8,7 @@ for round in 1 2; do
     if [ "$v" = cur ]; then cp /tmp/libadha_cur.so paper_1407_4859_b200/libadha.so; else cp "$v" paper_1407_4859_b200/libadha.so; fi
     echo "== $v round $round"
     python tools/power_probe.py 3 2>&1 | grep "remap C2" | tail -1
-    NARROW=1 CFGS=C2,P1,P2,C4 ROUNDS=3 python tools/ab_multi.py "" 2>&1 | tail -14 | tr '\n' ' '; echo
+    NARROW=1 CFGS=${CFGS:-C2,P1,P2,C4} ROUNDS=3 python tools/ab_multi.py "" 2>&1 | tail -14 | tr '\n' ' '; echo
   done
 done
 cp /tmp/libadha_cur.so paper_1407_4859_b200/libadha.so
