@@ -103,12 +103,11 @@ using TableOf = typename std::conditional<(NG > 0), GroupTable<NG>, EntryTable<N
 
 // NG = 0: unit mode (EntryTable<NENT>, EMAX instructions per warp); NG > 0: byte-group mode
 // (GroupTable<NG>, GMAX slots per warp, U = uint8_t for the tails).
-// TMAC (unit mode only): a 10th warp writes the permuted tiles back with TMA bulk stores
-// (TiledParams::tma_copy); otherwise the consumers write them back with STG.
+// TMAC: a 10th warp writes the permuted tiles back with TMA bulk stores (TiledParams::tma_copy);
+// otherwise the consumers write them back with STG.
 template <typename U, int NENT, int EMAX, int NG = 0, int GMAX = 1, bool TMAC = false>
 __global__ void __launch_bounds__(TMAC ? NTHREADS_TMA : NTHREADS, 1)
     remap_tiled_kernel(const __grid_constant__ TiledParams p, const __grid_constant__ TableOf<NENT, NG> et) {
-    static_assert(!TMAC || NG == 0, "TMA write-back is a unit-mode instantiation");
     extern __shared__ __align__(1024) uint8_t smem[];
     const uint32_t warp = threadIdx.x >> 5;
     const uint32_t lane = threadIdx.x & 31;

@@ -73,21 +73,27 @@ TiledLauncher pick_cls(int cls, const void** fn) {
     }
 }
 
-template <int GC>
+template <int GC, bool TMAC>
 void launch_groups(dim3 grid, dim3 block, size_t smem, cudaStream_t st, const TiledParams& p, const void* table) {
     constexpr int NG = GCLASS_NG[GC];
     constexpr int GMAX = GCLASS_GMAX[GC];
-    remap_tiled_kernel<uint8_t, 32, 1, NG, GMAX><<<grid, block, smem, st>>>(p, *static_cast<const GroupTable<NG>*>(table));
+    remap_tiled_kernel<uint8_t, 32, 1, NG, GMAX, TMAC><<<grid, block, smem, st>>>(
+        p, *static_cast<const GroupTable<NG>*>(table));
 }
-template <int GC>
+template <int GC, bool TMAC>
 const void* groups_fn() {
-    return (const void*)&remap_tiled_kernel<uint8_t, 32, 1, GCLASS_NG[GC], GCLASS_GMAX[GC]>;
+    return (const void*)&remap_tiled_kernel<uint8_t, 32, 1, GCLASS_NG[GC], GCLASS_GMAX[GC], TMAC>;
 }
 
-TiledLauncher pick_groups(int gcls, const void** fn) {
-    if (gcls == 0) { *fn = groups_fn<0>(); return &launch_groups<0>; }
-    *fn = groups_fn<1>();
-    return &launch_groups<1>;
+TiledLauncher pick_groups(int gcls, bool tma, const void** fn) {
+    if (tma) {
+        if (gcls == 0) { *fn = groups_fn<0, true>(); return &launch_groups<0, true>; }
+        *fn = groups_fn<1, true>();
+        return &launch_groups<1, true>;
+    }
+    if (gcls == 0) { *fn = groups_fn<0, false>(); return &launch_groups<0, false>; }
+    *fn = groups_fn<1, false>();
+    return &launch_groups<1, false>;
 }
 
 TiledLauncher pick(uint32_t unit, int cls, bool tma, const void** fn) {
@@ -326,7 +332,7 @@ adha_status remap_checked(const uint8_t* src, const Layout& ls, uint8_t* dst, co
     {
         const char* cm = std::getenv("ADHA_COPYOUT");
         bool tma = false;
-        if (ck.dst_local && !plan->byte_groups) {
+        if (ck.dst_local) {
             if (cm && std::strcmp(cm, "tma") == 0) {
                 tma = true;
             } else if (!(cm && std::strcmp(cm, "stg") == 0)) {
@@ -336,7 +342,10 @@ adha_status remap_checked(const uint8_t* src, const Layout& ls, uint8_t* dst, co
                     if (P->comp[k].n_tiles == 0) continue;
                     any = true;
                     const RemapPlan::Comp& K = plan->comps[k];
-                    if (K.dst_clusters.size() != 1 || K.src_clusters.size() > 8 || P->comp[k].out_bytes < 32768)
+                    // byte-group mode: the slower permutation gains more from the overlap (2-byte
+                    // SoA->AoS +16 % with 16 src chunks), 25 src chunks lose (1-byte, -6 %)
+                    const size_t max_src = plan->byte_groups ? 16 : 8;
+                    if (K.dst_clusters.size() != 1 || K.src_clusters.size() > max_src || P->comp[k].out_bytes < 32768)
                         tma = false;
                 }
                 tma = tma && any;
@@ -345,7 +354,7 @@ adha_status remap_checked(const uint8_t* src, const Layout& ls, uint8_t* dst, co
         P->tma_copy = tma ? 1u : 0u;
     }
     const void* fn = nullptr;
-    TiledLauncher launch = plan->byte_groups ? pick_groups(plan->group_class, &fn)
+    TiledLauncher launch = plan->byte_groups ? pick_groups(plan->group_class, P->tma_copy != 0, &fn)
                                              : pick(plan->unit, plan->table_class, P->tma_copy != 0, &fn);
     const int threads = P->tma_copy ? NTHREADS_TMA : NTHREADS;
     s = device_setup(fn, &n_sm, threads);
