@@ -266,6 +266,57 @@ ADHA_API adha_status adha_remap_host(const void* src_host, const adha_layout* sr
                             int64_t n_records, void* scratch, uint64_t scratch_bytes,
                             void* stream);
 
+/* ------------------------------------------------------------------ in-place remap
+ *
+ * The remap of adha_remap with src and dst in ONE device buffer (SURVEY.md 8(f) N1,
+ * "in-place"; the paper's remap edge, names no storage, reading Q5):
+ * after the call the buffer holds the N records in dst_layout,
+ *     buf[addr_Ld(f, i) .. + w_f) = (old buf)[addr_Ls(f, i) .. + w_f)   for all i < N, f,
+ * and every other byte of the buffer is unspecified.  The buffer needs
+ * max(bytes(Ls, N), bytes(Ld, N)) bytes, not their sum, so an array that fills most of HBM
+ * can still change layout.  Packed, unblocked layouts only (no ADHA_LAYOUT_ALIGNED, no
+ * AoSoA blocks).  Cost: the buffer is cut into S-byte slots (S in 256..4096); tiles of
+ * T = S/u records (u = largest power of two <= 16 dividing every width) of each cluster whose
+ * member set changes are transposed in place, every slot is moved along the cycles of a slot
+ * permutation, and the dst tiles are transposed back.  Clusters that keep their member set
+ * and their region base move no byte (the moved-subset rule).
+ *
+ * Usage: plan = create(Ls, Ld, N) [host only]; upload(plan, workspace) once; then
+ * adha_remap_inplace(buf, ...) any number of times (each call remaps the buffer's current
+ * contents from Ls to Ld).  The workspace (device, 256-byte aligned, plan-sized, see
+ * adha_inplace_plan_info) belongs to the plan while it is in use and must not overlap buf. */
+typedef struct adha_inplace_plan adha_inplace_plan;
+
+/* Host-side plan (slot permutation, its cycles, workspace layout) for an N-record buffer.
+ * Errors: INVALID_ARG (null, N < 0), LAYOUT_MISMATCH, TOO_LARGE, UNSUPPORTED (aligned or
+ * blocked layout; a changed cluster record too wide for a tile in shared memory), OOM. */
+ADHA_API adha_status adha_inplace_plan_create(const adha_layout* src_layout, const adha_layout* dst_layout,
+                                              int64_t n_records, adha_inplace_plan** out);
+
+/* buffer_bytes = max(bytes(Ls, N), bytes(Ld, N)); workspace_bytes = device workspace the plan
+ * needs (tables, one saved slot per cycle segment, the packed tail records).  Either may be NULL. */
+ADHA_API adha_status adha_inplace_plan_info(const adha_inplace_plan* plan, uint64_t* buffer_bytes,
+                                            uint64_t* workspace_bytes);
+
+/* JSON statistics of the plan (slot size, tile records, moved / fixed slots, cycles, segments,
+ * device traffic of one run); free with adha_free. */
+ADHA_API adha_status adha_inplace_plan_describe(const adha_inplace_plan* plan, char** json_out);
+
+/* Copy the plan's tables into `workspace` (device memory of the current device) on `stream`
+ * and wait for the copy.  Errors: INVALID_ARG (null, workspace too small), ALIGNMENT, CUDA. */
+ADHA_API adha_status adha_inplace_plan_upload(adha_inplace_plan* plan, void* workspace, uint64_t workspace_bytes,
+                                              void* stream);
+
+/* Enqueue the in-place remap of `buf` (device, 256-byte aligned, buf_bytes >= buffer_bytes)
+ * on `stream` (up to 6 kernel launches; allocates nothing).  Asynchronous like adha_remap.
+ * Errors: INVALID_ARG (null, buffer too small, plan not uploaded to this workspace on the
+ * current device), ALIGNMENT, OVERLAP (workspace inside the buffer), CUDA. */
+ADHA_API adha_status adha_remap_inplace(void* buf, uint64_t buf_bytes, const adha_inplace_plan* plan,
+                                        void* workspace, void* stream);
+
+/* Destroy a plan.  NULL is ok. */
+ADHA_API void adha_inplace_plan_destroy(adha_inplace_plan* plan);
+
 /* JSON description of the compiled remap plan for a layout pair (tile records,
  * pipeline stages, unit size, per-instruction table, kernel choice) -- for
  * tests and tooling; the hot path never calls it.  Free with adha_free. */

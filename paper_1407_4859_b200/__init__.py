@@ -66,6 +66,12 @@ _SIGS = {
     "adha_plan_pdl": (ctypes.c_int, [_cp, _cp, _cp, ctypes.POINTER(_vp)]),
     "adha_plan_candidates": (ctypes.c_int, [_cp, _cp, _cp, ctypes.POINTER(_vp)]),
     "adha_section_run": (ctypes.c_int, [_vp, _L, _i64, ctypes.POINTER(_i32), _i32, _vp, _i64, _vp, _vp]),
+    "adha_inplace_plan_create": (ctypes.c_int, [_L, _L, _i64, ctypes.POINTER(_vp)]),
+    "adha_inplace_plan_info": (ctypes.c_int, [_vp, ctypes.POINTER(_u64), ctypes.POINTER(_u64)]),
+    "adha_inplace_plan_describe": (ctypes.c_int, [_vp, ctypes.POINTER(_vp)]),
+    "adha_inplace_plan_upload": (ctypes.c_int, [_vp, _vp, _u64, _vp]),
+    "adha_remap_inplace": (ctypes.c_int, [_vp, _u64, _vp, _vp, _vp]),
+    "adha_inplace_plan_destroy": (None, [_vp]),
 }
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -384,6 +390,55 @@ def section_run(buf, layout: Layout, n_records: int, fields: Sequence[int], out,
                                  _ptr(idx), n_out, _ptr(out), _stream(stream)))
 
 
+class InplacePlan:
+    """Plan of an in-place remap of an n_records buffer from src_layout to dst_layout
+    (adha.h adha_inplace_plan_create; host only).  `buffer_bytes` is what the buffer needs
+    (max of both layouts), `workspace_bytes` the device workspace; `upload(workspace)` copies
+    the plan's tables there once, then `remap_inplace(buf, plan)` runs it."""
+
+    def __init__(self, src_layout: Layout, dst_layout: Layout, n_records: int):
+        h = _vp()
+        _check(_lib.adha_inplace_plan_create(src_layout.handle, dst_layout.handle, int(n_records), ctypes.byref(h)))
+        self._h = h
+        self.src_layout, self.dst_layout, self.n_records = src_layout, dst_layout, int(n_records)
+        b, w = _u64(), _u64()
+        _check(_lib.adha_inplace_plan_info(h, ctypes.byref(b), ctypes.byref(w)))
+        self.buffer_bytes, self.workspace_bytes = b.value, w.value
+        self.workspace = None
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and _lib is not None:
+            try:
+                _lib.adha_inplace_plan_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    def describe(self) -> dict:
+        p = _vp()
+        _check(_lib.adha_inplace_plan_describe(self._h, ctypes.byref(p)))
+        return json.loads(_take_string(p))
+
+    def upload(self, workspace=None, stream=None):
+        """Copy the tables into `workspace` (a uint8 CUDA tensor of >= workspace_bytes; allocated
+        on the current device when None) and keep a reference to it."""
+        if workspace is None:
+            import torch
+            workspace = torch.empty(max(self.workspace_bytes, 256), dtype=torch.uint8, device="cuda")
+        _check(_lib.adha_inplace_plan_upload(self._h, _ptr(workspace), int(_nbytes(workspace)), _stream(stream)))
+        self.workspace = workspace
+        return workspace
+
+
+def remap_inplace(buf, plan: InplacePlan, stream=None) -> None:
+    """Enqueue the in-place remap of `buf` (uint8 CUDA tensor of >= plan.buffer_bytes) from the
+    plan's src layout to its dst layout (adha_remap_inplace).  Uploads the plan on first use."""
+    if plan.workspace is None:
+        plan.upload(stream=stream)
+    _check(_lib.adha_remap_inplace(_ptr(buf), int(_nbytes(buf)), plan._h, _ptr(plan.workspace), _stream(stream)))
+
+
 def plan_layouts(plan: dict, field_names: Sequence[str], widths: Sequence[int]) -> List[Layout]:
     """One Layout per run of a PDL plan (adha_plan_pdl output), in execution order.  Consecutive
     runs with different layouts are the plan's remap edges."""
@@ -404,5 +459,5 @@ def run_plan_remaps(plan: dict, field_names: Sequence[str], widths: Sequence[int
 
 
 __all__ = ["Layout", "AdhaError", "remap", "remap_regions", "remap_chain", "plan_layouts", "run_plan_remaps",
-           "plan_candidates", "section_run", "shard_range", "remap_sharded", "remap_host",
+           "plan_candidates", "section_run", "InplacePlan", "remap_inplace", "shard_range", "remap_sharded", "remap_host",
            "plan_describe", "plan_ods", "plan_pdl", "version", "LIB_PATH"]

@@ -1,0 +1,280 @@
+// inplace_plan.cpp -- host plan of the in-place remap (adha.h
+// adha_inplace_plan_create).  See inplace_plan.h for the three steps.
+//
+// The remap itself is the one of adha_remap:
+//     dst[addr_Ld(f, i) .. + w_f) = src[addr_Ls(f, i) .. + w_f)
+// with dst and src the same buffer.  This file computes, once per (Ls, Ld, N), which S-byte
+// slot goes where (a permutation of slot indices), its cycles, and the workspace layout.
+#include <algorithm>
+#include <cstring>
+#include <string>
+
+#include "inplace_plan.h"
+
+namespace adha {
+
+namespace {
+
+uint32_t pow2_unit(const Layout& l) {
+    uint32_t u = 16;
+    for (int32_t f = 0; f < l.n_fields; ++f)
+        while (l.width[f] % u) u >>= 1;
+    return u;
+}
+
+bool same_members(const Layout& a, int32_t ca, const Layout& b, int32_t cb) {
+    return a.members[ca] == b.members[cb];
+}
+
+// field of cluster c at byte offset o of the cluster record (packed layouts: fields tile the record)
+int32_t field_at(const Layout& l, int32_t c, uint32_t o) {
+    const auto& mem = l.members[c];
+    int32_t lo = 0, hi = (int32_t)mem.size() - 1;
+    while (lo < hi) {   // last member with offset <= o
+        const int32_t mid = (lo + hi + 1) / 2;
+        if (l.offset[mem[mid]] <= o) lo = mid; else hi = mid - 1;
+    }
+    return mem[lo];
+}
+
+uint64_t smem_need(uint32_t T, uint32_t K, uint32_t u) {
+    // staged tile plus 4 bytes of padding per line (rows when record-major, columns otherwise)
+    return (uint64_t)T * K * u + 4ull * std::max<uint64_t>(T, K) + 16;
+}
+
+}  // namespace
+
+adha_status inplace_plan_build(const Layout& ls, const Layout& ld, int64_t n, InplacePlan* p) {
+    if (n < 0) return fail(ADHA_ERR_INVALID_ARG, "n_records < 0");
+    if (ls.n_fields != ld.n_fields) return fail(ADHA_ERR_LAYOUT_MISMATCH, "layouts differ in field count");
+    for (int32_t f = 0; f < ls.n_fields; ++f)
+        if (ls.width[f] != ld.width[f])
+            return fail(ADHA_ERR_LAYOUT_MISMATCH, "field " + std::to_string(f) + " differs in width");
+    for (const Layout* l : {&ls, &ld}) {
+        if (l->aligned) return fail(ADHA_ERR_UNSUPPORTED, "in-place remap: packed layouts only (no alignment padding)");
+        for (uint32_t b : l->block)
+            if (b != 1) return fail(ADHA_ERR_UNSUPPORTED, "in-place remap: unblocked layouts only (no AoSoA)");
+    }
+    p->ls = ls;
+    p->ld = ld;
+    p->n = n;
+    if (!ls.region_bases(n, p->bs, &p->bytes_s) || !ld.region_bases(n, p->bd, &p->bytes_d))
+        return fail(ADHA_ERR_TOO_LARGE, "N * record bytes overflows");
+    const uint32_t u = pow2_unit(ls);
+    p->u = u;
+
+    // clusters kept as raw slots: same member set in both layouts
+    const int32_t Cs = ls.n_clusters(), Cd = ld.n_clusters();
+    std::vector<int32_t> twin_s(Cs, -1), twin_d(Cd, -1);
+    for (int32_t c = 0; c < Cs; ++c) {
+        const int32_t cd = ld.cluster[ls.members[c][0]];
+        if (same_members(ls, c, ld, cd)) { twin_s[c] = cd; twin_d[cd] = c; }
+    }
+    auto transposed_s = [&](int32_t c) { return twin_s[c] < 0 && ls.stride[c] > u; };
+    auto transposed_d = [&](int32_t c) { return twin_d[c] < 0 && ld.stride[c] > u; };
+
+    // slot size: the largest power of two in [256, 4096] dividing every region base whose
+    // transposed tiles fit the shared-memory budget
+    uint32_t S = 0;
+    for (uint32_t cand = 4096; cand >= 256; cand >>= 1) {
+        bool ok = true;
+        for (uint64_t b : p->bs) ok = ok && (b % cand == 0);
+        for (uint64_t b : p->bd) ok = ok && (b % cand == 0);
+        const uint32_t T = cand / u;
+        for (int32_t c = 0; ok && c < Cs; ++c)
+            if (transposed_s(c) && smem_need(T, (uint32_t)(ls.stride[c] / u), u) > IP_MAX_PIECE) ok = false;
+        for (int32_t c = 0; ok && c < Cd; ++c)
+            if (transposed_d(c) && smem_need(T, (uint32_t)(ld.stride[c] / u), u) > IP_MAX_PIECE) ok = false;
+        if (ok) { S = cand; break; }
+    }
+    if (!S) return fail(ADHA_ERR_UNSUPPORTED, "in-place remap: a cluster record is too wide for a " +
+                                                  std::to_string(256 / u) + "-record tile in shared memory");
+    // (region bases are 256-aligned by construction, so only the tile budget can fail)
+    p->S = S;
+    p->T = S / u;
+    const uint32_t T = p->T;
+    p->m = n / T;
+    p->tail = n - p->m * (int64_t)T;
+    const uint64_t m = (uint64_t)p->m;
+
+    p->pre.clear();
+    p->post.clear();
+    p->max_piece = 0;
+    if (m > 0) {
+        for (int32_t c = 0; c < Cs; ++c)
+            if (transposed_s(c)) {
+                p->pre.push_back({p->bs[c], (uint32_t)(ls.stride[c] / u), (uint32_t)ls.stride[c]});
+                p->max_piece = std::max<uint32_t>(p->max_piece, (uint32_t)smem_need(T, (uint32_t)(ls.stride[c] / u), u));
+            }
+        for (int32_t c = 0; c < Cd; ++c)
+            if (transposed_d(c)) {
+                p->post.push_back({p->bd[c], (uint32_t)(ld.stride[c] / u), (uint32_t)ld.stride[c]});
+                p->max_piece = std::max<uint32_t>(p->max_piece, (uint32_t)smem_need(T, (uint32_t)(ld.stride[c] / u), u));
+            }
+    }
+
+    // ---- the slot permutation over U = (src body slots) u (dst body slots)
+    const uint64_t total = std::max(p->bytes_s, p->bytes_d);
+    const uint64_t nslot = (total + S - 1) / S;
+    if (nslot >= 0xFFFFFFFFull) return fail(ADHA_ERR_TOO_LARGE, "in-place remap: more than 2^32 slots");
+    constexpr uint32_t NONE = 0xFFFFFFFFu;
+    std::vector<uint32_t> P;
+    std::vector<uint8_t> in_d;
+    p->seq.clear();
+    p->segs.clear();
+    p->content_slots = p->moved_slots = p->fixed_slots = p->junk_slots = p->cycles = 0;
+    if (m > 0) {
+        P.assign(nslot, NONE);
+        in_d.assign(nslot, 0);
+        for (int32_t c = 0; c < Cs; ++c) {
+            const uint32_t K = (uint32_t)(ls.stride[c] / u);
+            const uint64_t s0 = p->bs[c] / S;
+            if (twin_s[c] >= 0) {                         // raw slots of an unchanged cluster
+                const uint64_t d0 = p->bd[twin_s[c]] / S;
+                for (uint64_t t = 0; t < m; ++t)
+                    for (uint32_t k = 0; k < K; ++k) P[s0 + t * K + k] = (uint32_t)(d0 + t * K + k);
+                continue;
+            }
+            // unit-column k of the (transposed) tile: field f, unit q of it
+            for (uint32_t k = 0; k < K; ++k) {
+                const int32_t f = field_at(ls, c, k * u);
+                const uint32_t q = (k * u - ls.offset[f]) / u;
+                const int32_t cd = ld.cluster[f];
+                const uint32_t Kd = (uint32_t)(ld.stride[cd] / u);
+                const uint64_t d0 = p->bd[cd] / S + ld.offset[f] / u + q;
+                for (uint64_t t = 0; t < m; ++t) P[s0 + t * K + k] = (uint32_t)(d0 + t * Kd);
+            }
+        }
+        std::vector<uint32_t> free_in, free_out;   // dst-only slots, src-only slots
+        for (uint64_t x = 0; x < nslot; ++x)
+            if (P[x] != NONE) { in_d[P[x]] = 1; ++p->content_slots; }
+        for (uint64_t x = 0; x < nslot; ++x) {
+            const bool ins = P[x] != NONE;
+            if (in_d[x] && !ins) free_in.push_back((uint32_t)x);
+            if (ins && !in_d[x]) free_out.push_back((uint32_t)x);
+        }
+        if (free_in.size() != free_out.size()) return fail(ADHA_ERR_UNSUPPORTED, "in-place plan: slot count mismatch");
+        // a dst slot whose old bytes are not content (src tail, gap) receives content; its junk goes
+        // to a src-only slot (which becomes dst tail / gap): the permutation closes on U
+        for (size_t i = 0; i < free_in.size(); ++i) P[free_in[i]] = free_out[i];
+        p->junk_slots = free_in.size();
+        // cycles, split into segments of at most IP_SEG positions
+        for (uint64_t x0 = 0; x0 < nslot; ++x0) {
+            if (P[x0] == NONE) continue;
+            if (P[x0] == (uint32_t)x0) { P[x0] = NONE; ++p->fixed_slots; continue; }
+            const uint32_t start = (uint32_t)p->seq.size();
+            uint64_t y = x0;
+            do {
+                p->seq.push_back((uint32_t)y);
+                const uint32_t ny = P[y];
+                P[y] = NONE;
+                y = ny;
+            } while (y != x0);
+            const uint32_t L = (uint32_t)p->seq.size() - start;
+            const uint32_t first = (uint32_t)p->segs.size();
+            const uint32_t ns = (L + IP_SEG - 1) / IP_SEG;
+            for (uint32_t s = 0; s < ns; ++s) {
+                const uint32_t a = start + s * IP_SEG;
+                const uint32_t len = std::min<uint32_t>(IP_SEG, start + L - a);
+                p->segs.push_back({a, len, s == 0 ? first + ns - 1 : first + s - 1, 0});
+            }
+            ++p->cycles;
+        }
+        p->moved_slots = p->seq.size();
+        if (p->seq.size() >= 0xFFFFFFFFull) return fail(ADHA_ERR_TOO_LARGE, "in-place remap: too many slots");
+    }
+
+    // ---- tail records [m*T, n): saved packed (declaration order), restored at the end
+    p->tail_fields.clear();
+    if (p->tail > 0) {
+        uint32_t toff = 0;
+        for (int32_t f = 0; f < ls.n_fields; ++f) {
+            const int32_t cs = ls.cluster[f], cd = ld.cluster[f];
+            p->tail_fields.push_back({p->bs[cs] + ls.offset[f], p->bd[cd] + ld.offset[f], (uint32_t)ls.stride[cs],
+                                      (uint32_t)ld.stride[cd], ls.width[f], toff});
+            toff += ls.width[f];
+        }
+    }
+
+    // ---- workspace layout
+    uint64_t o = 0;
+    auto take = [&](uint64_t bytes) { const uint64_t at = o; o = align256(o + bytes); return at; };
+    p->ws_pieces = take((p->pre.size() + p->post.size()) * sizeof(IpPiece));
+    p->ws_tailf = take(p->tail_fields.size() * sizeof(IpTailField));
+    p->ws_seq = take(p->seq.size() * sizeof(uint32_t));
+    p->ws_segs = take(p->segs.size() * sizeof(IpSeg));
+    p->ws_save = take(p->segs.size() * (uint64_t)S);
+    p->ws_tail = take((uint64_t)p->tail * ls.record_bytes);
+    p->ws_bytes = std::max<uint64_t>(o, 256);
+    p->uploaded = nullptr;
+    p->uploaded_device = -1;
+    return ADHA_OK;
+}
+
+std::string inplace_plan_json(const InplacePlan& p) {
+    auto u64 = [](uint64_t v) { return std::to_string(v); };
+    std::string s = "{";
+    s += "\"n_records\":" + std::to_string(p.n);
+    s += ",\"unit\":" + u64(p.u) + ",\"slot_bytes\":" + u64(p.S) + ",\"T\":" + u64(p.T);
+    s += ",\"body_tiles\":" + std::to_string(p.m) + ",\"tail_records\":" + std::to_string(p.tail);
+    s += ",\"src_bytes\":" + u64(p.bytes_s) + ",\"dst_bytes\":" + u64(p.bytes_d);
+    s += ",\"buffer_bytes\":" + u64(std::max(p.bytes_s, p.bytes_d));
+    s += ",\"pre_clusters\":" + u64(p.pre.size()) + ",\"post_clusters\":" + u64(p.post.size());
+    s += ",\"max_tile_smem\":" + u64(p.max_piece);
+    s += ",\"content_slots\":" + u64(p.content_slots) + ",\"moved_slots\":" + u64(p.moved_slots);
+    s += ",\"fixed_slots\":" + u64(p.fixed_slots) + ",\"junk_slots\":" + u64(p.junk_slots);
+    s += ",\"cycles\":" + u64(p.cycles) + ",\"segments\":" + u64(p.segs.size());
+    uint64_t pre_b = 0, post_b = 0;
+    for (const auto& x : p.pre) pre_b += (uint64_t)p.m * p.T * x.stride;
+    for (const auto& x : p.post) post_b += (uint64_t)p.m * p.T * x.stride;
+    // device traffic of one run: read + write of every transposed tile and moved slot
+    s += ",\"traffic_bytes\":" + u64(2 * (pre_b + post_b + (p.moved_slots + p.segs.size()) * p.S +
+                                          2 * (uint64_t)p.tail * p.ls.record_bytes));
+    s += ",\"workspace_bytes\":" + u64(p.ws_bytes);
+    s += "}";
+    return s;
+}
+
+}  // namespace adha
+
+using namespace adha;
+
+extern "C" adha_status adha_inplace_plan_create(const adha_layout* hs, const adha_layout* hd, int64_t n,
+                                                adha_inplace_plan** out) {
+    clear_error();
+    if (!hs || !hd || !out) return fail(ADHA_ERR_INVALID_ARG, "null argument");
+    *out = nullptr;
+    adha_inplace_plan* h = nullptr;
+    try {
+        h = new adha_inplace_plan();
+        adha_status st = inplace_plan_build(hs->L, hd->L, n, &h->P);
+        if (st != ADHA_OK) { delete h; return st; }
+    } catch (const std::bad_alloc&) {
+        delete h;
+        return fail(ADHA_ERR_OOM, "in-place plan: host allocation failed");
+    }
+    *out = h;
+    return ADHA_OK;
+}
+
+extern "C" adha_status adha_inplace_plan_info(const adha_inplace_plan* h, uint64_t* buffer_bytes,
+                                              uint64_t* workspace_bytes) {
+    clear_error();
+    if (!h) return fail(ADHA_ERR_INVALID_ARG, "null plan");
+    if (buffer_bytes) *buffer_bytes = std::max(h->P.bytes_s, h->P.bytes_d);
+    if (workspace_bytes) *workspace_bytes = h->P.ws_bytes;
+    return ADHA_OK;
+}
+
+extern "C" adha_status adha_inplace_plan_describe(const adha_inplace_plan* h, char** json_out) {
+    clear_error();
+    if (!h || !json_out) return fail(ADHA_ERR_INVALID_ARG, "null argument");
+    const std::string s = inplace_plan_json(h->P);
+    char* c = (char*)std::malloc(s.size() + 1);
+    if (!c) return fail(ADHA_ERR_OOM, "out of memory");
+    std::memcpy(c, s.c_str(), s.size() + 1);
+    *json_out = c;
+    return ADHA_OK;
+}
+
+extern "C" void adha_inplace_plan_destroy(adha_inplace_plan* h) { delete h; }

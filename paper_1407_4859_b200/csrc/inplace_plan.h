@@ -1,0 +1,79 @@
+// inplace_plan.h -- host plan of the in-place remap (the "in-place" half;
+// adha.h adha_inplace_plan_create).  Not part of the ABI.
+//
+// The buffer is cut into slots of S bytes (S a power of two in [256, 4096] dividing every
+// region base of both layouts).  A tile of T = S / u records (u = the largest power of two
+// <= 16 dividing every field width) of a cluster with stride s occupies K = s / u slots:
+//   step 1  (tile-local) each src tile of a changed cluster is transposed in place from
+//           record-major to unit-column-major: slot k of the tile then holds byte-unit k of
+//           the cluster record for the tile's T records;
+//   step 2  (slot permutation) every slot moves to the slot its unit-column occupies in the
+//           dst layout, by following the permutation's cycles (split into segments so that
+//           the warps work in parallel; the last slot of each segment is saved first);
+//   step 3  (tile-local) each dst tile of a changed cluster is transposed back to record-major.
+// Clusters whose member set is the same in both layouts are moved as raw slots (no transpose),
+// and not at all when their region base is the same (fixed points).  The last N mod T records
+// (the tail) are saved to the workspace first and written to their dst positions last.
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+#include "internal.h"
+
+namespace adha {
+
+struct IpPiece {        // one cluster region transposed tile by tile (steps 1 and 3)
+    uint64_t base;      // region base (bytes from the buffer start)
+    uint32_t K;         // byte-units per record (stride / u)
+    uint32_t stride;    // cluster record bytes
+};
+
+struct IpTailField {    // one field of the tail records: src/dst element address terms
+    uint64_t src;       // base_s(c) + offset_s(f)
+    uint64_t dst;       // base_d(c') + offset_d(f)
+    uint32_t stride_s, stride_d, width, toff;   // toff: byte offset in a packed tail record
+};
+
+struct IpSeg {          // a run of consecutive positions of one cycle
+    uint32_t start;     // first index into seq
+    uint32_t len;       // positions (>= 1)
+    uint32_t pred;      // segment holding the position just before `start` on the cycle
+    uint32_t pad;
+};
+
+struct InplacePlan {
+    Layout ls, ld;
+    int64_t n = 0;
+    uint32_t u = 0, S = 0, T = 0;
+    int64_t m = 0;                       // body tiles (T records each)
+    int64_t tail = 0;                    // n - m * T
+    uint64_t bytes_s = 0, bytes_d = 0;   // bytes(Ls, n), bytes(Ld, n)
+    std::vector<uint64_t> bs, bd;
+    std::vector<IpPiece> pre, post;      // step 1 (src clusters), step 3 (dst clusters)
+    uint32_t max_piece = 0;              // bytes of the largest transposed tile
+    std::vector<uint32_t> seq;           // slot indices, cycles in order (slot j -> next on its cycle)
+    std::vector<IpSeg> segs;
+    std::vector<IpTailField> tail_fields;
+    // statistics
+    uint64_t content_slots = 0, moved_slots = 0, fixed_slots = 0, junk_slots = 0, cycles = 0;
+    // workspace layout (byte offsets, each 256-aligned) and total size
+    uint64_t ws_pieces = 0, ws_tailf = 0, ws_seq = 0, ws_segs = 0, ws_save = 0, ws_tail = 0, ws_bytes = 0;
+    // upload state (adha_inplace_plan_upload)
+    const void* uploaded = nullptr;
+    int uploaded_device = -1;
+};
+
+// Segment length: positions per segment (a warp group walks one segment).
+constexpr uint32_t IP_SEG = 64;
+// Largest transposed tile (shared memory of one CTA, with row padding).
+constexpr uint32_t IP_MAX_PIECE = 160u * 1024u;
+
+adha_status inplace_plan_build(const Layout& ls, const Layout& ld, int64_t n, InplacePlan* p);
+std::string inplace_plan_json(const InplacePlan& p);
+
+}  // namespace adha
+
+struct adha_inplace_plan {
+    adha::InplacePlan P;
+};

@@ -537,3 +537,66 @@ def test_status_strings_and_version():
     assert A._lib.adha_status_string(999) is not None and A._lib.adha_status_string(-1) is not None
     v = A.version()
     assert v >= 100 and 0 <= v % 100 < 100
+
+
+# ----------------------------------------------------------------------------- in-place plan (host only)
+
+def _ip(widths, ls, ld, n):
+    return A.InplacePlan(A.Layout(widths, ls), A.Layout(widths, ld), n)
+
+
+def test_inplace_plan_counts_and_sizes():
+    """Host plan of adha_remap_inplace: the buffer needs max(bytes(Ls), bytes(Ld)) (not the sum);
+    every body slot of the src layout is content; the permutation closes on src u dst slots
+    (moved + fixed = content + junk); the slot size divides every region base of both layouts."""
+    widths = [8 if i % 4 == 3 else 4 for i in range(16)]
+    rng = random.Random(5)
+    for n in (0, 1, 63, 64, 65, 1000, 10_000_000, 12345):
+        for ls, ld in [([0] * 16, list(range(16))), (list(range(16)), [0] * 16),
+                       ([rng.randrange(5) for _ in range(16)], [rng.randrange(7) for _ in range(16)])]:
+            p = _ip(widths, ls, ld, n)
+            d = p.describe()
+            bs = O.layout_bytes(widths, ls, n)
+            bd = O.layout_bytes(widths, ld, n)
+            assert p.buffer_bytes == max(bs, bd) == d["buffer_bytes"]
+            S, T, u = d["slot_bytes"], d["T"], d["unit"]
+            assert u == 4 and S == T * u and S in (256, 512, 1024, 2048, 4096)
+            assert d["body_tiles"] == n // T and d["tail_records"] == n % T
+            assert d["content_slots"] == (n // T) * 80 // u
+            assert d["moved_slots"] + d["fixed_slots"] == d["content_slots"] + d["junk_slots"]
+            for lab in (ls, ld):
+                base, _, _, _ = O.field_addresses(widths, lab, n)
+                assert all(int(b) % S == 0 for b in base)
+            assert p.workspace_bytes >= d["segments"] * S
+
+
+def test_inplace_plan_identity_and_moved_subset():
+    widths = [4] * 9
+    aosv, soa = [0, 0, 0, 1, 2, 3, 4, 5, 6], list(range(9))
+    d = _ip(widths, aosv, aosv, 1 << 16).describe()
+    assert d["moved_slots"] == 0 and d["pre_clusters"] == 0 and d["post_clusters"] == 0
+    d = _ip(widths, aosv, soa, 1 << 20).describe()     # PAPER.md:113 AoSV -> SoA: only V1..V3 move
+    S = d["slot_bytes"]
+    # V1..V3's slots move (a couple are fixed points, e.g. V1 of tile 0); the six singletons don't
+    assert 0 < d["moved_slots"] <= 3 * 4 * (1 << 20) // S
+    assert d["moved_slots"] + d["fixed_slots"] == 9 * 4 * (1 << 20) // S
+
+
+def test_inplace_plan_errors():
+    w = [4, 4, 8]
+    with pytest.raises(A.AdhaError) as e:
+        _ip(w, [0, 0, 0], [0, 1, 2], -1)
+    assert e.value.name == "ADHA_ERR_INVALID_ARG"
+    with pytest.raises(A.AdhaError) as e:
+        A.InplacePlan(A.Layout(w, [0, 0, 0]), A.Layout([4, 4, 4], [0, 1, 2]), 10)
+    assert e.value.name == "ADHA_ERR_LAYOUT_MISMATCH"
+    with pytest.raises(A.AdhaError) as e:
+        A.InplacePlan(A.Layout(w, [0, 0, 0], aligned=True), A.Layout(w, [0, 1, 2]), 10)
+    assert e.value.name == "ADHA_ERR_UNSUPPORTED"
+    with pytest.raises(A.AdhaError) as e:
+        A.InplacePlan(A.Layout(w, [0, 0, 0], blocks=[8, 8, 8]), A.Layout(w, [0, 1, 2]), 10)
+    assert e.value.name == "ADHA_ERR_UNSUPPORTED"
+    # a record too wide for a 256 / u record tile in shared memory
+    with pytest.raises(A.AdhaError) as e:
+        _ip([1] * 1000, [0] * 1000, list(range(1000)), 10)
+    assert e.value.name == "ADHA_ERR_UNSUPPORTED"
