@@ -4,10 +4,10 @@
 //
 // Plan (inplace_plan.cpp): S-byte slots, T = S / u records per tile.  Launches, in order:
 //   ip_tail_kernel (save)         the last N mod T records -> workspace, packed
-//   ip_transpose_kernel (step 1)  src tiles of changed clusters: record-major -> unit-columns
+//   ip_tile_kernel (step 1)       src tiles of changed multi-field clusters: record-major -> field-blocked
 //   ip_cycle_save_kernel          the last slot of every cycle segment -> workspace
 //   ip_cycle_shift_kernel         every slot moves one step along its cycle
-//   ip_transpose_kernel (step 3)  dst tiles of changed clusters: unit-columns -> record-major
+//   ip_tile_kernel (step 3)       dst tiles of changed multi-field clusters: field-blocked -> record-major
 //   ip_tail_kernel (restore)      the tail records -> their dst addresses
 // Type-blind byte moves throughout (reading Q6): no floating-point instruction.
 #include <cuda_runtime.h>
@@ -42,73 +42,183 @@ __global__ void ip_tail_kernel(uint8_t* __restrict__ buf, const IpTailField* __r
     }
 }
 
-// ---------------------------------------------------------------------------- tile transpose
-// A tile of cluster c: T records x K byte-units of u bytes, T * K * u bytes at
-// base + t * T * stride.  to_cols: record-major (r, k) -> unit-column-major (k, r); else back.
-// Staged in shared memory with one padding word per line so that the gather is (nearly)
-// bank-conflict free; written back with coalesced 32-bit stores.  Atom = the element moved:
-// 32-bit words when u % 4 == 0, bytes otherwise.
+// ---------------------------------------------------------------------------- tile rewrite
+// q = floor(n / d) for n * d < 2^32 with magic = ceil(2^32 / d) (0 encodes d == 1).
+__device__ __forceinline__ uint32_t fdiv(uint32_t n, uint32_t magic) { return magic ? __umulhi(n, magic) : n; }
+
+// One tile of cluster c (T records, RA atoms per record, T * stride bytes at base + t*T*stride)
+// is rewritten in place between record-major form (atom (r, j) at r * RA + j) and field-blocked
+// form (field f's T * a_f atoms contiguous from T * col_f, record r's atoms at r * a_f).
+// to_blocks: record-major -> field-blocked (step 1); else field-blocked -> record-major (step 3).
+// The tile is staged in shared memory with padding (one atom per record row, or per field
+// block) so that the gather along the other major is (nearly) bank-conflict free, then written
+// back with coalesced 16-byte stores.  Atom = 32-bit word when u % 4 == 0, else one byte.
+// Loads are issued IP_LB vectors per thread at a time, and the first batch of the CTA's next
+// tile is loaded into registers before the gather of the current one, so global loads overlap
+// the shared-memory work.  Shared memory: [column table: tab_cap bytes][padded tile].
+#ifndef IP_LB
+#define IP_LB 2
+#endif
+
 template <typename Atom>
-__global__ void __launch_bounds__(256) ip_transpose_kernel(uint8_t* __restrict__ buf, const IpPiece* __restrict__ cl,
-                                                           uint32_t ncl, uint64_t m, uint32_t T, uint32_t u,
-                                                           int to_cols) {
-    extern __shared__ __align__(16) uint8_t sm[];
-    Atom* sa = reinterpret_cast<Atom*>(sm);
-    constexpr uint32_t PER_WORD = 4 / sizeof(Atom);
-    const uint32_t A = u / sizeof(Atom);                 // atoms per unit
-    const uint32_t lgT = 31 - __clz(T);
-    const uint64_t total = (uint64_t)ncl * m;
-    for (uint64_t p = blockIdx.x; p < total; p += gridDim.x) {
-        const uint32_t c = (uint32_t)(p / m);
-        const uint64_t t = p - (uint64_t)c * m;
-        const IpPiece pc = cl[c];
-        const uint32_t K = pc.K;
-        const uint32_t RA = K * A, CA = T * A;           // atoms per record row / per unit column
-        const uint32_t lineA = to_cols ? RA : CA;
-        const uint32_t pitch = lineA + (sizeof(Atom) == 4 ? ((lineA & 1) ? 0 : 1) : 4);
-        uint8_t* g = buf + pc.base + t * (uint64_t)T * pc.stride;
-        const uint32_t bytes = T * pc.stride;
-        // load: 16-byte vectors, scattered into padded lines
-        const uint4* g4 = reinterpret_cast<const uint4*>(g);
-        for (uint32_t v = threadIdx.x; v < bytes / 16; v += blockDim.x) {
-            const uint4 x = g4[v];
-            const uint32_t w4[4] = {x.x, x.y, x.z, x.w};
-            const uint32_t a0 = v * (16 / sizeof(Atom));
+__device__ __forceinline__ void ip_scatter(Atom* sa, const uint4 x, uint32_t v, int to_blocks, uint32_t lgT,
+                                           uint32_t RA, uint32_t magic_RA, uint32_t padR, const IpCol* tab) {
+    constexpr uint32_t APV = 16 / sizeof(Atom);
+    const uint32_t w4[4] = {x.x, x.y, x.z, x.w};
+    const uint32_t i0 = v * APV;
+    if (to_blocks) {   // record-major input: pad per row (row r starts at r * (RA + padR))
+        if (sizeof(Atom) == 4) {
 #pragma unroll
-            for (uint32_t j = 0; j < 16 / sizeof(Atom); ++j) {
-                const uint32_t a = a0 + j;
-                const uint32_t line = a / lineA, col = a - line * lineA;
-                Atom val;
-                if (sizeof(Atom) == 4) val = (Atom)w4[j];
-                else val = (Atom)(w4[j / 4] >> (8 * (j % 4)));
-                sa[line * pitch + col] = val;
+            for (uint32_t j = 0; j < 4; ++j) sa[i0 + j + fdiv(i0 + j, magic_RA) * padR] = (Atom)w4[j];
+        } else {
+            const uint32_t r0 = fdiv(i0, magic_RA);
+            uint32_t o = i0 + r0 * padR, rr = i0 - r0 * RA;
+#pragma unroll
+            for (uint32_t j = 0; j < 16; ++j) {
+                sa[o] = (Atom)(w4[j >> 2] >> (8 * (j & 3)));
+                ++o;
+                if (++rr == RA) { rr = 0; o += padR; }
+            }
+        }
+    } else {           // field-blocked input: pad per field block (a vector never straddles one)
+        const uint32_t o = i0 + reinterpret_cast<const uint32_t*>(tab)[RA + (i0 >> lgT)];
+        if (sizeof(Atom) == 4) {
+#pragma unroll
+            for (uint32_t j = 0; j < 4; ++j) sa[o + j] = (Atom)w4[j];
+        } else {
+#pragma unroll
+            for (uint32_t j = 0; j < 16; ++j) sa[o + j] = (Atom)(w4[j >> 2] >> (8 * (j & 3)));
+        }
+    }
+}
+
+template <typename Atom>
+__device__ __forceinline__ uint4 ip_gather(const Atom* sa, uint32_t v, int to_blocks, uint32_t lgT, uint32_t RA,
+                                           uint32_t magic_RA, uint32_t P, const IpCol* tab) {
+    constexpr uint32_t APV = 16 / sizeof(Atom);
+    uint32_t w4[4] = {0, 0, 0, 0};
+    const uint32_t o0 = v * APV;
+    if (to_blocks) {   // output field-blocked: the vector lies in one column block
+        const IpCol e = tab[o0 >> lgT];
+        const uint32_t col = e.col_fp & 0xFFFFu;
+        const uint32_t local0 = o0 - (col << lgT);
+        if (sizeof(Atom) == 4 && e.a == 1) {          // 4 consecutive records of one column
+            const uint32_t a0 = local0 * P + col;
+#pragma unroll
+            for (uint32_t j = 0; j < 4; ++j) w4[j] = (uint32_t)sa[a0 + j * P];
+        } else if (sizeof(Atom) == 4 && e.a == 2) {   // 2 records x 2 atoms
+            const uint32_t a0 = (local0 >> 1) * P + col;
+            w4[0] = (uint32_t)sa[a0];
+            w4[1] = (uint32_t)sa[a0 + 1];
+            w4[2] = (uint32_t)sa[a0 + P];
+            w4[3] = (uint32_t)sa[a0 + P + 1];
+        } else {
+#pragma unroll
+            for (uint32_t j = 0; j < APV; ++j) {
+                const uint32_t local = local0 + j;
+                const uint32_t r = fdiv(local, e.magic_a);
+                const Atom val = sa[r * P + col + (local - r * e.a)];
+                if (sizeof(Atom) == 4) w4[j] = (uint32_t)val;
+                else w4[j >> 2] |= (uint32_t)val << (8 * (j & 3));
+            }
+        }
+    } else {           // output record-major: atom (r, jc) <- field-blocked bo(jc) + r * a(jc)
+        const uint32_t* bo_a = reinterpret_cast<const uint32_t*>(tab);   // packed bo | a << 17 (see ip_tile_kernel)
+        uint32_t r = fdiv(o0, magic_RA);
+        uint32_t jc = o0 - r * RA;
+#pragma unroll
+        for (uint32_t j = 0; j < APV; ++j) {
+            const uint32_t e = bo_a[jc];
+            const Atom val = sa[(e & 0x1FFFFu) + r * (e >> 17)];
+            if (sizeof(Atom) == 4) w4[j] = (uint32_t)val;
+            else w4[j >> 2] |= (uint32_t)val << (8 * (j & 3));
+            if (++jc == RA) { jc = 0; ++r; }
+        }
+    }
+    return make_uint4(w4[0], w4[1], w4[2], w4[3]);
+}
+
+template <typename Atom, int to_blocks>
+__global__ void __launch_bounds__(256) ip_tile_kernel(uint8_t* __restrict__ buf, const IpPiece* __restrict__ cl,
+                                                      const IpCol* __restrict__ cols, uint32_t ncl, uint64_t m,
+                                                      uint32_t T, uint32_t tab_cap) {
+    extern __shared__ __align__(16) uint8_t sm[];
+    IpCol* tab = reinterpret_cast<IpCol*>(sm);
+    Atom* sa = reinterpret_cast<Atom*>(sm + tab_cap);
+    const uint32_t lgT = 31 - __clz(T);
+    const uint32_t tid = threadIdx.x, nt = blockDim.x;
+    uint4 x[IP_LB];
+    uint32_t cur_c = 0xFFFFFFFFu;
+    // tiles are visited cluster-major: tile p = (c, t) with p = c * m + t, stepping by gridDim.x
+    uint32_t c = (uint32_t)(blockIdx.x / m);
+    uint64_t t = blockIdx.x - (uint64_t)c * m;
+    const uint64_t step_c = gridDim.x / m, step_t = gridDim.x - step_c * m;
+    auto advance = [&](uint32_t& cc, uint64_t& tt) {
+        cc += (uint32_t)step_c;
+        tt += step_t;
+        if (tt >= m) { tt -= m; ++cc; }
+    };
+    if (c < ncl) {   // batch 0 of the first tile
+        const IpPiece pc = cl[c];
+        const uint4* g4 = reinterpret_cast<const uint4*>(buf + pc.base + t * (uint64_t)T * pc.stride);
+        const uint32_t nvec = (T * pc.stride) >> 4;
+#pragma unroll
+        for (uint32_t k = 0; k < IP_LB; ++k)
+            if (tid + k * nt < nvec) x[k] = g4[tid + k * nt];
+    }
+    for (; c < ncl; advance(c, t)) {
+        const IpPiece pc = cl[c];
+        uint8_t* g = buf + pc.base + t * (uint64_t)T * pc.stride;
+        if (c != cur_c) {   // this cluster's column table -> shared memory
+            if (to_blocks) {
+                for (uint32_t j = tid; j < pc.RA; j += nt) tab[j] = cols[pc.col_off + j];
+            } else {        // field-blocked -> record-major needs only bo and a: one packed word per column
+                uint32_t* bo_a = reinterpret_cast<uint32_t*>(tab);   // [RA] bo | a << 17, then [RA] padding
+                for (uint32_t j = tid; j < pc.RA; j += nt) {
+                    const IpCol e = cols[pc.col_off + j];
+                    bo_a[j] = e.bo | (e.a << 17);
+                    bo_a[pc.RA + j] = e.col_fp >> 16;
+                }
+            }
+            cur_c = c;
+            __syncthreads();
+        }
+        const uint32_t RA = pc.RA;
+        const uint32_t padR = sizeof(Atom) == 4 ? ((RA & 1) ? 0 : 1) : 4;   // row padding (odd word pitch)
+        const uint32_t P = RA + padR;
+        const uint32_t nvec = (T * pc.stride) >> 4;
+        const uint4* g4 = reinterpret_cast<const uint4*>(g);
+        // ---- load: batch 0 is already in registers; further batches are loaded here
+        for (uint32_t b0 = 0; b0 < nvec; b0 += IP_LB * nt) {
+            if (b0) {
+#pragma unroll
+                for (uint32_t k = 0; k < IP_LB; ++k)
+                    if (b0 + tid + k * nt < nvec) x[k] = g4[b0 + tid + k * nt];
+            }
+#pragma unroll
+            for (uint32_t k = 0; k < IP_LB; ++k) {
+                const uint32_t v = b0 + tid + k * nt;
+                if (v < nvec) ip_scatter<Atom>(sa, x[k], v, to_blocks, lgT, RA, pc.magic_RA, padR, tab);
             }
         }
         __syncthreads();
-        // store: output word w = atoms 4w/size .. ; output order is the other major
-        uint32_t* g32 = reinterpret_cast<uint32_t*>(g);
-        for (uint32_t w = threadIdx.x; w < bytes / 4; w += blockDim.x) {
-            uint32_t out = 0;
+        // ---- prefetch batch 0 of this CTA's next tile (no other CTA writes it)
+        {
+            uint32_t cn = c;
+            uint64_t tn = t;
+            advance(cn, tn);
+            if (cn < ncl) {
+                const IpPiece pcn = cl[cn];
+                const uint4* gn = reinterpret_cast<const uint4*>(buf + pcn.base + tn * (uint64_t)T * pcn.stride);
+                const uint32_t nvn = (T * pcn.stride) >> 4;
 #pragma unroll
-            for (uint32_t j = 0; j < PER_WORD; ++j) {
-                const uint32_t o = w * PER_WORD + j;
-                const uint32_t a = o % A, ku = o / A;    // ku: unit index in output order
-                uint32_t line, col;
-                if (to_cols) {   // output (k, r): ku = k * T + r; input row r, column k*A + a
-                    const uint32_t k = ku >> lgT, r = ku & (T - 1);
-                    line = r;
-                    col = k * A + a;
-                } else {         // output (r, k): ku = r * K + k; input column k, row r*A + a
-                    const uint32_t r = ku / K, k = ku - r * K;
-                    line = k;
-                    col = r * A + a;
-                }
-                const Atom val = sa[line * pitch + col];
-                if (sizeof(Atom) == 4) out = (uint32_t)val;
-                else out |= (uint32_t)val << (8 * j);
+                for (uint32_t k = 0; k < IP_LB; ++k)
+                    if (tid + k * nt < nvn) x[k] = gn[tid + k * nt];
             }
-            g32[w] = out;
         }
+        // ---- gather in output order -> 16-byte stores
+        uint4* o4 = reinterpret_cast<uint4*>(g);
+        for (uint32_t v = tid; v < nvec; v += nt) o4[v] = ip_gather<Atom>(sa, v, to_blocks, lgT, RA, pc.magic_RA, P, tab);
         __syncthreads();
     }
 }
@@ -211,14 +321,18 @@ adha_status smem_optin(int dev, const void* fn) {
     return ADHA_OK;
 }
 
-adha_status launch_transpose(const InplacePlan& P, uint8_t* buf, const uint8_t* ws, bool post, int dev, int sms,
+adha_status launch_tiles(const InplacePlan& P, uint8_t* buf, const uint8_t* ws, bool post, int dev, int sms,
                              cudaStream_t st) {
     const auto& v = post ? P.post : P.pre;
     if (v.empty() || P.m == 0) return ADHA_OK;
     const IpPiece* tab = reinterpret_cast<const IpPiece*>(ws + P.ws_pieces) + (post ? P.pre.size() : 0);
-    const uint32_t smem = (P.max_piece + 15) & ~15u;
-    const void* fn = P.u % 4 == 0 ? (const void*)ipdev::ip_transpose_kernel<uint32_t>
-                                  : (const void*)ipdev::ip_transpose_kernel<uint8_t>;
+    const IpCol* cols = reinterpret_cast<const IpCol*>(ws + P.ws_cols);
+    const uint32_t tab_cap = (P.max_tab + 15) & ~15u;
+    const uint32_t smem = tab_cap + P.max_tile;
+    const void* fn = P.u % 4 == 0 ? (post ? (const void*)ipdev::ip_tile_kernel<uint32_t, 0>
+                                          : (const void*)ipdev::ip_tile_kernel<uint32_t, 1>)
+                                  : (post ? (const void*)ipdev::ip_tile_kernel<uint8_t, 0>
+                                          : (const void*)ipdev::ip_tile_kernel<uint8_t, 1>);
     adha_status s = smem_optin(dev, fn);
     if (s != ADHA_OK) return s;
     int occ = 0;
@@ -226,14 +340,11 @@ adha_status launch_transpose(const InplacePlan& P, uint8_t* buf, const uint8_t* 
     if (e != cudaSuccess) return cuda_err(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
     const uint64_t pieces = (uint64_t)v.size() * (uint64_t)P.m;
     const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(pieces, (uint64_t)sms * std::max(occ, 1)));
-    if (P.u % 4 == 0)
-        ipdev::ip_transpose_kernel<uint32_t><<<grid, 256, smem, st>>>(buf, tab, (uint32_t)v.size(), (uint64_t)P.m,
-                                                                     P.T, P.u, post ? 0 : 1);
-    else
-        ipdev::ip_transpose_kernel<uint8_t><<<grid, 256, smem, st>>>(buf, tab, (uint32_t)v.size(), (uint64_t)P.m,
-                                                                    P.T, P.u, post ? 0 : 1);
-    e = cudaGetLastError();
-    return e == cudaSuccess ? ADHA_OK : cuda_err(e, "ip_transpose_kernel launch");
+    uint32_t ncl = (uint32_t)v.size(), T = P.T;
+    uint64_t m = (uint64_t)P.m;
+    void* args[] = {&buf, (void*)&tab, (void*)&cols, &ncl, &m, &T, (void*)&tab_cap};
+    e = cudaLaunchKernel(fn, dim3(grid), dim3(256), args, smem, st);
+    return e == cudaSuccess ? ADHA_OK : cuda_err(e, "ip_tile_kernel launch");
 }
 
 adha_status launch_tail(const InplacePlan& P, uint8_t* buf, uint8_t* ws, bool restore, cudaStream_t st) {
@@ -272,6 +383,7 @@ extern "C" adha_status adha_inplace_plan_upload(adha_inplace_plan* h, void* work
     pieces.insert(pieces.end(), P.post.begin(), P.post.end());
     struct Part { uint64_t off; const void* src; size_t bytes; };
     const Part parts[] = {{P.ws_pieces, pieces.data(), pieces.size() * sizeof(IpPiece)},
+                          {P.ws_cols, P.cols.data(), P.cols.size() * sizeof(IpCol)},
                           {P.ws_tailf, P.tail_fields.data(), P.tail_fields.size() * sizeof(IpTailField)},
                           {P.ws_seq, P.seq.data(), P.seq.size() * sizeof(uint32_t)},
                           {P.ws_segs, P.segs.data(), P.segs.size() * sizeof(IpSeg)}};
@@ -315,7 +427,7 @@ extern "C" adha_status adha_remap_inplace(void* buf, uint64_t buf_bytes, const a
     uint8_t* ws = (uint8_t*)workspace;
     adha_status s = launch_tail(P, b, ws, false, st);
     if (s != ADHA_OK) return s;
-    s = launch_transpose(P, b, ws, false, dev, sms, st);
+    s = launch_tiles(P, b, ws, false, dev, sms, st);
     if (s != ADHA_OK) return s;
     if (!P.segs.empty()) {
         const uint32_t nseg = (uint32_t)P.segs.size();
@@ -335,7 +447,7 @@ extern "C" adha_status adha_remap_inplace(void* buf, uint64_t buf_bytes, const a
         e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_err(e, "ip_cycle kernels launch");
     }
-    s = launch_transpose(P, b, ws, true, dev, sms, st);
+    s = launch_tiles(P, b, ws, true, dev, sms, st);
     if (s != ADHA_OK) return s;
     return launch_tail(P, b, ws, true, st);
 }

@@ -37,9 +37,38 @@ int32_t field_at(const Layout& l, int32_t c, uint32_t o) {
     return mem[lo];
 }
 
-uint64_t smem_need(uint32_t T, uint32_t K, uint32_t u) {
-    // staged tile plus 4 bytes of padding per line (rows when record-major, columns otherwise)
-    return (uint64_t)T * K * u + 4ull * std::max<uint64_t>(T, K) + 16;
+uint64_t tile_smem(uint32_t T, uint64_t stride, size_t n_fields) {
+    // staged tile plus one padding atom (<= 4 bytes) per line: per record row in record-major
+    // form, per field block in field-blocked form
+    return ((uint64_t)T * stride + 4ull * std::max<uint64_t>(T, n_fields) + 15) & ~15ull;
+}
+
+uint64_t table_smem(uint64_t stride, uint32_t atom) { return stride / atom * sizeof(IpCol); }
+
+uint64_t smem_need(uint32_t T, uint64_t stride, size_t n_fields, uint32_t atom) {
+    // the kernel packs a padded atom index in 17 bits (field-blocked -> record-major table)
+    if ((uint64_t)T * stride / atom + 4ull * std::max<uint64_t>(T, n_fields) >= (1u << 17)) return ~0ull;
+    return tile_smem(T, stride, n_fields) + table_smem(stride, atom);
+}
+
+uint32_t magic(uint32_t d) {   // ceil(2^32 / d); 0 encodes d == 1
+    return d <= 1 ? 0u : (uint32_t)(((1ull << 32) + d - 1) / d);
+}
+
+// column table of a cluster record in atoms (word atoms when u % 4 == 0, else bytes)
+void add_cluster(const Layout& l, int32_t c, uint64_t base, uint32_t atom, uint32_t T, std::vector<IpPiece>& out,
+                 std::vector<IpCol>& cols) {
+    const uint32_t RA = (uint32_t)(l.stride[c] / atom);
+    IpPiece pc{base, (uint32_t)l.stride[c], RA, (uint32_t)cols.size(), magic(RA)};
+    out.push_back(pc);
+    const uint32_t padf = atom == 4 ? 1 : 4;   // padding atoms per field block (the kernel's PADF)
+    uint32_t fidx = 0;
+    for (int32_t f : l.members[c]) {
+        const uint32_t col = l.offset[f] / atom, a = l.width[f] / atom;
+        for (uint32_t k = 0; k < a; ++k)
+            cols.push_back({col | ((fidx * padf) << 16), a, magic(a), T * col + fidx * padf + k});
+        ++fidx;
+    }
 }
 
 }  // namespace
@@ -62,6 +91,7 @@ adha_status inplace_plan_build(const Layout& ls, const Layout& ld, int64_t n, In
         return fail(ADHA_ERR_TOO_LARGE, "N * record bytes overflows");
     const uint32_t u = pow2_unit(ls);
     p->u = u;
+    const uint32_t atom = u % 4 == 0 ? 4 : 1;
 
     // clusters kept as raw slots: same member set in both layouts
     const int32_t Cs = ls.n_clusters(), Cd = ld.n_clusters();
@@ -70,8 +100,9 @@ adha_status inplace_plan_build(const Layout& ls, const Layout& ld, int64_t n, In
         const int32_t cd = ld.cluster[ls.members[c][0]];
         if (same_members(ls, c, ld, cd)) { twin_s[c] = cd; twin_d[cd] = c; }
     }
-    auto transposed_s = [&](int32_t c) { return twin_s[c] < 0 && ls.stride[c] > u; };
-    auto transposed_d = [&](int32_t c) { return twin_d[c] < 0 && ld.stride[c] > u; };
+    // a single-field cluster's tile is already field-blocked
+    auto transposed_s = [&](int32_t c) { return twin_s[c] < 0 && ls.members[c].size() > 1; };
+    auto transposed_d = [&](int32_t c) { return twin_d[c] < 0 && ld.members[c].size() > 1; };
 
     // slot size: the largest power of two in [256, 4096] dividing every region base whose
     // transposed tiles fit the shared-memory budget
@@ -82,9 +113,9 @@ adha_status inplace_plan_build(const Layout& ls, const Layout& ld, int64_t n, In
         for (uint64_t b : p->bd) ok = ok && (b % cand == 0);
         const uint32_t T = cand / u;
         for (int32_t c = 0; ok && c < Cs; ++c)
-            if (transposed_s(c) && smem_need(T, (uint32_t)(ls.stride[c] / u), u) > IP_MAX_PIECE) ok = false;
+            if (transposed_s(c) && smem_need(T, ls.stride[c], ls.members[c].size(), atom) > IP_MAX_PIECE) ok = false;
         for (int32_t c = 0; ok && c < Cd; ++c)
-            if (transposed_d(c) && smem_need(T, (uint32_t)(ld.stride[c] / u), u) > IP_MAX_PIECE) ok = false;
+            if (transposed_d(c) && smem_need(T, ld.stride[c], ld.members[c].size(), atom) > IP_MAX_PIECE) ok = false;
         if (ok) { S = cand; break; }
     }
     if (!S) return fail(ADHA_ERR_UNSUPPORTED, "in-place remap: a cluster record is too wide for a " +
@@ -99,17 +130,20 @@ adha_status inplace_plan_build(const Layout& ls, const Layout& ld, int64_t n, In
 
     p->pre.clear();
     p->post.clear();
-    p->max_piece = 0;
+    p->cols.clear();
+    p->max_tile = p->max_tab = 0;
     if (m > 0) {
         for (int32_t c = 0; c < Cs; ++c)
             if (transposed_s(c)) {
-                p->pre.push_back({p->bs[c], (uint32_t)(ls.stride[c] / u), (uint32_t)ls.stride[c]});
-                p->max_piece = std::max<uint32_t>(p->max_piece, (uint32_t)smem_need(T, (uint32_t)(ls.stride[c] / u), u));
+                add_cluster(ls, c, p->bs[c], atom, T, p->pre, p->cols);
+                p->max_tile = std::max<uint32_t>(p->max_tile, (uint32_t)tile_smem(T, ls.stride[c], ls.members[c].size()));
+                p->max_tab = std::max<uint32_t>(p->max_tab, (uint32_t)table_smem(ls.stride[c], atom));
             }
         for (int32_t c = 0; c < Cd; ++c)
             if (transposed_d(c)) {
-                p->post.push_back({p->bd[c], (uint32_t)(ld.stride[c] / u), (uint32_t)ld.stride[c]});
-                p->max_piece = std::max<uint32_t>(p->max_piece, (uint32_t)smem_need(T, (uint32_t)(ld.stride[c] / u), u));
+                add_cluster(ld, c, p->bd[c], atom, T, p->post, p->cols);
+                p->max_tile = std::max<uint32_t>(p->max_tile, (uint32_t)tile_smem(T, ld.stride[c], ld.members[c].size()));
+                p->max_tab = std::max<uint32_t>(p->max_tab, (uint32_t)table_smem(ld.stride[c], atom));
             }
     }
 
@@ -200,6 +234,7 @@ adha_status inplace_plan_build(const Layout& ls, const Layout& ld, int64_t n, In
     uint64_t o = 0;
     auto take = [&](uint64_t bytes) { const uint64_t at = o; o = align256(o + bytes); return at; };
     p->ws_pieces = take((p->pre.size() + p->post.size()) * sizeof(IpPiece));
+    p->ws_cols = take(p->cols.size() * sizeof(IpCol));
     p->ws_tailf = take(p->tail_fields.size() * sizeof(IpTailField));
     p->ws_seq = take(p->seq.size() * sizeof(uint32_t));
     p->ws_segs = take(p->segs.size() * sizeof(IpSeg));
@@ -220,7 +255,7 @@ std::string inplace_plan_json(const InplacePlan& p) {
     s += ",\"src_bytes\":" + u64(p.bytes_s) + ",\"dst_bytes\":" + u64(p.bytes_d);
     s += ",\"buffer_bytes\":" + u64(std::max(p.bytes_s, p.bytes_d));
     s += ",\"pre_clusters\":" + u64(p.pre.size()) + ",\"post_clusters\":" + u64(p.post.size());
-    s += ",\"max_tile_smem\":" + u64(p.max_piece);
+    s += ",\"tile_smem\":" + u64(p.max_tile + p.max_tab);
     s += ",\"content_slots\":" + u64(p.content_slots) + ",\"moved_slots\":" + u64(p.moved_slots);
     s += ",\"fixed_slots\":" + u64(p.fixed_slots) + ",\"junk_slots\":" + u64(p.junk_slots);
     s += ",\"cycles\":" + u64(p.cycles) + ",\"segments\":" + u64(p.segs.size());

@@ -3,15 +3,18 @@
 //
 // The buffer is cut into slots of S bytes (S a power of two in [256, 4096] dividing every
 // region base of both layouts).  A tile of T = S / u records (u = the largest power of two
-// <= 16 dividing every field width) of a cluster with stride s occupies K = s / u slots:
-//   step 1  (tile-local) each src tile of a changed cluster is transposed in place from
-//           record-major to unit-column-major: slot k of the tile then holds byte-unit k of
-//           the cluster record for the tile's T records;
-//   step 2  (slot permutation) every slot moves to the slot its unit-column occupies in the
-//           dst layout, by following the permutation's cycles (split into segments so that
-//           the warps work in parallel; the last slot of each segment is saved first);
-//   step 3  (tile-local) each dst tile of a changed cluster is transposed back to record-major.
-// Clusters whose member set is the same in both layouts are moved as raw slots (no transpose),
+// <= 16 dividing every field width) of a cluster with stride s occupies s / u slots.  In the
+// tile's FIELD-BLOCKED form (AoSoA with block T) field f's T values are contiguous, T * w_f
+// bytes = w_f / u whole slots, each holding S / w_f consecutive records of f:
+//   step 1  (tile-local) each src tile of a multi-field cluster that changes is rewritten in
+//           place from record-major to field-blocked form (single-field clusters already are);
+//   step 2  (slot permutation) every slot moves to the slot its (field, records) occupy in the
+//           dst layout's field-blocked form, by following the permutation's cycles (split into
+//           segments so that warps work in parallel; the last slot of each segment is saved
+//           first);
+//   step 3  (tile-local) each dst tile of a multi-field cluster that changed is rewritten from
+//           field-blocked to record-major form.
+// Clusters whose member set is the same in both layouts are moved as raw slots (no rewrite),
 // and not at all when their region base is the same (fixed points).  The last N mod T records
 // (the tail) are saved to the workspace first and written to their dst positions last.
 #pragma once
@@ -23,10 +26,20 @@
 
 namespace adha {
 
-struct IpPiece {        // one cluster region transposed tile by tile (steps 1 and 3)
+struct IpPiece {        // one cluster region rewritten tile by tile (steps 1 and 3)
     uint64_t base;      // region base (bytes from the buffer start)
-    uint32_t K;         // byte-units per record (stride / u)
     uint32_t stride;    // cluster record bytes
+    uint32_t RA;        // atoms per record (atom = 4 bytes when u % 4 == 0, else 1 byte)
+    uint32_t col_off;   // first entry of this cluster in the column table
+    uint32_t magic_RA;  // ceil(2^32 / RA) (0 when RA == 1): q = umulhi(n, magic) for n * RA < 2^32
+};
+
+struct IpCol {          // one atom column j of a cluster record
+    uint32_t col_fp;    // first column of j's field (low 16 bits) | padding atoms before its block << 16
+    uint32_t a;         // atoms of j's field
+    uint32_t magic_a;   // ceil(2^32 / a) (0 when a == 1)
+    uint32_t bo;        // shared-memory atom of (record 0, column j) in the padded field-blocked tile:
+                        // T * col + padding before the block + (j - col); record r adds r * a
 };
 
 struct IpTailField {    // one field of the tail records: src/dst element address terms
@@ -51,14 +64,16 @@ struct InplacePlan {
     uint64_t bytes_s = 0, bytes_d = 0;   // bytes(Ls, n), bytes(Ld, n)
     std::vector<uint64_t> bs, bd;
     std::vector<IpPiece> pre, post;      // step 1 (src clusters), step 3 (dst clusters)
-    uint32_t max_piece = 0;              // bytes of the largest transposed tile
+    std::vector<IpCol> cols;             // column tables of pre then post clusters
+    uint32_t max_tile = 0;               // shared memory of the largest rewritten tile (with padding)
+    uint32_t max_tab = 0;                // shared memory of the largest column table
     std::vector<uint32_t> seq;           // slot indices, cycles in order (slot j -> next on its cycle)
     std::vector<IpSeg> segs;
     std::vector<IpTailField> tail_fields;
     // statistics
     uint64_t content_slots = 0, moved_slots = 0, fixed_slots = 0, junk_slots = 0, cycles = 0;
     // workspace layout (byte offsets, each 256-aligned) and total size
-    uint64_t ws_pieces = 0, ws_tailf = 0, ws_seq = 0, ws_segs = 0, ws_save = 0, ws_tail = 0, ws_bytes = 0;
+    uint64_t ws_pieces = 0, ws_cols = 0, ws_tailf = 0, ws_seq = 0, ws_segs = 0, ws_save = 0, ws_tail = 0, ws_bytes = 0;
     // upload state (adha_inplace_plan_upload)
     const void* uploaded = nullptr;
     int uploaded_device = -1;
