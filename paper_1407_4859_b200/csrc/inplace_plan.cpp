@@ -37,18 +37,68 @@ int32_t field_at(const Layout& l, int32_t c, uint32_t o) {
     return mem[lo];
 }
 
-uint64_t tile_smem(uint32_t T, uint64_t stride, size_t n_fields) {
-    // staged tile plus one padding atom (<= 4 bytes) per line: per record row in record-major
-    // form, per field block in field-blocked form
-    return ((uint64_t)T * stride + 4ull * std::max<uint64_t>(T, n_fields) + 15) & ~15ull;
+// Padding between field blocks of a field-blocked tile in shared memory (atoms per field): chosen
+// per cluster by simulating the bank conflicts of the field-blocked -> record-major gather
+// (ip_gather in inplace.cu: thread v builds output vector v, atoms (r, jc) with 4v + j = r*RA + jc,
+// read from bo(jc) + r * a(jc)); candidates keep the padding <= 64 bytes per field block.
+uint32_t choose_padf(const Layout& l, int32_t c, uint32_t T, uint32_t atom) {
+    const uint32_t RA = (uint32_t)(l.stride[c] / atom);
+    const uint32_t APV = 16 / atom;
+    const uint64_t natoms = (uint64_t)T * RA;
+    std::vector<uint32_t> col(RA), a(RA), fidx(RA);
+    uint32_t fi = 0;
+    for (int32_t f : l.members[c]) {
+        for (uint32_t k = 0; k < l.width[f] / atom; ++k) {
+            const uint32_t j = l.offset[f] / atom + k;
+            col[j] = l.offset[f] / atom;
+            a[j] = l.width[f] / atom;
+            fidx[j] = fi;
+        }
+        ++fi;
+    }
+    uint32_t best = 0;
+    uint64_t best_cost = ~0ull;
+    for (uint32_t padf = 0; padf * atom <= 64; padf += (atom == 4 ? 1 : 4)) {
+        uint64_t cost = 0;
+        for (uint64_t w = 0; w < 8 && (w * 32 + 31) * APV < natoms; ++w) {
+            for (uint32_t j = 0; j < APV; ++j) {
+                uint32_t words[32];
+                int nw = 0;
+                uint32_t per_bank[32] = {0};
+                for (uint32_t L = 0; L < 32; ++L) {
+                    const uint64_t o = (w * 32 + L) * APV + j;
+                    const uint32_t r = (uint32_t)(o / RA), jc = (uint32_t)(o % RA);
+                    const uint64_t at = (uint64_t)T * col[jc] + (uint64_t)fidx[jc] * padf + (jc - col[jc]) + (uint64_t)r * a[jc];
+                    const uint32_t word = (uint32_t)(at * atom / 4);
+                    bool seen = false;
+                    for (int q = 0; q < nw; ++q) seen = seen || words[q] == word;
+                    if (!seen) { words[nw++] = word; ++per_bank[word % 32]; }
+                }
+                uint32_t mx = 0;
+                for (uint32_t b = 0; b < 32; ++b) mx = std::max(mx, per_bank[b]);
+                cost += mx;
+            }
+        }
+        if (cost < best_cost) { best_cost = cost; best = padf; }
+    }
+    return best;
+}
+
+uint64_t tile_smem(uint32_t T, uint64_t stride, size_t n_fields, uint32_t atom, uint32_t padf) {
+    // staged tile plus its padding: one atom (<= 4 bytes) per record row in record-major form,
+    // padf atoms per field block in field-blocked form
+    return ((uint64_t)T * stride + std::max<uint64_t>(4ull * T, (uint64_t)n_fields * padf * atom) + 15) & ~15ull;
 }
 
 uint64_t table_smem(uint64_t stride, uint32_t atom) { return stride / atom * sizeof(IpCol); }
 
+constexpr uint32_t MAX_PADF_BYTES = 64;
+
 uint64_t smem_need(uint32_t T, uint64_t stride, size_t n_fields, uint32_t atom) {
     // the kernel packs a padded atom index in 17 bits (field-blocked -> record-major table)
-    if ((uint64_t)T * stride / atom + 4ull * std::max<uint64_t>(T, n_fields) >= (1u << 17)) return ~0ull;
-    return tile_smem(T, stride, n_fields) + table_smem(stride, atom);
+    const uint64_t pad_atoms = std::max<uint64_t>(4ull * T, (uint64_t)n_fields * MAX_PADF_BYTES) / atom;
+    if ((uint64_t)T * stride / atom + pad_atoms >= (1u << 17)) return ~0ull;
+    return tile_smem(T, stride, n_fields, atom, MAX_PADF_BYTES / atom) + table_smem(stride, atom);
 }
 
 uint32_t magic(uint32_t d) {   // ceil(2^32 / d); 0 encodes d == 1
@@ -56,12 +106,11 @@ uint32_t magic(uint32_t d) {   // ceil(2^32 / d); 0 encodes d == 1
 }
 
 // column table of a cluster record in atoms (word atoms when u % 4 == 0, else bytes)
-void add_cluster(const Layout& l, int32_t c, uint64_t base, uint32_t atom, uint32_t T, std::vector<IpPiece>& out,
-                 std::vector<IpCol>& cols) {
+void add_cluster(const Layout& l, int32_t c, uint64_t base, uint32_t atom, uint32_t T, uint32_t padf,
+                 std::vector<IpPiece>& out, std::vector<IpCol>& cols) {
     const uint32_t RA = (uint32_t)(l.stride[c] / atom);
     IpPiece pc{base, (uint32_t)l.stride[c], RA, (uint32_t)cols.size(), magic(RA)};
     out.push_back(pc);
-    const uint32_t padf = atom == 4 ? 1 : 4;   // padding atoms per field block (the kernel's PADF)
     uint32_t fidx = 0;
     for (int32_t f : l.members[c]) {
         const uint32_t col = l.offset[f] / atom, a = l.width[f] / atom;
@@ -135,14 +184,16 @@ adha_status inplace_plan_build(const Layout& ls, const Layout& ld, int64_t n, In
     if (m > 0) {
         for (int32_t c = 0; c < Cs; ++c)
             if (transposed_s(c)) {
-                add_cluster(ls, c, p->bs[c], atom, T, p->pre, p->cols);
-                p->max_tile = std::max<uint32_t>(p->max_tile, (uint32_t)tile_smem(T, ls.stride[c], ls.members[c].size()));
+                add_cluster(ls, c, p->bs[c], atom, T, 0, p->pre, p->cols);
+                p->max_tile = std::max<uint32_t>(p->max_tile, (uint32_t)tile_smem(T, ls.stride[c], ls.members[c].size(), atom, 0));
                 p->max_tab = std::max<uint32_t>(p->max_tab, (uint32_t)table_smem(ls.stride[c], atom));
             }
         for (int32_t c = 0; c < Cd; ++c)
             if (transposed_d(c)) {
-                add_cluster(ld, c, p->bd[c], atom, T, p->post, p->cols);
-                p->max_tile = std::max<uint32_t>(p->max_tile, (uint32_t)tile_smem(T, ld.stride[c], ld.members[c].size()));
+                const uint32_t padf = choose_padf(ld, c, T, atom);
+                add_cluster(ld, c, p->bd[c], atom, T, padf, p->post, p->cols);
+                p->max_tile = std::max<uint32_t>(p->max_tile,
+                                                 (uint32_t)tile_smem(T, ld.stride[c], ld.members[c].size(), atom, padf));
                 p->max_tab = std::max<uint32_t>(p->max_tab, (uint32_t)table_smem(ld.stride[c], atom));
             }
     }
