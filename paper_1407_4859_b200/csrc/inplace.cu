@@ -60,18 +60,20 @@ __device__ __forceinline__ uint32_t fdiv(uint32_t n, uint32_t magic) { return ma
 #define IP_LB 2
 #endif
 
-template <typename Atom>
+template <typename Atom, bool GROUPED>
 __device__ __forceinline__ void ip_scatter(Atom* sa, const uint4 x, uint32_t v, int to_blocks, uint32_t lgT,
-                                           uint32_t RA, uint32_t magic_RA, uint32_t padR, const IpCol* tab) {
+                                           const IpPiece& pc, uint32_t padR, const IpCol* tab) {
     constexpr uint32_t APV = 16 / sizeof(Atom);
-    const uint32_t w4[4] = {x.x, x.y, x.z, x.w};
     const uint32_t i0 = v * APV;
-    if (to_blocks) {   // record-major input: pad per row (row r starts at r * (RA + padR))
+    const uint32_t RA = pc.RA;
+    if (to_blocks) {   // record-major input: pad per row (row r starts at r * (RA + padR)); rows run on
+                       // across the tiles of a piece
+        const uint32_t w4[4] = {x.x, x.y, x.z, x.w};
         if (sizeof(Atom) == 4) {
 #pragma unroll
-            for (uint32_t j = 0; j < 4; ++j) sa[i0 + j + fdiv(i0 + j, magic_RA) * padR] = (Atom)w4[j];
+            for (uint32_t j = 0; j < 4; ++j) sa[i0 + j + fdiv(i0 + j, pc.magic_RA) * padR] = (Atom)w4[j];
         } else {
-            const uint32_t r0 = fdiv(i0, magic_RA);
+            const uint32_t r0 = fdiv(i0, pc.magic_RA);
             uint32_t o = i0 + r0 * padR, rr = i0 - r0 * RA;
 #pragma unroll
             for (uint32_t j = 0; j < 16; ++j) {
@@ -80,34 +82,36 @@ __device__ __forceinline__ void ip_scatter(Atom* sa, const uint4 x, uint32_t v, 
                 if (++rr == RA) { rr = 0; o += padR; }
             }
         }
-    } else {           // field-blocked input: pad per field block (a vector never straddles one)
-        const uint32_t o = i0 + reinterpret_cast<const uint32_t*>(tab)[RA + (i0 >> lgT)];
-        if (sizeof(Atom) == 4) {
-#pragma unroll
-            for (uint32_t j = 0; j < 4; ++j) sa[o + j] = (Atom)w4[j];
-        } else {
-#pragma unroll
-            for (uint32_t j = 0; j < 16; ++j) sa[o + j] = (Atom)(w4[j >> 2] >> (8 * (j & 3)));
-        }
+    } else {           // field-blocked input: tile q of the piece at q * TS, padding before each field
+                       // block, a multiple of 16 bytes (inplace_plan.cpp choose_padf), so the vector
+                       // stays 16-byte aligned: one conflict-free 16-byte store
+        const uint32_t q = GROUPED ? fdiv(i0, pc.magic_TRA) : 0;
+        const uint32_t i = i0 - q * (RA << lgT);
+        const uint32_t o = q * pc.TS + i + reinterpret_cast<const uint32_t*>(tab)[RA + (i >> lgT)];
+        *reinterpret_cast<uint4*>(sa + o) = x;
     }
 }
 
-template <typename Atom>
-__device__ __forceinline__ uint4 ip_gather(const Atom* sa, uint32_t v, int to_blocks, uint32_t lgT, uint32_t RA,
-                                           uint32_t magic_RA, uint32_t P, const IpCol* tab) {
+template <typename Atom, bool GROUPED>
+__device__ __forceinline__ uint4 ip_gather(const Atom* sa, uint32_t v, int to_blocks, uint32_t lgT, const IpPiece& pc,
+                                           uint32_t P, const IpCol* tab) {
     constexpr uint32_t APV = 16 / sizeof(Atom);
+    const uint32_t RA = pc.RA;
     uint32_t w4[4] = {0, 0, 0, 0};
     const uint32_t o0 = v * APV;
-    if (to_blocks) {   // output field-blocked: the vector lies in one column block
-        const IpCol e = tab[o0 >> lgT];
+    if (to_blocks) {   // output field-blocked: the vector lies in one column block of tile q
+        const uint32_t q = GROUPED ? fdiv(o0, pc.magic_TRA) : 0;
+        const uint32_t ot = o0 - q * (RA << lgT);
+        const IpCol e = tab[ot >> lgT];
         const uint32_t col = e.col_fp & 0xFFFFu;
-        const uint32_t local0 = o0 - (col << lgT);
+        const uint32_t local0 = ot - (col << lgT);
+        const uint32_t rq = q << lgT;                  // first record row of tile q
         if (sizeof(Atom) == 4 && e.a == 1) {          // 4 consecutive records of one column
-            const uint32_t a0 = local0 * P + col;
+            const uint32_t a0 = (rq + local0) * P + col;
 #pragma unroll
             for (uint32_t j = 0; j < 4; ++j) w4[j] = (uint32_t)sa[a0 + j * P];
         } else if (sizeof(Atom) == 4 && e.a == 2) {   // 2 records x 2 atoms
-            const uint32_t a0 = (local0 >> 1) * P + col;
+            const uint32_t a0 = (rq + (local0 >> 1)) * P + col;
             w4[0] = (uint32_t)sa[a0];
             w4[1] = (uint32_t)sa[a0 + 1];
             w4[2] = (uint32_t)sa[a0 + P];
@@ -117,19 +121,21 @@ __device__ __forceinline__ uint4 ip_gather(const Atom* sa, uint32_t v, int to_bl
             for (uint32_t j = 0; j < APV; ++j) {
                 const uint32_t local = local0 + j;
                 const uint32_t r = fdiv(local, e.magic_a);
-                const Atom val = sa[r * P + col + (local - r * e.a)];
+                const Atom val = sa[(rq + r) * P + col + (local - r * e.a)];
                 if (sizeof(Atom) == 4) w4[j] = (uint32_t)val;
                 else w4[j >> 2] |= (uint32_t)val << (8 * (j & 3));
             }
         }
-    } else {           // output record-major: atom (r, jc) <- field-blocked bo(jc) + r * a(jc)
+    } else {           // output record-major: atom (r', jc), r' = q*T + r <- q*TS + bo(jc) + r*a(jc)
         const uint32_t* bo_a = reinterpret_cast<const uint32_t*>(tab);   // packed bo | a << 17 (see ip_tile_kernel)
-        uint32_t r = fdiv(o0, magic_RA);
+        uint32_t r = fdiv(o0, pc.magic_RA);
         uint32_t jc = o0 - r * RA;
+        const uint32_t T1 = (1u << lgT) - 1;
 #pragma unroll
         for (uint32_t j = 0; j < APV; ++j) {
             const uint32_t e = bo_a[jc];
-            const Atom val = sa[(e & 0x1FFFFu) + r * (e >> 17)];
+            const Atom val = GROUPED ? sa[(r >> lgT) * pc.TS + (e & 0x1FFFFu) + (r & T1) * (e >> 17)]
+                                     : sa[(e & 0x1FFFFu) + r * (e >> 17)];
             if (sizeof(Atom) == 4) w4[j] = (uint32_t)val;
             else w4[j >> 2] |= (uint32_t)val << (8 * (j & 3));
             if (++jc == RA) { jc = 0; ++r; }
@@ -138,8 +144,10 @@ __device__ __forceinline__ uint4 ip_gather(const Atom* sa, uint32_t v, int to_bl
     return make_uint4(w4[0], w4[1], w4[2], w4[3]);
 }
 
-template <typename Atom, int to_blocks>
-__global__ void __launch_bounds__(256) ip_tile_kernel(uint8_t* __restrict__ buf, const IpPiece* __restrict__ cl,
+// MINB: 8 resident CTAs (32 registers) for small pieces, where occupancy hides the load latency;
+// 1 for large pieces (fewer CTAs fit anyway; the register budget then goes to the address math).
+template <typename Atom, int to_blocks, bool GROUPED, int MINB>
+__global__ void __launch_bounds__(256, MINB) ip_tile_kernel(uint8_t* __restrict__ buf, const IpPiece* __restrict__ cl,
                                                       const IpCol* __restrict__ cols, uint32_t ncl, uint64_t m,
                                                       uint32_t T, uint32_t tab_cap) {
     extern __shared__ __align__(16) uint8_t sm[];
@@ -149,46 +157,35 @@ __global__ void __launch_bounds__(256) ip_tile_kernel(uint8_t* __restrict__ buf,
     const uint32_t tid = threadIdx.x, nt = blockDim.x;
     uint4 x[IP_LB];
     uint32_t cur_c = 0xFFFFFFFFu;
-    // tiles are visited cluster-major: tile p = (c, t) with p = c * m + t, stepping by gridDim.x
-    uint32_t c = (uint32_t)(blockIdx.x / m);
-    uint64_t t = blockIdx.x - (uint64_t)c * m;
-    const uint64_t step_c = gridDim.x / m, step_t = gridDim.x - step_c * m;
-    auto advance = [&](uint32_t& cc, uint64_t& tt) {
-        cc += (uint32_t)step_c;
-        tt += step_t;
-        if (tt >= m) { tt -= m; ++cc; }
-    };
-    if (c < ncl) {   // batch 0 of the first tile
-        const IpPiece pc = cl[c];
-        const uint4* g4 = reinterpret_cast<const uint4*>(buf + pc.base + t * (uint64_t)T * pc.stride);
-        const uint32_t nvec = (T * pc.stride) >> 4;
+
+    auto load_batch0 = [&](const uint8_t* gp, uint32_t nvec) {
+        const uint4* g4 = reinterpret_cast<const uint4*>(gp);
 #pragma unroll
         for (uint32_t k = 0; k < IP_LB; ++k)
             if (tid + k * nt < nvec) x[k] = g4[tid + k * nt];
-    }
-    for (; c < ncl; advance(c, t)) {
-        const IpPiece pc = cl[c];
-        uint8_t* g = buf + pc.base + t * (uint64_t)T * pc.stride;
-        if (c != cur_c) {   // this cluster's column table -> shared memory
-            if (to_blocks) {
-                for (uint32_t j = tid; j < pc.RA; j += nt) tab[j] = cols[pc.col_off + j];
-            } else {        // field-blocked -> record-major needs only bo and a: one packed word per column
-                uint32_t* bo_a = reinterpret_cast<uint32_t*>(tab);   // [RA] bo | a << 17, then [RA] padding
-                for (uint32_t j = tid; j < pc.RA; j += nt) {
-                    const IpCol e = cols[pc.col_off + j];
-                    bo_a[j] = e.bo | (e.a << 17);
-                    bo_a[pc.RA + j] = e.col_fp >> 16;
-                }
+    };
+    auto load_table = [&](uint32_t c, const IpPiece& d) {   // cluster descriptor's column table -> smem
+        if (c == cur_c) return;
+        if (to_blocks) {
+            for (uint32_t j = tid; j < d.RA; j += nt) tab[j] = cols[d.col_off + j];
+        } else {        // field-blocked -> record-major needs only bo and a: one packed word per column
+            uint32_t* bo_a = reinterpret_cast<uint32_t*>(tab);   // [RA] bo | a << 17, then [RA] padding
+            for (uint32_t j = tid; j < d.RA; j += nt) {
+                const IpCol e = cols[d.col_off + j];
+                bo_a[j] = e.bo | (e.a << 17);
+                bo_a[d.RA + j] = e.col_fp >> 16;
             }
-            cur_c = c;
-            __syncthreads();
         }
+        cur_c = c;
+        __syncthreads();
+    };
+    // one piece: batch 0 is in registers; scatter into the padded tile, prefetch the next piece's
+    // batch 0, gather in output order, write back with 16-byte stores
+    auto body = [&](const IpPiece& pc, uint8_t* g, uint32_t nvec, auto&& prefetch_next) {
         const uint32_t RA = pc.RA;
         const uint32_t padR = sizeof(Atom) == 4 ? ((RA & 1) ? 0 : 1) : 4;   // row padding (odd word pitch)
         const uint32_t P = RA + padR;
-        const uint32_t nvec = (T * pc.stride) >> 4;
         const uint4* g4 = reinterpret_cast<const uint4*>(g);
-        // ---- load: batch 0 is already in registers; further batches are loaded here
         for (uint32_t b0 = 0; b0 < nvec; b0 += IP_LB * nt) {
             if (b0) {
 #pragma unroll
@@ -198,28 +195,78 @@ __global__ void __launch_bounds__(256) ip_tile_kernel(uint8_t* __restrict__ buf,
 #pragma unroll
             for (uint32_t k = 0; k < IP_LB; ++k) {
                 const uint32_t v = b0 + tid + k * nt;
-                if (v < nvec) ip_scatter<Atom>(sa, x[k], v, to_blocks, lgT, RA, pc.magic_RA, padR, tab);
+                if (v < nvec) ip_scatter<Atom, GROUPED>(sa, x[k], v, to_blocks, lgT, pc, padR, tab);
             }
         }
         __syncthreads();
-        // ---- prefetch batch 0 of this CTA's next tile (no other CTA writes it)
-        {
-            uint32_t cn = c;
-            uint64_t tn = t;
-            advance(cn, tn);
-            if (cn < ncl) {
-                const IpPiece pcn = cl[cn];
-                const uint4* gn = reinterpret_cast<const uint4*>(buf + pcn.base + tn * (uint64_t)T * pcn.stride);
-                const uint32_t nvn = (T * pcn.stride) >> 4;
-#pragma unroll
-                for (uint32_t k = 0; k < IP_LB; ++k)
-                    if (tid + k * nt < nvn) x[k] = gn[tid + k * nt];
-            }
-        }
-        // ---- gather in output order -> 16-byte stores
+        prefetch_next();   // no other CTA writes the next piece
         uint4* o4 = reinterpret_cast<uint4*>(g);
-        for (uint32_t v = tid; v < nvec; v += nt) o4[v] = ip_gather<Atom>(sa, v, to_blocks, lgT, RA, pc.magic_RA, P, tab);
+        for (uint32_t v = tid; v < nvec; v += nt) o4[v] = ip_gather<Atom, GROUPED>(sa, v, to_blocks, lgT, pc, P, tab);
         __syncthreads();
+    };
+
+    if constexpr (!GROUPED) {
+        // one tile per piece: tile p = (c, t) with p = c * m + t, stepping by gridDim.x
+        uint32_t c = (uint32_t)(blockIdx.x / m);
+        uint64_t t = blockIdx.x - (uint64_t)c * m;
+        const uint64_t step_c = gridDim.x / m, step_t = gridDim.x - step_c * m;
+        auto advance = [&](uint32_t& cc, uint64_t& tt) {
+            cc += (uint32_t)step_c;
+            tt += step_t;
+            if (tt >= m) { tt -= m; ++cc; }
+        };
+        if (c < ncl) {
+            const IpPiece d = cl[c];
+            load_batch0(buf + d.base + t * (uint64_t)T * d.stride, T * d.stride >> 4);
+        }
+        for (; c < ncl; advance(c, t)) {
+            const IpPiece pc = cl[c];
+            load_table(c, pc);
+            body(pc, buf + pc.base + t * (uint64_t)T * pc.stride, T * pc.stride >> 4, [&] {
+                uint32_t cn = c;
+                uint64_t tn = t;
+                advance(cn, tn);
+                if (cn < ncl) {
+                    const IpPiece pn = cl[cn];
+                    load_batch0(buf + pn.base + tn * (uint64_t)T * pn.stride, T * pn.stride >> 4);
+                }
+            });
+        }
+    } else {
+        // pieces of g_c tiles: piece (c, t) covers tiles [t*g_c, min((t+1)*g_c, m)) of cluster c;
+        // a CTA steps by gridDim.x pieces (piece counts differ between clusters)
+        uint32_t c = 0;
+        uint64_t t = blockIdx.x;
+        auto normalize = [&](uint32_t& cc, uint64_t& tt) {
+            while (cc < ncl) {
+                const uint64_t np = cl[cc].pieces;
+                if (tt < np) break;
+                tt -= np;
+                ++cc;
+            }
+        };
+        auto piece_vecs = [&](const IpPiece& d, uint64_t tt) {
+            const uint64_t t0 = tt * d.g;
+            return (uint32_t)(m - t0 < d.g ? m - t0 : d.g) * T * d.stride >> 4;
+        };
+        normalize(c, t);
+        if (c < ncl) {
+            const IpPiece d = cl[c];
+            load_batch0(buf + d.base + t * d.g * (uint64_t)T * d.stride, piece_vecs(d, t));
+        }
+        for (; c < ncl; t += gridDim.x, normalize(c, t)) {
+            const IpPiece pc = cl[c];
+            load_table(c, pc);
+            body(pc, buf + pc.base + t * pc.g * (uint64_t)T * pc.stride, piece_vecs(pc, t), [&] {
+                uint32_t cn = c;
+                uint64_t tn = t + gridDim.x;
+                normalize(cn, tn);
+                if (cn < ncl) {
+                    const IpPiece pn = cl[cn];
+                    load_batch0(buf + pn.base + tn * pn.g * (uint64_t)T * pn.stride, piece_vecs(pn, tn));
+                }
+            });
+        }
     }
 }
 
@@ -315,7 +362,11 @@ std::set<std::pair<int, const void*>> g_attr_done;
 adha_status smem_optin(int dev, const void* fn) {
     std::lock_guard<std::mutex> g(g_attr_mu);
     if (g_attr_done.count({dev, fn})) return ADHA_OK;
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    cudaFuncAttributes fa;
+    cudaError_t e = cudaFuncGetAttributes(&fa, fn);
+    if (e != cudaSuccess) return cuda_err(e, "cudaFuncGetAttributes");
+    // opt-in limit per block (227 KB on sm_100) minus the kernel's static shared memory
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448 - (int)fa.sharedSizeBytes);
     if (e != cudaSuccess) return cuda_err(e, "cudaFuncSetAttribute");
     g_attr_done.insert({dev, fn});
     return ADHA_OK;
@@ -329,16 +380,28 @@ adha_status launch_tiles(const InplacePlan& P, uint8_t* buf, const uint8_t* ws, 
     const IpCol* cols = reinterpret_cast<const IpCol*>(ws + P.ws_cols);
     const uint32_t tab_cap = (P.max_tab + 15) & ~15u;
     const uint32_t smem = tab_cap + P.max_tile;
-    const void* fn = P.u % 4 == 0 ? (post ? (const void*)ipdev::ip_tile_kernel<uint32_t, 0>
-                                          : (const void*)ipdev::ip_tile_kernel<uint32_t, 1>)
-                                  : (post ? (const void*)ipdev::ip_tile_kernel<uint8_t, 0>
-                                          : (const void*)ipdev::ip_tile_kernel<uint8_t, 1>);
+    bool grouped = false;
+    for (const IpPiece& pc : v) grouped = grouped || pc.g > 1;
+    const bool small = 8ull * (smem + 1024) <= 232448;   // 8 CTAs of this size fit in one SM
+    using K = void (*)(uint8_t*, const IpPiece*, const IpCol*, uint32_t, uint64_t, uint32_t, uint32_t);
+    // [word atoms?][post?][grouped?][small?]
+    static const K table[2][2][2][2] = {
+        {{{ipdev::ip_tile_kernel<uint8_t, 1, false, 1>, ipdev::ip_tile_kernel<uint8_t, 1, false, 8>},
+          {ipdev::ip_tile_kernel<uint8_t, 1, true, 1>, ipdev::ip_tile_kernel<uint8_t, 1, true, 8>}},
+         {{ipdev::ip_tile_kernel<uint8_t, 0, false, 1>, ipdev::ip_tile_kernel<uint8_t, 0, false, 8>},
+          {ipdev::ip_tile_kernel<uint8_t, 0, true, 1>, ipdev::ip_tile_kernel<uint8_t, 0, true, 8>}}},
+        {{{ipdev::ip_tile_kernel<uint32_t, 1, false, 1>, ipdev::ip_tile_kernel<uint32_t, 1, false, 8>},
+          {ipdev::ip_tile_kernel<uint32_t, 1, true, 1>, ipdev::ip_tile_kernel<uint32_t, 1, true, 8>}},
+         {{ipdev::ip_tile_kernel<uint32_t, 0, false, 1>, ipdev::ip_tile_kernel<uint32_t, 0, false, 8>},
+          {ipdev::ip_tile_kernel<uint32_t, 0, true, 1>, ipdev::ip_tile_kernel<uint32_t, 0, true, 8>}}}};
+    const void* fn = (const void*)table[P.u % 4 == 0][post][grouped][small];
     adha_status s = smem_optin(dev, fn);
     if (s != ADHA_OK) return s;
     int occ = 0;
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 256, smem);
     if (e != cudaSuccess) return cuda_err(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
-    const uint64_t pieces = (uint64_t)v.size() * (uint64_t)P.m;
+    uint64_t pieces = 0;
+    for (const IpPiece& pc : v) pieces += pc.pieces;
     const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(pieces, (uint64_t)sms * std::max(occ, 1)));
     uint32_t ncl = (uint32_t)v.size(), T = P.T;
     uint64_t m = (uint64_t)P.m;

@@ -40,7 +40,8 @@ int32_t field_at(const Layout& l, int32_t c, uint32_t o) {
 // Padding between field blocks of a field-blocked tile in shared memory (atoms per field): chosen
 // per cluster by simulating the bank conflicts of the field-blocked -> record-major gather
 // (ip_gather in inplace.cu: thread v builds output vector v, atoms (r, jc) with 4v + j = r*RA + jc,
-// read from bo(jc) + r * a(jc)); candidates keep the padding <= 64 bytes per field block.
+// read from bo(jc) + r * a(jc)); candidates are multiples of 16 bytes (the tile is staged with
+// 16-byte shared-memory stores) up to 64 bytes per field block.
 uint32_t choose_padf(const Layout& l, int32_t c, uint32_t T, uint32_t atom) {
     const uint32_t RA = (uint32_t)(l.stride[c] / atom);
     const uint32_t APV = 16 / atom;
@@ -58,7 +59,7 @@ uint32_t choose_padf(const Layout& l, int32_t c, uint32_t T, uint32_t atom) {
     }
     uint32_t best = 0;
     uint64_t best_cost = ~0ull;
-    for (uint32_t padf = 0; padf * atom <= 64; padf += (atom == 4 ? 1 : 4)) {
+    for (uint32_t padf = 0; padf * atom <= 64; padf += 16 / atom) {
         uint64_t cost = 0;
         for (uint64_t w = 0; w < 8 && (w * 32 + 31) * APV < natoms; ++w) {
             for (uint32_t j = 0; j < APV; ++j) {
@@ -105,11 +106,26 @@ uint32_t magic(uint32_t d) {   // ceil(2^32 / d); 0 encodes d == 1
     return d <= 1 ? 0u : (uint32_t)(((1ull << 32) + d - 1) / d);
 }
 
-// column table of a cluster record in atoms (word atoms when u % 4 == 0, else bytes)
-void add_cluster(const Layout& l, int32_t c, uint64_t base, uint32_t atom, uint32_t T, uint32_t padf,
-                 std::vector<IpPiece>& out, std::vector<IpCol>& cols) {
+constexpr uint64_t IP_PIECE_TARGET = 16384;   // bytes: small tiles are grouped up to this
+
+// column table of a cluster record in atoms (word atoms when u % 4 == 0, else bytes); returns the
+// shared memory of one piece (g padded tiles)
+uint64_t add_cluster(const Layout& l, int32_t c, uint64_t base, uint32_t atom, uint32_t T, uint64_t m, uint32_t padf,
+                     std::vector<IpPiece>& out, std::vector<IpCol>& cols) {
     const uint32_t RA = (uint32_t)(l.stride[c] / atom);
-    IpPiece pc{base, (uint32_t)l.stride[c], RA, (uint32_t)cols.size(), magic(RA)};
+    const uint64_t tile = (uint64_t)T * l.stride[c];
+    const uint32_t g = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(IP_PIECE_TARGET / tile, m));
+    const uint32_t nf = (uint32_t)l.members[c].size();
+    IpPiece pc{};
+    pc.base = base;
+    pc.g = g;
+    pc.pieces = (m + g - 1) / g;
+    pc.stride = (uint32_t)l.stride[c];
+    pc.RA = RA;
+    pc.col_off = (uint32_t)cols.size();
+    pc.magic_RA = magic(RA);
+    pc.magic_TRA = magic(T * RA);
+    pc.TS = T * RA + nf * padf;
     out.push_back(pc);
     uint32_t fidx = 0;
     for (int32_t f : l.members[c]) {
@@ -118,6 +134,8 @@ void add_cluster(const Layout& l, int32_t c, uint64_t base, uint32_t atom, uint3
             cols.push_back({col | ((fidx * padf) << 16), a, magic(a), T * col + fidx * padf + k});
         ++fidx;
     }
+    // field-blocked: g tiles of TS atoms; record-major: g*T rows with one padding atom (4 bytes) each
+    return (std::max<uint64_t>((uint64_t)g * pc.TS * atom, (uint64_t)g * T * (l.stride[c] + 4)) + 15) & ~15ull;
 }
 
 }  // namespace
@@ -184,16 +202,15 @@ adha_status inplace_plan_build(const Layout& ls, const Layout& ld, int64_t n, In
     if (m > 0) {
         for (int32_t c = 0; c < Cs; ++c)
             if (transposed_s(c)) {
-                add_cluster(ls, c, p->bs[c], atom, T, 0, p->pre, p->cols);
-                p->max_tile = std::max<uint32_t>(p->max_tile, (uint32_t)tile_smem(T, ls.stride[c], ls.members[c].size(), atom, 0));
+                const uint64_t sm = add_cluster(ls, c, p->bs[c], atom, T, m, 0, p->pre, p->cols);
+                p->max_tile = std::max<uint32_t>(p->max_tile, (uint32_t)sm);
                 p->max_tab = std::max<uint32_t>(p->max_tab, (uint32_t)table_smem(ls.stride[c], atom));
             }
         for (int32_t c = 0; c < Cd; ++c)
             if (transposed_d(c)) {
                 const uint32_t padf = choose_padf(ld, c, T, atom);
-                add_cluster(ld, c, p->bd[c], atom, T, padf, p->post, p->cols);
-                p->max_tile = std::max<uint32_t>(p->max_tile,
-                                                 (uint32_t)tile_smem(T, ld.stride[c], ld.members[c].size(), atom, padf));
+                const uint64_t sm = add_cluster(ld, c, p->bd[c], atom, T, m, padf, p->post, p->cols);
+                p->max_tile = std::max<uint32_t>(p->max_tile, (uint32_t)sm);
                 p->max_tab = std::max<uint32_t>(p->max_tab, (uint32_t)table_smem(ld.stride[c], atom));
             }
     }

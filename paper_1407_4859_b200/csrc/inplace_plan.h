@@ -26,12 +26,17 @@
 
 namespace adha {
 
-struct IpPiece {        // one cluster region rewritten tile by tile (steps 1 and 3)
+struct IpPiece {        // one cluster region rewritten piece by piece (steps 1 and 3)
     uint64_t base;      // region base (bytes from the buffer start)
+    uint64_t pieces;    // ceil(m / g): pieces of this cluster
     uint32_t stride;    // cluster record bytes
     uint32_t RA;        // atoms per record (atom = 4 bytes when u % 4 == 0, else 1 byte)
     uint32_t col_off;   // first entry of this cluster in the column table
     uint32_t magic_RA;  // ceil(2^32 / RA) (0 when RA == 1): q = umulhi(n, magic) for n * RA < 2^32
+    uint32_t g;         // tiles per piece (small tiles are grouped so that a piece is ~16 KB)
+    uint32_t magic_TRA; // ceil(2^32 / (T * RA)) (used when g > 1)
+    uint32_t TS;        // atoms of one padded field-blocked tile in shared memory
+    uint32_t pad;
 };
 
 struct IpCol {          // one atom column j of a cluster record
