@@ -298,7 +298,10 @@ __global__ void __launch_bounds__(256) ip_cycle_shift_kernel(uint8_t* buf, const
                                                              const IpSeg* __restrict__ segs, uint32_t nseg,
                                                              const uint8_t* __restrict__ save) {
     constexpr uint32_t V = S / 16, G = V < 32 ? V : 32, VPL = V / G;
-    constexpr uint32_t B = VPL >= 8 ? 1 : 8 / VPL;     // slots per batch (8 vectors in flight per lane)
+#ifndef IP_SHIFT_VEC
+#define IP_SHIFT_VEC 8
+#endif
+    constexpr uint32_t B = VPL >= IP_SHIFT_VEC ? 1 : IP_SHIFT_VEC / VPL;   // slots per batch (IP_SHIFT_VEC vectors in flight per lane)
     const uint32_t lane = threadIdx.x % G;
     const uint64_t g0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / G;
     const uint64_t ng = (uint64_t)gridDim.x * blockDim.x / G;
