@@ -290,6 +290,137 @@ def run_reference(args, rank, world):
     return 0
 
 
+# ----------------------------------------------------------------------------------------- in-place arm
+
+def run_inplace(args, rank, world, local, share):
+    """--inplace: the same workload remapped IN PLACE (adha_remap_inplace, NEXT N1): one buffer of
+    max(bytes) per rank instead of one per layout.  A step runs every hop of the config's chain;
+    odd steps run the chain backwards, so each step remaps real contents.  `value` counts the
+    remap's algorithmic bytes (2 N R per hop, like the out-of-place line); `roofline` is the whole
+    in-place step (tile + cycle kernels) against the plans' device traffic."""
+    import torch
+    import torch.distributed as dist
+    import paper_1407_4859_b200 as A
+    from paper_1407_4859_b200.sharding import shard_for, max_over_ranks, aggregate_gbs
+    from adha_inputs import fill_random_device, SEED_BASE
+
+    dev = torch.device("cuda", local)
+    name = args.config
+    desc, kind, n_cfg, scaling = CONFIGS[name]
+    widths, chain = chain_for(kind)
+    R = sum(widths)
+    n_total, lo, hi = shard_for(n_cfg, world, rank, scaling)
+    n = hi - lo
+    lays = [A.Layout(widths, lab) for lab in chain]
+    t_plan = time.perf_counter()
+    fwd = [A.InplacePlan(lays[k], lays[k + 1], n) for k in range(len(lays) - 1)]
+    bwd = [A.InplacePlan(lays[k + 1], lays[k], n) for k in reversed(range(len(lays) - 1))]
+    plan_ms = (time.perf_counter() - t_plan) * 1e3
+    buf = torch.empty(max(max(p.buffer_bytes for p in fwd + bwd), 256), dtype=torch.uint8, device=dev)
+    fill_random_device(buf, SEED_BASE + 1 + rank)
+    for p in fwd + bwd:
+        p.upload()
+    stream = torch.cuda.current_stream(dev)
+    hops = len(fwd)
+    parity = [0]
+
+    def step():
+        for p in (fwd if parity[0] == 0 else bwd):
+            A.remap_inplace(buf, p)
+        parity[0] ^= 1
+
+    def barrier():
+        if world > 1:
+            dist.barrier() if share else dist.barrier(device_ids=[local])
+
+    def launches(p):
+        d = p.describe()
+        return (2 * (d["tail_records"] > 0) + (d["pre_clusters"] > 0) + (d["post_clusters"] > 0)
+                + 2 * (d["segments"] > 0))
+    for _ in range(max(args.warmup, 3) + (max(args.warmup, 3) % 2)):   # even: the buffer is back in chain[0]
+        step()
+    torch.cuda.synchronize(dev)
+    barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.005)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.steps):
+        step()
+    t1.record(stream)
+    torch.cuda.synchronize(dev)
+    barrier()
+    clk = clocks.stop()
+    ms_total = t0.elapsed_time(t1)
+    ms_max = max_over_ranks(ms_total, dev)
+    value = aggregate_gbs(n_total, R, hops, args.steps, ms_max)
+    n_f, n_b = (args.steps + 1) // 2, args.steps // 2
+    traffic_rank = (n_f * sum(p.describe()["traffic_bytes"] for p in fwd)
+                    + n_b * sum(p.describe()["traffic_bytes"] for p in bwd))
+    n_launch = n_f * sum(launches(p) for p in fwd) + n_b * sum(launches(p) for p in bwd)
+    peak, peak_src = measured_peak()
+    achieved = traffic_rank / (ms_total * 1e-3) / 1e9
+
+    # end to end through the public API: pinned host records in, in-place remap(s), host records out
+    e2e = None
+    if not args.no_e2e and n > 0:
+        nb0, nbl = lays[0].nbytes(n), lays[-1].nbytes(n)
+        h_in = torch.empty(nb0, dtype=torch.uint8).pin_memory()
+        h_in.copy_(buf[:nb0].cpu())
+        h_out = torch.empty(nbl, dtype=torch.uint8).pin_memory()
+
+        def e2e_step():
+            buf[:nb0].copy_(h_in, non_blocking=True)
+            for p in fwd:
+                A.remap_inplace(buf, p)
+            h_out.copy_(buf[:nbl], non_blocking=True)
+        e2e_steps = max(3, min(args.steps, 10))
+        e2e_step()
+        torch.cuda.synchronize(dev)
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(e2e_steps):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        barrier()
+        e_ms = max_over_ranks(e0.elapsed_time(e1), dev)
+        e2e = {"value": aggregate_gbs(n_total, R, hops, e2e_steps, e_ms), "unit": "GB/s",
+               "h2d_bytes_per_step": nb0, "d2h_bytes_per_step": nbl,
+               "api": "H2D copy + adha_remap_inplace x%d + D2H copy" % hops, "ms_per_step": e_ms / e2e_steps}
+
+    if rank == 0:
+        line = {
+            "metric": "remap GB/s (read+write)", "value": value, "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic (seeded random bytes generated on the device)", "impl": "adha-inplace",
+            "config": {
+                "workload": f"{name} in place: {desc}", "n_records_total": n_total, "n_records_per_rank": n,
+                "record_bytes": R, "remaps_per_step": hops, "layouts": [l.to_string() for l in lays],
+                "direction": "chain forwards on even steps, backwards on odd steps",
+                "buffer_bytes_per_rank": buf.numel(),
+                "out_of_place_buffers_bytes_per_rank": sum(l.nbytes(n) for l in lays),
+                "workspace_bytes_per_rank": sum(p.workspace_bytes for p in fwd + bwd),
+                "plans": [p.describe() for p in fwd],
+                "host_plan_ms": plan_ms,
+                "l2": "inputs larger than L2; no flush" if 2 * n * R > (252 << 20) else "inputs fit in L2 (latency-bound)",
+                "parallelism": f"shard by contiguous record range over {world} GPU(s), no data-path collective",
+            },
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": None, "peak_source": peak_src,
+                         "kernel": "whole in-place step (ip_tile_kernel + ip_cycle kernels), plan traffic_bytes",
+                         "algorithmic_bytes_per_step": traffic_rank / args.steps, "avg_step_ms": ms_total / args.steps},
+            "gpu_launches": n_launch, "clocks": clk, "e2e": e2e, "cpu_baseline": None,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 # ----------------------------------------------------------------------------------------- adha arm
 
 def main():
@@ -299,6 +430,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="adha", choices=["adha", "reference"])
+    ap.add_argument("--inplace", action="store_true",
+                    help="remap in place (adha_remap_inplace): one buffer of max(bytes) per rank")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-copy-ref", action="store_true")
@@ -331,6 +464,9 @@ def main():
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=dev)
+
+    if args.inplace:
+        return run_inplace(args, rank, world, local, share)
 
     import paper_1407_4859_b200 as A
     from paper_1407_4859_b200.sharding import shard_for, max_over_ranks, aggregate_gbs

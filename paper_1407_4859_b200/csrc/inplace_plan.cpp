@@ -107,6 +107,7 @@ uint32_t magic(uint32_t d) {   // ceil(2^32 / d); 0 encodes d == 1
 }
 
 constexpr uint64_t IP_PIECE_TARGET = 16384;   // bytes: small tiles are grouped up to this
+constexpr uint64_t IP_TILE_PREF = 32768;      // bytes: preferred largest rewritten tile
 
 // column table of a cluster record in atoms (word atoms when u % 4 == 0, else bytes); returns the
 // shared memory of one piece (g padded tiles)
@@ -172,18 +173,25 @@ adha_status inplace_plan_build(const Layout& ls, const Layout& ld, int64_t n, In
     auto transposed_d = [&](int32_t c) { return twin_d[c] < 0 && ld.members[c].size() > 1; };
 
     // slot size: the largest power of two in [256, 4096] dividing every region base whose
-    // transposed tiles fit the shared-memory budget
+    // rewritten tiles stay small (<= IP_TILE_PREF bytes: several CTAs per SM hide the load
+    // latency of the tile pass), else the largest whose tiles fit the shared-memory budget
     uint32_t S = 0;
-    for (uint32_t cand = 4096; cand >= 256; cand >>= 1) {
-        bool ok = true;
-        for (uint64_t b : p->bs) ok = ok && (b % cand == 0);
-        for (uint64_t b : p->bd) ok = ok && (b % cand == 0);
-        const uint32_t T = cand / u;
-        for (int32_t c = 0; ok && c < Cs; ++c)
-            if (transposed_s(c) && smem_need(T, ls.stride[c], ls.members[c].size(), atom) > IP_MAX_PIECE) ok = false;
-        for (int32_t c = 0; ok && c < Cd; ++c)
-            if (transposed_d(c) && smem_need(T, ld.stride[c], ld.members[c].size(), atom) > IP_MAX_PIECE) ok = false;
-        if (ok) { S = cand; break; }
+    for (int pass = 0; pass < 2 && !S; ++pass) {
+        for (uint32_t cand = 4096; cand >= 256; cand >>= 1) {
+            bool ok = true;
+            for (uint64_t b : p->bs) ok = ok && (b % cand == 0);
+            for (uint64_t b : p->bd) ok = ok && (b % cand == 0);
+            const uint32_t T = cand / u;
+            auto fits = [&](const Layout& l, int32_t c) {
+                if (pass == 0 && (uint64_t)T * l.stride[c] > IP_TILE_PREF) return false;
+                return smem_need(T, l.stride[c], l.members[c].size(), atom) <= IP_MAX_PIECE;
+            };
+            for (int32_t c = 0; ok && c < Cs; ++c)
+                if (transposed_s(c) && !fits(ls, c)) ok = false;
+            for (int32_t c = 0; ok && c < Cd; ++c)
+                if (transposed_d(c) && !fits(ld, c)) ok = false;
+            if (ok) { S = cand; break; }
+        }
     }
     if (!S) return fail(ADHA_ERR_UNSUPPORTED, "in-place remap: a cluster record is too wide for a " +
                                                   std::to_string(256 / u) + "-record tile in shared memory");

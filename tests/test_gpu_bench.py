@@ -63,3 +63,17 @@ def test_bench_two_ranks_share_gpu():
                    "--no-copy-ref"], env={"ADHA_BENCH_SHARE_GPU": "1"}, torchrun=2)
     assert d["n_gpus"] == 2 and d["scaling"] == "weak"
     assert d["config"]["n_records_total"] == 2 * d["config"]["n_records_per_rank"]
+
+
+@pytest.mark.parametrize("cfg", ["C2", "C4"])
+def test_bench_inplace_contract(cfg):
+    """--inplace: the same contract keys; C4's chain returns to AoS each step, C2 alternates
+    direction; the buffer is max(bytes), not the sum."""
+    d = run_bench(["--inplace", "--config", cfg, "--steps", "6", "--warmup", "3"])
+    for k in KEYS:
+        assert k in d, k
+    assert d["impl"] == "adha-inplace" and d["value"] > 500
+    c = d["config"]
+    assert c["buffer_bytes_per_rank"] < c["out_of_place_buffers_bytes_per_rank"]
+    assert 0 < d["roofline"]["frac"] < 1.2 and d["gpu_launches"] > 0
+    assert d["e2e"]["value"] > 0

@@ -50,6 +50,7 @@ def cases():
         "P1": (med, [0] * 9, [0, 0, 0, 1, 2, 3, 4, 5, 6], 1 << 24),
         "P1b": (med, [0, 0, 0, 1, 2, 3, 4, 5, 6], list(range(9)), 1 << 24),
         "P2": (km, list(range(32)), [f // 8 for f in range(32)], 1 << 23),
+        "P2b": (km, [f // 8 for f in range(32)], [0] * 32, 1 << 23),
         "C3s": (w64, list(range(64)), c3_labels(), 10_000_000),
     }
 
@@ -70,7 +71,7 @@ def time_fn(fn, reps, st):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=10)
-    ap.add_argument("--cases", default="C2,C2r,P1,P1b,P2,C3s")
+    ap.add_argument("--cases", default="C2,C2r,P1,P1b,P2,P2b,C3s")
     ap.add_argument("--no-oop", action="store_true")
     ap.add_argument("--kernels", action="store_true", help="per-kernel device times (torch.profiler / CUPTI)")
     a = ap.parse_args()
