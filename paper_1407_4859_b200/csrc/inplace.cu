@@ -344,8 +344,9 @@ adha_status cuda_err(cudaError_t e, const char* what) {
     return fail(ADHA_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+// calls f(save kernel, shift kernel) instantiated for slot size S
 template <typename F>
-adha_status launch_cycles(uint32_t S, int blocks, cudaStream_t st, F&& f) {
+adha_status with_cycle_kernels(uint32_t S, F&& f) {
     switch (S) {
         case 256: f(ipdev::ip_cycle_save_kernel<256>, ipdev::ip_cycle_shift_kernel<256>); break;
         case 512: f(ipdev::ip_cycle_save_kernel<512>, ipdev::ip_cycle_shift_kernel<512>); break;
@@ -354,8 +355,6 @@ adha_status launch_cycles(uint32_t S, int blocks, cudaStream_t st, F&& f) {
         case 4096: f(ipdev::ip_cycle_save_kernel<4096>, ipdev::ip_cycle_shift_kernel<4096>); break;
         default: return fail(ADHA_ERR_UNSUPPORTED, "slot size");
     }
-    (void)blocks;
-    (void)st;
     return ADHA_OK;
 }
 
@@ -376,7 +375,7 @@ adha_status smem_optin(int dev, const void* fn) {
 }
 
 adha_status launch_tiles(const InplacePlan& P, uint8_t* buf, const uint8_t* ws, bool post, int dev, int sms,
-                             cudaStream_t st) {
+                         cudaStream_t st) {
     const auto& v = post ? P.post : P.pre;
     if (v.empty() || P.m == 0) return ADHA_OK;
     const IpPiece* tab = reinterpret_cast<const IpPiece*>(ws + P.ws_pieces) + (post ? P.pre.size() : 0);
@@ -505,7 +504,7 @@ extern "C" adha_status adha_remap_inplace(void* buf, uint64_t buf_bytes, const a
         const uint32_t* seq = reinterpret_cast<const uint32_t*>(ws + P.ws_seq);
         const IpSeg* segs = reinterpret_cast<const IpSeg*>(ws + P.ws_segs);
         uint8_t* save = ws + P.ws_save;
-        s = launch_cycles(P.S, (int)grid, st, [&](auto save_k, auto shift_k) {
+        s = with_cycle_kernels(P.S, [&](auto save_k, auto shift_k) {
             save_k<<<grid, 256, 0, st>>>(b, seq, segs, nseg, save);
             shift_k<<<grid, 256, 0, st>>>(b, seq, segs, nseg, save);
         });
