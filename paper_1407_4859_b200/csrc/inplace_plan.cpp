@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cstring>
 #include <string>
+#include <thread>
 
 #include "inplace_plan.h"
 
@@ -139,6 +140,111 @@ uint64_t add_cluster(const Layout& l, int32_t c, uint64_t base, uint32_t atom, u
     return (std::max<uint64_t>((uint64_t)g * pc.TS * atom, (uint64_t)g * T * (l.stride[c] + 4)) + 15) & ~15ull;
 }
 
+constexpr uint32_t NONE_SLOT = 0xFFFFFFFFu;
+
+unsigned plan_threads(uint64_t work) {
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>({(uint64_t)hw, 32, work / (1u << 16)}));
+}
+
+// f(chunk, begin, end) over [0, n) split evenly into nthr chunks, chunk i on thread i
+template <typename F>
+void parallel_for(unsigned nthr, uint64_t n, F&& f) {
+    if (nthr <= 1) { f(0u, (uint64_t)0, n); return; }
+    std::vector<std::thread> th;
+    for (unsigned i = 0; i < nthr; ++i)
+        th.emplace_back([&, i] { f(i, n * i / nthr, n * (i + 1) / nthr); });
+    for (auto& t : th) t.join();
+}
+
+inline bool is_cut(uint32_t x) {   // pseudo-random 1-in-512 cut points along the cycles
+    uint32_t h = x * 0x9E3779B1u;
+    h ^= h >> 15;
+    h *= 0x85EBCA77u;
+    h ^= h >> 13;
+    return (h & 511u) == 0;
+}
+
+// The permutation's cycles as segments of at most IP_SEG positions.  Cycles are cut at pseudo-
+// random cut points; the walks from the cut points are independent (one per thread chunk, so the
+// random accesses of many walks overlap); cycles without a cut point are walked afterwards.
+// Fixed points are dropped.  P is consumed (entries set to NONE_SLOT as they are placed).
+void build_segments(std::vector<uint32_t>& P, uint64_t nslot, unsigned nthr, InplacePlan* p) {
+    std::vector<uint32_t> cuts;
+    for (uint64_t x = 0; x < nslot; ++x) {
+        if (P[x] == NONE_SLOT) continue;
+        if (P[x] == (uint32_t)x) { P[x] = NONE_SLOT; ++p->fixed_slots; continue; }
+        if (is_cut((uint32_t)x)) cuts.push_back((uint32_t)x);
+    }
+    // walk from every cut point up to (not including) the next cut point on its cycle
+    struct Walk { std::vector<uint32_t> pos; std::vector<uint32_t> len; std::vector<uint32_t> next_cut; };
+    const unsigned nw = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(nthr, cuts.size()));
+    std::vector<Walk> walks(nw);
+    parallel_for(nw, cuts.size(), [&](unsigned chunk, uint64_t i0, uint64_t i1) {
+        Walk& w = walks[chunk];
+        for (uint64_t i = i0; i < i1; ++i) {
+            uint32_t y = cuts[i];
+            uint32_t L = 0;
+            do {
+                w.pos.push_back(y);
+                ++L;
+                y = P[y];
+            } while (!is_cut(y));
+            w.len.push_back(L);
+            w.next_cut.push_back(y);
+        }
+    });
+    for (const Walk& w : walks)
+        for (uint32_t y : w.pos) P[y] = NONE_SLOT;        // placed
+    // concatenate in cut order; split long walks into segments of <= IP_SEG
+    std::vector<uint32_t> first_seg(cuts.size()), last_seg(cuts.size());
+    p->seq.reserve(p->content_slots + p->junk_slots);
+    size_t ci = 0;
+    for (const Walk& w : walks) {
+        size_t off = 0;
+        for (size_t k = 0; k < w.len.size(); ++k, ++ci) {
+            const uint32_t L = w.len[k];
+            const uint32_t start = (uint32_t)p->seq.size();
+            p->seq.insert(p->seq.end(), w.pos.begin() + off, w.pos.begin() + off + L);
+            off += L;
+            first_seg[ci] = (uint32_t)p->segs.size();
+            for (uint32_t a = 0; a < L; a += IP_SEG) {
+                const uint32_t sidx = (uint32_t)p->segs.size();
+                p->segs.push_back({start + a, std::min<uint32_t>(IP_SEG, L - a), a ? sidx - 1 : 0u, 0});
+            }
+            last_seg[ci] = (uint32_t)p->segs.size() - 1;
+        }
+    }
+    // the first segment of cut i's walk receives the last slot of the walk that reaches cut i
+    ci = 0;
+    for (const Walk& w : walks)
+        for (size_t k = 0; k < w.len.size(); ++k, ++ci) {
+            const size_t nxt = (size_t)(std::lower_bound(cuts.begin(), cuts.end(), w.next_cut[k]) - cuts.begin());
+            p->segs[first_seg[nxt]].pred = last_seg[ci];
+        }
+    p->cycles = 0;   // cut walks do not count cycles; the uncut ones below do
+    // cycles with no cut point
+    for (uint64_t x0 = 0; x0 < nslot; ++x0) {
+        if (P[x0] == NONE_SLOT) continue;
+        const uint32_t start = (uint32_t)p->seq.size();
+        uint64_t y = x0;
+        do {
+            p->seq.push_back((uint32_t)y);
+            const uint32_t ny = P[y];
+            P[y] = NONE_SLOT;
+            y = ny;
+        } while (y != x0);
+        const uint32_t L = (uint32_t)p->seq.size() - start;
+        const uint32_t first = (uint32_t)p->segs.size();
+        const uint32_t ns = (L + IP_SEG - 1) / IP_SEG;
+        for (uint32_t s = 0; s < ns; ++s) {
+            const uint32_t a = start + s * IP_SEG;
+            p->segs.push_back({a, std::min<uint32_t>(IP_SEG, start + L - a), s == 0 ? first + ns - 1 : first + s - 1, 0});
+        }
+        ++p->cycles;
+    }
+}
+
 }  // namespace
 
 adha_status inplace_plan_build(const Layout& ls, const Layout& ld, int64_t n, InplacePlan* p) {
@@ -227,37 +333,49 @@ adha_status inplace_plan_build(const Layout& ls, const Layout& ld, int64_t n, In
     const uint64_t total = std::max(p->bytes_s, p->bytes_d);
     const uint64_t nslot = (total + S - 1) / S;
     if (nslot >= 0xFFFFFFFFull) return fail(ADHA_ERR_TOO_LARGE, "in-place remap: more than 2^32 slots");
-    constexpr uint32_t NONE = 0xFFFFFFFFu;
+    constexpr uint32_t NONE = NONE_SLOT;
     std::vector<uint32_t> P;
     std::vector<uint8_t> in_d;
     p->seq.clear();
     p->segs.clear();
     p->content_slots = p->moved_slots = p->fixed_slots = p->junk_slots = p->cycles = 0;
     if (m > 0) {
+        const unsigned nthr = plan_threads(nslot);
         P.assign(nslot, NONE);
         in_d.assign(nslot, 0);
+        // per src cluster, per unit column k: slots s0 + t*K + k (t < m) -> d0 + t*Kd (+ k when raw)
+        struct Col { uint64_t s0, d0; uint32_t K, Kd, k; bool raw; };
+        std::vector<Col> colv;
         for (int32_t c = 0; c < Cs; ++c) {
             const uint32_t K = (uint32_t)(ls.stride[c] / u);
             const uint64_t s0 = p->bs[c] / S;
-            if (twin_s[c] >= 0) {                         // raw slots of an unchanged cluster
-                const uint64_t d0 = p->bd[twin_s[c]] / S;
-                for (uint64_t t = 0; t < m; ++t)
-                    for (uint32_t k = 0; k < K; ++k) P[s0 + t * K + k] = (uint32_t)(d0 + t * K + k);
-                continue;
-            }
-            // unit-column k of the (transposed) tile: field f, unit q of it
             for (uint32_t k = 0; k < K; ++k) {
+                if (twin_s[c] >= 0) {                     // raw slots of an unchanged cluster
+                    colv.push_back({s0, p->bd[twin_s[c]] / S, K, K, k, true});
+                    continue;
+                }
+                // unit column k of the field-blocked tile: field f, unit q of it
                 const int32_t f = field_at(ls, c, k * u);
                 const uint32_t q = (k * u - ls.offset[f]) / u;
                 const int32_t cd = ld.cluster[f];
-                const uint32_t Kd = (uint32_t)(ld.stride[cd] / u);
-                const uint64_t d0 = p->bd[cd] / S + ld.offset[f] / u + q;
-                for (uint64_t t = 0; t < m; ++t) P[s0 + t * K + k] = (uint32_t)(d0 + t * Kd);
+                colv.push_back({s0, p->bd[cd] / S + ld.offset[f] / u + q, K, (uint32_t)(ld.stride[cd] / u), k, false});
             }
         }
+        parallel_for(nthr, m, [&](unsigned, uint64_t t0, uint64_t t1) {
+            for (const Col& cv : colv)
+                for (uint64_t t = t0; t < t1; ++t)
+                    P[cv.s0 + t * cv.K + cv.k] = (uint32_t)(cv.d0 + t * cv.Kd + (cv.raw ? cv.k : 0));
+        });
+        // P is injective, so the in_d writes of different threads never collide
+        std::vector<uint64_t> cnt(nthr, 0);
+        parallel_for(nthr, nslot, [&](unsigned chunk, uint64_t x0, uint64_t x1) {
+            uint64_t k = 0;
+            for (uint64_t x = x0; x < x1; ++x)
+                if (P[x] != NONE) { in_d[P[x]] = 1; ++k; }
+            cnt[chunk] = k;
+        });
+        for (uint64_t k : cnt) p->content_slots += k;
         std::vector<uint32_t> free_in, free_out;   // dst-only slots, src-only slots
-        for (uint64_t x = 0; x < nslot; ++x)
-            if (P[x] != NONE) { in_d[P[x]] = 1; ++p->content_slots; }
         for (uint64_t x = 0; x < nslot; ++x) {
             const bool ins = P[x] != NONE;
             if (in_d[x] && !ins) free_in.push_back((uint32_t)x);
@@ -268,28 +386,7 @@ adha_status inplace_plan_build(const Layout& ls, const Layout& ld, int64_t n, In
         // to a src-only slot (which becomes dst tail / gap): the permutation closes on U
         for (size_t i = 0; i < free_in.size(); ++i) P[free_in[i]] = free_out[i];
         p->junk_slots = free_in.size();
-        // cycles, split into segments of at most IP_SEG positions
-        for (uint64_t x0 = 0; x0 < nslot; ++x0) {
-            if (P[x0] == NONE) continue;
-            if (P[x0] == (uint32_t)x0) { P[x0] = NONE; ++p->fixed_slots; continue; }
-            const uint32_t start = (uint32_t)p->seq.size();
-            uint64_t y = x0;
-            do {
-                p->seq.push_back((uint32_t)y);
-                const uint32_t ny = P[y];
-                P[y] = NONE;
-                y = ny;
-            } while (y != x0);
-            const uint32_t L = (uint32_t)p->seq.size() - start;
-            const uint32_t first = (uint32_t)p->segs.size();
-            const uint32_t ns = (L + IP_SEG - 1) / IP_SEG;
-            for (uint32_t s = 0; s < ns; ++s) {
-                const uint32_t a = start + s * IP_SEG;
-                const uint32_t len = std::min<uint32_t>(IP_SEG, start + L - a);
-                p->segs.push_back({a, len, s == 0 ? first + ns - 1 : first + s - 1, 0});
-            }
-            ++p->cycles;
-        }
+        build_segments(P, nslot, nthr, p);
         p->moved_slots = p->seq.size();
         if (p->seq.size() >= 0xFFFFFFFFull) return fail(ADHA_ERR_TOO_LARGE, "in-place remap: too many slots");
     }
