@@ -77,3 +77,10 @@ def test_bench_inplace_contract(cfg):
     assert c["buffer_bytes_per_rank"] < c["out_of_place_buffers_bytes_per_rank"]
     assert 0 < d["roofline"]["frac"] < 1.2 and d["gpu_launches"] > 0
     assert d["e2e"]["value"] > 0
+
+
+def test_bench_inplace_two_ranks_share_gpu():
+    d = run_bench(["--inplace", "--gpus", "2", "--steps", "4", "--warmup", "3", "--no-e2e"],
+                  env={"ADHA_BENCH_SHARE_GPU": "1"}, torchrun=2)
+    assert d["n_gpus"] == 2 and d["impl"] == "adha-inplace"
+    assert d["config"]["n_records_total"] == 2 * d["config"]["n_records_per_rank"]

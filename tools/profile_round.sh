@@ -23,3 +23,13 @@ for c in C2 C3 C4 C5 P1 P2; do
         python bench.py --config $c --steps 2 --warmup 1 --soak-s 0 --no-cpu-baseline --no-e2e --no-copy-ref > $out/ncu_full_${tag}_$c.log 2>&1
   echo "ncu full $c=$?"
 done
+# in-place remap (adha_remap_inplace): bench lines per config and one ncu --set full capture of
+# C2's in-place kernels (each after the same command exited 0 without ncu)
+for c in C2 C3 C4 P1 P2; do
+  python bench.py --inplace --config $c > $out/bench_${tag}_inplace_$c.json 2> $out/bench_${tag}_inplace_$c.err; echo "bench inplace $c=$?"
+done
+python tools/inplace_probe.py > $out/inplace_probe_$tag.log 2>&1; echo "inplace probe=$?"
+python tools/inplace_probe.py --reps 2 --no-oop --cases C2 > $out/plain_ip_$tag.log 2>&1 && \
+  ncu --set full --clock-control none --import-source on -k regex:ip_ -c 12 -o $out/prof_${tag}_inplace \
+      python tools/inplace_probe.py --reps 2 --no-oop --cases C2 > $out/ncu_ip_$tag.log 2>&1
+echo "ncu inplace=$?"
