@@ -24,17 +24,23 @@ def export(rep, page):
 
 def main():
     tag = sys.argv[1]
-    cfgs = sys.argv[2:] or [c for c in ALGO
-                            if os.path.exists(os.path.join(ROOT, "gpurun_out", f"prof_{tag}_{c}.ncu-rep"))]
+    def have(c):
+        return any(os.path.exists(os.path.join(ROOT, "gpurun_out", f)) for f in
+                   (f"prof_{tag}_{c}.ncu-rep", f"prof_{tag}_{c}_raw.csv"))
+    cfgs = sys.argv[2:] or [c for c in ALGO if have(c)]
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     table = json.load(open(path)) if os.path.exists(path) else {}
     for cfg in cfgs:
         rep = os.path.join(ROOT, "gpurun_out", f"prof_{tag}_{cfg}.ncu-rep")
-        raw = export(rep, "raw")
+        if os.path.exists(rep):
+            raw, details = export(rep, "raw"), export(rep, "details")
+        else:   # exported on the GPU box (profile_round.sh), the report itself not brought back
+            base = os.path.join(ROOT, "gpurun_out", f"prof_{tag}_{cfg}")
+            raw, details = open(base + "_raw.csv").read(), open(base + "_details.csv").read()
         with open(os.path.join(ROOT, "profiles", f"{tag}_ncu_full_{cfg}_raw.csv"), "w") as f:
             f.write(raw)
         with open(os.path.join(ROOT, "profiles", f"{tag}_ncu_full_{cfg}_details.csv"), "w") as f:
-            f.write(export(rep, "details"))
+            f.write(details)
         rows = list(csv.reader(raw.splitlines()))
         hdr, units, vals = rows[0], rows[1], rows[2]
 

@@ -22,6 +22,12 @@ for c in C2 C3 C4 C5 P1 P2; do
     ncu --set full --clock-control none --import-source on -k regex:remap_tiled -s 3 -c 1 -o $out/prof_${tag}_$c \
         python bench.py --config $c --steps 2 --warmup 1 --soak-s 0 --no-cpu-baseline --no-e2e --no-copy-ref > $out/ncu_full_${tag}_$c.log 2>&1
   echo "ncu full $c=$?"
+  # export on the box and drop the report: gpurun brings back at most 64 MiB
+  if [ -f $out/prof_${tag}_$c.ncu-rep ]; then
+    ncu -i $out/prof_${tag}_$c.ncu-rep --page raw --csv > $out/prof_${tag}_${c}_raw.csv 2>/dev/null
+    ncu -i $out/prof_${tag}_$c.ncu-rep --page details --csv > $out/prof_${tag}_${c}_details.csv 2>/dev/null
+    rm -f $out/prof_${tag}_$c.ncu-rep
+  fi
 done
 # in-place remap (adha_remap_inplace): bench lines per config and one ncu --set full capture of
 # C2's in-place kernels (each after the same command exited 0 without ncu)
@@ -33,3 +39,8 @@ python tools/inplace_probe.py --reps 2 --no-oop --cases C2 > $out/plain_ip_$tag.
   ncu --set full --clock-control none --import-source on -k regex:ip_ -c 12 -o $out/prof_${tag}_inplace \
       python tools/inplace_probe.py --reps 2 --no-oop --cases C2 > $out/ncu_ip_$tag.log 2>&1
 echo "ncu inplace=$?"
+if [ -f $out/prof_${tag}_inplace.ncu-rep ]; then
+  ncu -i $out/prof_${tag}_inplace.ncu-rep --page raw --csv > $out/prof_${tag}_inplace_raw.csv 2>/dev/null
+  rm -f $out/prof_${tag}_inplace.ncu-rep
+fi
+du -sh $out
