@@ -61,6 +61,30 @@ def main():
             "source": f"profiles/{tag}_ncu_full_{cfg}_raw.csv (ncu --set full --clock-control none, one launch)",
         }
         print(cfg, json.dumps(table[cfg]))
+    # in-place C2 (profile_round.sh: ncu of tools/inplace_probe.py --cases C2, both directions):
+    # dram bytes of all in-place kernels per step, averaged over the captured steps
+    ip = os.path.join(ROOT, "gpurun_out", f"prof_{tag}_inplace_raw.csv")
+    if os.path.exists(ip):
+        raw = open(ip).read()
+        with open(os.path.join(ROOT, "profiles", f"{tag}_ncu_full_inplace_raw.csv"), "w") as f:
+            f.write(raw)
+        rows = list(csv.reader(raw.splitlines()))
+        hdr, units = rows[0], rows[1]
+        tot, t_s, steps = 0.0, 0.0, 0
+        for vals in rows[2:]:
+            def g(k):
+                i = hdr.index(k)
+                return float(vals[i].replace(",", "")) * SCALE.get(units[i], 1.0)
+            tot += g("dram__bytes_read.sum") + g("dram__bytes_write.sum")
+            t_s += g("gpu__time_duration.sum")
+            steps += "ip_cycle_shift" in vals[hdr.index("Kernel Name")]
+        if steps:
+            table["C2_inplace"] = {"kernels": "ip_tile_kernel + ip_cycle_save_kernel + ip_cycle_shift_kernel",
+                                   "dram_bytes_per_launch": tot / steps, "gpu_time_s_per_step": t_s / steps,
+                                   "steps_captured": steps, "algorithmic_remap_bytes_per_step": ALGO["C2"],
+                                   "source": f"profiles/{tag}_ncu_full_inplace_raw.csv (ncu --set full, C2 in place "
+                                             "both directions)"}
+            print("C2_inplace", json.dumps(table["C2_inplace"]))
     with open(path, "w") as f:
         json.dump(table, f, indent=1)
 
