@@ -59,6 +59,12 @@ __device__ __forceinline__ uint32_t fdiv(uint32_t n, uint32_t magic) { return ma
 #ifndef IP_LB
 #define IP_LB 2
 #endif
+#ifndef IP_SKEW
+#define IP_SKEW 1
+#endif
+#ifndef IP_SKEW_ST
+#define IP_SKEW_ST 0
+#endif
 
 template <typename Atom, bool GROUPED>
 __device__ __forceinline__ void ip_scatter(Atom* sa, const uint4 x, uint32_t v, int to_blocks, uint32_t lgT,
@@ -70,8 +76,23 @@ __device__ __forceinline__ void ip_scatter(Atom* sa, const uint4 x, uint32_t v, 
                        // across the tiles of a piece
         const uint32_t w4[4] = {x.x, x.y, x.z, x.w};
         if (sizeof(Atom) == 4) {
+#if IP_SKEW_ST
+            // lanes 8g..8g+7 store their 4 words starting at word g (rotated in registers first), so
+            // the 32 lanes of each store hit different banks
+            const uint32_t k = (threadIdx.x >> 3) & 3;
+            const bool r1 = k & 1, r2 = k & 2;
+            const uint32_t t0 = r1 ? w4[1] : w4[0], t1 = r1 ? w4[2] : w4[1], t2 = r1 ? w4[3] : w4[2],
+                           t3 = r1 ? w4[0] : w4[3];
+            const uint32_t v[4] = {r2 ? t2 : t0, r2 ? t3 : t1, r2 ? t0 : t2, r2 ? t1 : t3};   // v[j] = w4[(j+k)&3]
+#pragma unroll
+            for (uint32_t j = 0; j < 4; ++j) {
+                const uint32_t i = i0 + ((j + k) & 3);
+                sa[i + fdiv(i, pc.magic_RA) * padR] = (Atom)v[j];
+            }
+#else
 #pragma unroll
             for (uint32_t j = 0; j < 4; ++j) sa[i0 + j + fdiv(i0 + j, pc.magic_RA) * padR] = (Atom)w4[j];
+#endif
         } else {
             const uint32_t r0 = fdiv(i0, pc.magic_RA);
             uint32_t o = i0 + r0 * padR, rr = i0 - r0 * RA;
@@ -108,8 +129,23 @@ __device__ __forceinline__ uint4 ip_gather(const Atom* sa, uint32_t v, int to_bl
         const uint32_t rq = q << lgT;                  // first record row of tile q
         if (sizeof(Atom) == 4 && e.a == 1) {          // 4 consecutive records of one column
             const uint32_t a0 = (rq + local0) * P + col;
+#if IP_SKEW
+            // lanes 8g..8g+7 read their 4 rows starting at row g: with an odd pitch the 32 lanes of
+            // each read then hit 32 different banks; the values are rotated back in registers
+            const uint32_t k = (threadIdx.x >> 3) & 3;
+            uint32_t v[4];
+#pragma unroll
+            for (uint32_t j = 0; j < 4; ++j) v[j] = (uint32_t)sa[a0 + ((j + k) & 3) * P];
+            const bool r1 = k & 1, r2 = k & 2;
+            const uint32_t t0 = r1 ? v[3] : v[0], t1 = r1 ? v[0] : v[1], t2 = r1 ? v[1] : v[2], t3 = r1 ? v[2] : v[3];
+            w4[0] = r2 ? t2 : t0;
+            w4[1] = r2 ? t3 : t1;
+            w4[2] = r2 ? t0 : t2;
+            w4[3] = r2 ? t1 : t3;
+#else
 #pragma unroll
             for (uint32_t j = 0; j < 4; ++j) w4[j] = (uint32_t)sa[a0 + j * P];
+#endif
         } else if (sizeof(Atom) == 4 && e.a == 2) {   // 2 records x 2 atoms
             const uint32_t a0 = (rq + (local0 >> 1)) * P + col;
             w4[0] = (uint32_t)sa[a0];
