@@ -33,6 +33,8 @@ CONFIGS = {
     "C1": ("3-field float record (x,y,z), 1024 records, AoS->SoA->AoS", "xyz", 1024, "weak"),
     "C2": ("16-field mixed 4/8-byte record, 10M records, AoS->SoA", "c2", 10_000_000, "weak"),
     "C3": ("64-field record, SoA->ODS hybrid (128-byte cluster cap), 50M records", "c3", 50_000_000, "weak"),
+    "C3R": ("64-field record, SoA->ODS hybrid of the seeded random program (SURVEY 8(d)), 50M records", "c3r",
+            50_000_000, "weak"),
     "C4": ("Medical 9x fp32, PDL chain AoS->AoSV->SoA->AoS over 2 GiB of records", "c4", (2 ** 31) // 36, "weak"),
     "C5": ("8 GiB mixed-width record array AoS->SoA, sharded across GPUs", "c2", (2 ** 33) // 80, "strong"),
     "P1": ("Medical 256^3 voxels x 9 fp32: AoS->AoSV->SoA", "p1", 256 ** 3, "weak"),
@@ -46,9 +48,9 @@ def golden(name):
         return json.load(fh)
 
 
-def c3_labels():
+def c3_labels(program="c3_program.json", section="c3"):
     import paper_1407_4859_b200 as A
-    layout = A.plan_ods(golden("c3_program.json"), golden("b200_arch.json"), "c3", "b200")
+    layout = A.plan_ods(golden(program), golden("b200_arch.json"), section, "b200")
     names = [f"f{i}" for i in range(64)]
     from adha_inputs import config_widths
     return A.Layout.from_string(layout, names, config_widths(64)).cluster_of, layout
@@ -65,6 +67,9 @@ def chain_for(kind):
     if kind == "c3":
         w = config_widths(64)
         return w, [list(range(64)), c3_labels()[0]]
+    if kind == "c3r":      # the seeded random program variant (tests/golden/c3_random_program.json)
+        w = config_widths(64)
+        return w, [list(range(64)), c3_labels("c3_random_program.json", "c3r")[0]]
     if kind == "c4":
         return [4] * 9, [[0] * 9, [0, 0, 0, 1, 2, 3, 4, 5, 6], list(range(9)), [0] * 9]
     if kind == "p1":
@@ -410,7 +415,8 @@ def run_inplace(args, rank, world, local, share):
                 "parallelism": f"shard by contiguous record range over {world} GPU(s), no data-path collective",
             },
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": None, "peak_source": peak_src,
+                         "traffic": ncu_traffic(name + "_inplace"), "traffic_unit": "bytes per step (ncu, all in-place kernels)",
+                         "peak_source": peak_src,
                          "kernel": "whole in-place step (ip_tile_kernel + ip_cycle kernels), plan traffic_bytes",
                          "algorithmic_bytes_per_step": traffic_rank / args.steps, "avg_step_ms": ms_total / args.steps},
             "gpu_launches": n_launch, "clocks": clk, "e2e": e2e, "cpu_baseline": None,

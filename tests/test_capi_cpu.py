@@ -153,6 +153,9 @@ def test_cpp_ods_fixtures(expected):
     assert A.plan_ods(km, t3, "k1", "gpu") == expected["kmeans_coalescing_soa"]["value"]
     assert A.plan_ods(golden("c3_program.json"), golden("b200_arch.json"), "c3", "b200") == \
         expected["c3_hybrid"]["value"]
+    # SURVEY.md 8(d) random program variant: the C++ planner gives the oracle's layout
+    assert A.plan_ods(golden("c3_random_program.json"), golden("b200_arch.json"), "c3r", "b200") == \
+        golden("c3_random_expected.json")["c3_random_hybrid"]["value"]
 
 
 def test_cpp_pdl_fixtures(expected):

@@ -208,13 +208,15 @@ def test_c2_full_size_in_place_every_payload_byte():
     assert np.array_equal(got[mask], exp[mask])
 
 
-def test_c3_shape_in_place_sampled():
-    """C3's remap (64 SoA fields -> the 24-cluster ODS hybrid) in place at 5M records, sampled
-    records compared through the oracle's address model."""
-    from tests.test_gpu_parity import c3_labels
+@pytest.mark.parametrize("variant", ["structured", "random"])
+def test_c3_shape_in_place_sampled(variant):
+    """C3's remap (64 SoA fields -> the ODS hybrid of the structured program, or of the seeded
+    random program variant) in place at 5M records, sampled records compared through the
+    oracle's address model."""
+    from tests.test_gpu_parity import c3_labels, c3r_labels
     from tests.gpu_util import sample_records, gather_fields_dev
     widths, n = config_widths(64), 5_000_003
-    ls, ld = list(range(64)), c3_labels()
+    ls, ld = list(range(64)), (c3_labels() if variant == "structured" else c3r_labels())
     Ls, Ld = A.Layout(widths, ls), A.Layout(widths, ld)
     plan = A.InplacePlan(Ls, Ld, n)
     buf = torch.empty(plan.buffer_bytes, dtype=torch.uint8, device="cuda")

@@ -102,6 +102,18 @@ def c3_labels():
     return lab
 
 
+def c3r_labels():
+    """The oracle's layout of the seeded random C3 program (tests/golden/c3_random_expected.json)."""
+    from oracle import planner as P
+    from tests.conftest import golden
+    hyb = P.parse_layout(golden("c3_random_expected.json")["c3_random_hybrid"]["value"], {f"f{i}": i for i in range(64)})
+    lab = [0] * 64
+    for c, cl in enumerate(hyb):
+        for nm in cl:
+            lab[int(nm[1:])] = c
+    return lab
+
+
 AOSV = [0, 0, 0, 1, 2, 3, 4, 5, 6]
 
 
@@ -110,6 +122,8 @@ AOSV = [0, 0, 0, 1, 2, 3, 4, 5, 6]
     ("C2-back", config_widths(16), list(range(16)), [0] * 16),
     ("C3", config_widths(64), list(range(64)), c3_labels()),
     ("C3-back", config_widths(64), c3_labels(), list(range(64))),
+    ("C3R", config_widths(64), list(range(64)), c3r_labels()),
+    ("C3R-back", config_widths(64), c3r_labels(), list(range(64))),
     ("C4-aos-aosv", [4] * 9, [0] * 9, AOSV),
     ("C4-aosv-soa", [4] * 9, AOSV, list(range(9))),
     ("C4-soa-aos", [4] * 9, list(range(9)), [0] * 9),

@@ -97,6 +97,36 @@ def test_c3_structured_program_hybrid(expected):
     assert [P.cluster_bytes(c, eb) for c in l] == e["strides"]
 
 
+def test_c3_random_program_variant():
+    """the seeded random variant of C3's program (tools/make_c3_random_program.py,
+    seed 14074859, 24 groups of 2-10 fields, freq 1..4, 70 % irregular).  The stored layout is the
+    oracle's own output (regression pin); what pins it to the method are ODS's invariants
+    (SPEC.md:161-166): a partition of the 64 fields, every cluster within the 128-byte capacity,
+    every multi-field cluster held together by positive affinity, canonical order."""
+    p, a, _ = load("c3_random_program.json", "b200_arch.json")
+    d = a.device("b200")
+    l = P.ods(p.sections[0], d, p)
+    e = golden("c3_random_expected.json")["c3_random_hybrid"]
+    assert P.layout_string(l) == e["value"] and len(l) == e["n_clusters"]
+    eb = p.elem_bytes()
+    names = sorted((f.name for f in p.fields), key=lambda n: int(n[1:]))
+    assert sorted(n for c in l for n in c) == sorted(names)
+    assert all(P.cluster_bytes(c, eb) <= d.cluster_capacity_bytes for c in l)
+    decl = {f.name: f.decl_index for f in p.fields}
+    _, w = P.build_affinity_graph(p.sections[0], d, decl)
+    for c in l:
+        if len(c) > 1:     # connected through positive edges inside the cluster
+            seen, todo = {c[0]}, [c[0]]
+            while todo:
+                x = todo.pop()
+                for y in c:
+                    if y not in seen and w.get((min(x, y, key=decl.get), max(x, y, key=decl.get)), 0) > 0:
+                        seen.add(y)
+                        todo.append(y)
+            assert seen == set(c), c
+    assert [min(decl[n] for n in c) for c in l] == sorted(min(decl[n] for n in c) for c in l)
+
+
 def test_canonical_string_round_trip_and_paper_notation(expected):
     decl = {n: i for i, n in enumerate(["V1", "V2", "V3", "U1", "U2", "U3", "S", "T", "interpT"])}
     paper = "V1,V2,V3,{U1,U2,U3},S,T,interpT"                  # PAPER.md:112 notation

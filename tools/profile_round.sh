@@ -8,7 +8,7 @@ out=gpurun_out
 timeout 900 python -m pytest tests -m gpu -q > $out/pytest_gpu_$tag.log 2>&1; echo "pytest=$?"
 python -c "import __graft_entry__ as g; g.smoke()" > $out/smoke_$tag.log 2>&1; echo "smoke=$?"
 python bench.py > $out/bench_$tag.json 2> $out/bench_$tag.err; echo "bench=$?"
-for c in C1 C3 C4 C5 P1 P2; do
+for c in C1 C3 C3R C4 C5 P1 P2; do
   python bench.py --config $c --no-cpu-baseline > $out/bench_${tag}_$c.json 2> $out/bench_${tag}_$c.err; echo "bench $c=$?"
 done
 python bench.py --impl reference --steps 3 --warmup 1 > $out/bench_${tag}_reference.json 2>&1; echo "reference=$?"
@@ -17,7 +17,7 @@ python bench.py --steps 2 --warmup 1 --soak-s 0 --no-cpu-baseline > $out/plain_$
   ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $out/launches_$tag.csv \
       python bench.py --steps 2 --warmup 1 --soak-s 0 --no-cpu-baseline > $out/ncu_launch_$tag.log 2>&1
 echo "ncu launches=$?"
-for c in C2 C3 C4 C5 P1 P2; do
+for c in C2 C3 C3R C4 C5 P1 P2; do
   python bench.py --config $c --steps 2 --warmup 1 --soak-s 0 --no-cpu-baseline --no-e2e --no-copy-ref > $out/plainf_${tag}_$c.log 2>&1 && \
     ncu --set full --clock-control none --import-source on -k regex:remap_tiled -s 3 -c 1 -o $out/prof_${tag}_$c \
         python bench.py --config $c --steps 2 --warmup 1 --soak-s 0 --no-cpu-baseline --no-e2e --no-copy-ref > $out/ncu_full_${tag}_$c.log 2>&1
@@ -31,7 +31,7 @@ for c in C2 C3 C4 C5 P1 P2; do
 done
 # in-place remap (adha_remap_inplace): bench lines per config and one ncu --set full capture of
 # C2's in-place kernels (each after the same command exited 0 without ncu)
-for c in C2 C3 C4 P1 P2; do
+for c in C2 C3 C3R C4 P1 P2; do
   python bench.py --inplace --config $c > $out/bench_${tag}_inplace_$c.json 2> $out/bench_${tag}_inplace_$c.err; echo "bench inplace $c=$?"
 done
 python tools/inplace_probe.py > $out/inplace_probe_$tag.log 2>&1; echo "inplace probe=$?"
