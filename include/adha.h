@@ -284,7 +284,10 @@ ADHA_API adha_status adha_remap_host(const void* src_host, const adha_layout* sr
  * Usage: plan = create(Ls, Ld, N) [host only]; upload(plan, workspace) once; then
  * adha_remap_inplace(buf, ...) any number of times (each call remaps the buffer's current
  * contents from Ls to Ld).  The workspace (device, 256-byte aligned, plan-sized, see
- * adha_inplace_plan_info) belongs to the plan while it is in use and must not overlap buf. */
+ * adha_inplace_plan_info) belongs to the plan while it is in use and must not overlap buf; it
+ * also holds per-run scratch (saved slots, the tail), so two runs of one plan must not overlap
+ * in time: order them on one stream, or give concurrent runs their own plan and workspace.
+ * adha_inplace_plan_upload is not thread-safe with respect to other calls on the same plan. */
 typedef struct adha_inplace_plan adha_inplace_plan;
 
 /* Host-side plan (slot permutation, its cycles, workspace layout) for an N-record buffer.
