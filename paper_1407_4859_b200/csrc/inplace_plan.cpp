@@ -107,7 +107,14 @@ uint32_t magic(uint32_t d) {   // ceil(2^32 / d); 0 encodes d == 1
     return d <= 1 ? 0u : (uint32_t)(((1ull << 32) + d - 1) / d);
 }
 
-constexpr uint64_t IP_PIECE_TARGET = 16384;   // bytes: small tiles are grouped up to this
+#ifndef IP_PIECE_TARGET_BYTES
+#define IP_PIECE_TARGET_BYTES 16384
+#endif
+#ifndef IP_GROUP_MAX_TILE
+#define IP_GROUP_MAX_TILE 4096
+#endif
+constexpr uint64_t IP_PIECE_TARGET = IP_PIECE_TARGET_BYTES;   // bytes: small tiles are grouped up to this
+constexpr uint64_t IP_GROUP_TILE = IP_GROUP_MAX_TILE;         // bytes: only tiles this small are grouped
 constexpr uint64_t IP_TILE_PREF = 32768;      // bytes: preferred largest rewritten tile
 
 // column table of a cluster record in atoms (word atoms when u % 4 == 0, else bytes); returns the
@@ -116,7 +123,7 @@ uint64_t add_cluster(const Layout& l, int32_t c, uint64_t base, uint32_t atom, u
                      std::vector<IpPiece>& out, std::vector<IpCol>& cols) {
     const uint32_t RA = (uint32_t)(l.stride[c] / atom);
     const uint64_t tile = (uint64_t)T * l.stride[c];
-    const uint32_t g = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(IP_PIECE_TARGET / tile, m));
+    const uint32_t g = tile > IP_GROUP_TILE ? 1u : (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(IP_PIECE_TARGET / tile, m));
     const uint32_t nf = (uint32_t)l.members[c].size();
     IpPiece pc{};
     pc.base = base;
