@@ -27,15 +27,14 @@ bool same_members(const Layout& a, int32_t ca, const Layout& b, int32_t cb) {
     return a.members[ca] == b.members[cb];
 }
 
-// field of cluster c at byte offset o of the cluster record (packed layouts: fields tile the record)
-int32_t field_at(const Layout& l, int32_t c, uint32_t o) {
-    const auto& mem = l.members[c];
-    int32_t lo = 0, hi = (int32_t)mem.size() - 1;
-    while (lo < hi) {   // last member with offset <= o
-        const int32_t mid = (lo + hi + 1) / 2;
-        if (l.offset[mem[mid]] <= o) lo = mid; else hi = mid - 1;
+// block of a cluster record containing byte offset o (blocks sorted by offset, tiling the record)
+const IpBlock& block_at(const std::vector<IpBlock>& blocks, uint32_t o) {
+    size_t lo = 0, hi = blocks.size() - 1;
+    while (lo < hi) {   // last block with offset <= o
+        const size_t mid = (lo + hi + 1) / 2;
+        if (blocks[mid].off <= o) lo = mid; else hi = mid - 1;
     }
-    return mem[lo];
+    return blocks[lo];
 }
 
 // Padding between field blocks of a field-blocked tile in shared memory (atoms per field): chosen
@@ -43,17 +42,17 @@ int32_t field_at(const Layout& l, int32_t c, uint32_t o) {
 // (ip_gather in inplace.cu: thread v builds output vector v, atoms (r, jc) with 4v + j = r*RA + jc,
 // read from bo(jc) + r * a(jc)); candidates are multiples of 16 bytes (the tile is staged with
 // 16-byte shared-memory stores) up to 64 bytes per field block.
-uint32_t choose_padf(const Layout& l, int32_t c, uint32_t T, uint32_t atom) {
-    const uint32_t RA = (uint32_t)(l.stride[c] / atom);
+uint32_t choose_padf(const std::vector<IpBlock>& blocks, uint64_t stride, uint32_t T, uint32_t atom) {
+    const uint32_t RA = (uint32_t)(stride / atom);
     const uint32_t APV = 16 / atom;
     const uint64_t natoms = (uint64_t)T * RA;
     std::vector<uint32_t> col(RA), a(RA), fidx(RA);
     uint32_t fi = 0;
-    for (int32_t f : l.members[c]) {
-        for (uint32_t k = 0; k < l.width[f] / atom; ++k) {
-            const uint32_t j = l.offset[f] / atom + k;
-            col[j] = l.offset[f] / atom;
-            a[j] = l.width[f] / atom;
+    for (const IpBlock& b : blocks) {
+        for (uint32_t k = 0; k < b.width / atom; ++k) {
+            const uint32_t j = b.off / atom + k;
+            col[j] = b.off / atom;
+            a[j] = b.width / atom;
             fidx[j] = fi;
         }
         ++fi;
@@ -119,32 +118,32 @@ constexpr uint64_t IP_TILE_PREF = 32768;      // bytes: preferred largest rewrit
 
 // column table of a cluster record in atoms (word atoms when u % 4 == 0, else bytes); returns the
 // shared memory of one piece (g padded tiles)
-uint64_t add_cluster(const Layout& l, int32_t c, uint64_t base, uint32_t atom, uint32_t T, uint64_t m, uint32_t padf,
-                     std::vector<IpPiece>& out, std::vector<IpCol>& cols) {
-    const uint32_t RA = (uint32_t)(l.stride[c] / atom);
-    const uint64_t tile = (uint64_t)T * l.stride[c];
+uint64_t add_cluster(const std::vector<IpBlock>& blocks, uint64_t stride, uint64_t base, uint32_t atom, uint32_t T,
+                     uint64_t m, uint32_t padf, std::vector<IpPiece>& out, std::vector<IpCol>& cols) {
+    const uint32_t RA = (uint32_t)(stride / atom);
+    const uint64_t tile = (uint64_t)T * stride;
     const uint32_t g = tile > IP_GROUP_TILE ? 1u : (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(IP_PIECE_TARGET / tile, m));
-    const uint32_t nf = (uint32_t)l.members[c].size();
+    const uint32_t nb = (uint32_t)blocks.size();
     IpPiece pc{};
     pc.base = base;
     pc.g = g;
     pc.pieces = (m + g - 1) / g;
-    pc.stride = (uint32_t)l.stride[c];
+    pc.stride = (uint32_t)stride;
     pc.RA = RA;
     pc.col_off = (uint32_t)cols.size();
     pc.magic_RA = magic(RA);
     pc.magic_TRA = magic(T * RA);
-    pc.TS = T * RA + nf * padf;
+    pc.TS = T * RA + nb * padf;
     out.push_back(pc);
-    uint32_t fidx = 0;
-    for (int32_t f : l.members[c]) {
-        const uint32_t col = l.offset[f] / atom, a = l.width[f] / atom;
+    uint32_t bidx = 0;
+    for (const IpBlock& b : blocks) {
+        const uint32_t col = b.off / atom, a = b.width / atom;
         for (uint32_t k = 0; k < a; ++k)
-            cols.push_back({col | ((fidx * padf) << 16), a, magic(a), T * col + fidx * padf + k});
-        ++fidx;
+            cols.push_back({col | ((bidx * padf) << 16), a, magic(a), T * col + bidx * padf + k});
+        ++bidx;
     }
-    // field-blocked: g tiles of TS atoms; record-major: g*T rows with one padding atom (4 bytes) each
-    return (std::max<uint64_t>((uint64_t)g * pc.TS * atom, (uint64_t)g * T * (l.stride[c] + 4)) + 15) & ~15ull;
+    // blocked: g tiles of TS atoms; record-major: g*T rows with one padding atom (4 bytes) each
+    return (std::max<uint64_t>((uint64_t)g * pc.TS * atom, (uint64_t)g * T * (stride + 4)) + 15) & ~15ull;
 }
 
 constexpr uint32_t NONE_SLOT = 0xFFFFFFFFu;
@@ -281,9 +280,32 @@ adha_status inplace_plan_build(const Layout& ls, const Layout& ld, int64_t n, In
         const int32_t cd = ld.cluster[ls.members[c][0]];
         if (same_members(ls, c, ld, cd)) { twin_s[c] = cd; twin_d[cd] = c; }
     }
-    // a single-field cluster's tile is already field-blocked
-    auto transposed_s = [&](int32_t c) { return twin_s[c] < 0 && ls.members[c].size() > 1; };
-    auto transposed_d = [&](int32_t c) { return twin_d[c] < 0 && ld.members[c].size() > 1; };
+    // Runs: maximal sequences of fields that are consecutive in BOTH the src and the dst cluster
+    // record (same cluster pair, same order).  A run is contiguous in both records, so a tile's
+    // BLOCKED form -- each run's T records contiguous -- holds the same bytes for the run on both
+    // sides.  A cluster made of one run is already in blocked form: no tile rewrite for it.
+    std::vector<std::vector<IpBlock>> sblk(Cs), dblk(Cd);
+    std::vector<int32_t> dpos(ls.n_fields);       // position of each field inside its dst cluster
+    for (int32_t c = 0; c < Cd; ++c)
+        for (size_t i = 0; i < ld.members[c].size(); ++i) dpos[ld.members[c][i]] = (int32_t)i;
+    for (int32_t c = 0; c < Cs; ++c) {
+        const auto& mem = ls.members[c];
+        for (size_t i = 0; i < mem.size(); ++i) {
+            const int32_t f = mem[i], cd = ld.cluster[f];
+            const bool cont = i > 0 && ld.cluster[mem[i - 1]] == cd && dpos[mem[i - 1]] + 1 == dpos[f];
+            if (cont) {
+                sblk[c].back().width += ls.width[f];
+            } else {
+                sblk[c].push_back({ls.offset[f], ls.width[f], cd, ld.offset[f]});
+            }
+        }
+    }
+    for (int32_t c = 0; c < Cs; ++c)
+        for (const IpBlock& b : sblk[c]) dblk[b.peer].push_back({b.peer_off, b.width, c, b.off});
+    for (auto& v : dblk)
+        std::sort(v.begin(), v.end(), [](const IpBlock& x, const IpBlock& y) { return x.off < y.off; });
+    auto transposed_s = [&](int32_t c) { return twin_s[c] < 0 && sblk[c].size() > 1; };
+    auto transposed_d = [&](int32_t c) { return twin_d[c] < 0 && dblk[c].size() > 1; };
 
     // slot size: the largest power of two in [256, 4096] dividing every region base whose
     // rewritten tiles stay small (<= IP_TILE_PREF bytes: several CTAs per SM hide the load
@@ -295,14 +317,14 @@ adha_status inplace_plan_build(const Layout& ls, const Layout& ld, int64_t n, In
             for (uint64_t b : p->bs) ok = ok && (b % cand == 0);
             for (uint64_t b : p->bd) ok = ok && (b % cand == 0);
             const uint32_t T = cand / u;
-            auto fits = [&](const Layout& l, int32_t c) {
+            auto fits = [&](const Layout& l, int32_t c, size_t nblocks) {
                 if (pass == 0 && (uint64_t)T * l.stride[c] > IP_TILE_PREF) return false;
-                return smem_need(T, l.stride[c], l.members[c].size(), atom) <= IP_MAX_PIECE;
+                return smem_need(T, l.stride[c], nblocks, atom) <= IP_MAX_PIECE;
             };
             for (int32_t c = 0; ok && c < Cs; ++c)
-                if (transposed_s(c) && !fits(ls, c)) ok = false;
+                if (transposed_s(c) && !fits(ls, c, sblk[c].size())) ok = false;
             for (int32_t c = 0; ok && c < Cd; ++c)
-                if (transposed_d(c) && !fits(ld, c)) ok = false;
+                if (transposed_d(c) && !fits(ld, c, dblk[c].size())) ok = false;
             if (ok) { S = cand; break; }
         }
     }
@@ -323,14 +345,14 @@ adha_status inplace_plan_build(const Layout& ls, const Layout& ld, int64_t n, In
     if (m > 0) {
         for (int32_t c = 0; c < Cs; ++c)
             if (transposed_s(c)) {
-                const uint64_t sm = add_cluster(ls, c, p->bs[c], atom, T, m, 0, p->pre, p->cols);
+                const uint64_t sm = add_cluster(sblk[c], ls.stride[c], p->bs[c], atom, T, m, 0, p->pre, p->cols);
                 p->max_tile = std::max<uint32_t>(p->max_tile, (uint32_t)sm);
                 p->max_tab = std::max<uint32_t>(p->max_tab, (uint32_t)table_smem(ls.stride[c], atom));
             }
         for (int32_t c = 0; c < Cd; ++c)
             if (transposed_d(c)) {
-                const uint32_t padf = choose_padf(ld, c, T, atom);
-                const uint64_t sm = add_cluster(ld, c, p->bd[c], atom, T, m, padf, p->post, p->cols);
+                const uint32_t padf = choose_padf(dblk[c], ld.stride[c], T, atom);
+                const uint64_t sm = add_cluster(dblk[c], ld.stride[c], p->bd[c], atom, T, m, padf, p->post, p->cols);
                 p->max_tile = std::max<uint32_t>(p->max_tile, (uint32_t)sm);
                 p->max_tab = std::max<uint32_t>(p->max_tab, (uint32_t)table_smem(ld.stride[c], atom));
             }
@@ -361,11 +383,11 @@ adha_status inplace_plan_build(const Layout& ls, const Layout& ld, int64_t n, In
                     colv.push_back({s0, p->bd[twin_s[c]] / S, K, K, k, true});
                     continue;
                 }
-                // unit column k of the field-blocked tile: field f, unit q of it
-                const int32_t f = field_at(ls, c, k * u);
-                const uint32_t q = (k * u - ls.offset[f]) / u;
-                const int32_t cd = ld.cluster[f];
-                colv.push_back({s0, p->bd[cd] / S + ld.offset[f] / u + q, K, (uint32_t)(ld.stride[cd] / u), k, false});
+                // slot k of the blocked tile: run b, slot q of its block
+                const IpBlock& b = block_at(sblk[c], k * u);
+                const uint32_t q = (k * u - b.off) / u;
+                const int32_t cd = b.peer;
+                colv.push_back({s0, p->bd[cd] / S + b.peer_off / u + q, K, (uint32_t)(ld.stride[cd] / u), k, false});
             }
         }
         parallel_for(nthr, m, [&](unsigned, uint64_t t0, uint64_t t1) {

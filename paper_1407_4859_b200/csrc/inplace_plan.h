@@ -47,6 +47,13 @@ struct IpCol {          // one atom column j of a cluster record
                         // T * col + padding before the block + (j - col); record r adds r * a
 };
 
+struct IpBlock {        // a run of fields contiguous in both the src and the dst cluster record
+    uint32_t off;       // byte offset of the run in this side's cluster record
+    uint32_t width;     // bytes of the run
+    int32_t peer;       // the other side's cluster
+    uint32_t peer_off;  // byte offset of the run in the other side's cluster record
+};
+
 struct IpTailField {    // one field of the tail records: src/dst element address terms
     uint64_t src;       // base_s(c) + offset_s(f)
     uint64_t dst;       // base_d(c') + offset_d(f)
