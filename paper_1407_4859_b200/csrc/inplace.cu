@@ -4,10 +4,10 @@
 //
 // Plan (inplace_plan.cpp): S-byte slots, T = S / u records per tile.  Launches, in order:
 //   ip_tail_kernel (save)         the last N mod T records -> workspace, packed
-//   ip_tile_kernel (step 1)       src tiles of changed multi-field clusters: record-major -> field-blocked
+//   ip_tile_kernel (step 1)       src tiles of changed clusters of several runs: record-major -> blocked
 //   ip_cycle_save_kernel          the last slot of every cycle segment -> workspace
 //   ip_cycle_shift_kernel         every slot moves one step along its cycle
-//   ip_tile_kernel (step 3)       dst tiles of changed multi-field clusters: field-blocked -> record-major
+//   ip_tile_kernel (step 3)       dst tiles of changed clusters of several runs: blocked -> record-major
 //   ip_tail_kernel (restore)      the tail records -> their dst addresses
 // Type-blind byte moves throughout (reading Q6): no floating-point instruction.
 #include <cuda_runtime.h>
@@ -47,9 +47,10 @@ __global__ void ip_tail_kernel(uint8_t* __restrict__ buf, const IpTailField* __r
 __device__ __forceinline__ uint32_t fdiv(uint32_t n, uint32_t magic) { return magic ? __umulhi(n, magic) : n; }
 
 // One tile of cluster c (T records, RA atoms per record, T * stride bytes at base + t*T*stride)
-// is rewritten in place between record-major form (atom (r, j) at r * RA + j) and field-blocked
-// form (field f's T * a_f atoms contiguous from T * col_f, record r's atoms at r * a_f).
-// to_blocks: record-major -> field-blocked (step 1); else field-blocked -> record-major (step 3).
+// is rewritten in place between record-major form (atom (r, j) at r * RA + j) and blocked form
+// (run b's T * a_b atoms contiguous from T * col_b, record r's atoms at r * a_b; a run is a field
+// or several fields contiguous in both records, inplace_plan.h; the kernel calls runs "fields").
+// to_blocks: record-major -> blocked (step 1); else blocked -> record-major (step 3).
 // The tile is staged in shared memory with padding (one atom per record row, or per field
 // block) so that the gather along the other major is (nearly) bank-conflict free, then written
 // back with coalesced 16-byte stores.  Atom = 32-bit word when u % 4 == 0, else one byte.

@@ -3,17 +3,17 @@
 //
 // The buffer is cut into slots of S bytes (S a power of two in [256, 4096] dividing every
 // region base of both layouts).  A tile of T = S / u records (u = the largest power of two
-// <= 16 dividing every field width) of a cluster with stride s occupies s / u slots.  In the
-// tile's FIELD-BLOCKED form (AoSoA with block T) field f's T values are contiguous, T * w_f
-// bytes = w_f / u whole slots, each holding S / w_f consecutive records of f:
-//   step 1  (tile-local) each src tile of a multi-field cluster that changes is rewritten in
-//           place from record-major to field-blocked form (single-field clusters already are);
-//   step 2  (slot permutation) every slot moves to the slot its (field, records) occupy in the
-//           dst layout's field-blocked form, by following the permutation's cycles (split into
-//           segments so that warps work in parallel; the last slot of each segment is saved
-//           first);
-//   step 3  (tile-local) each dst tile of a multi-field cluster that changed is rewritten from
-//           field-blocked to record-major form.
+// <= 16 dividing every field width) of a cluster with stride s occupies s / u slots.  A RUN is a
+// maximal sequence of fields consecutive in both the src and the dst cluster record; in a tile's
+// BLOCKED form (AoSoA with block T, one block per run) run b's T values are contiguous, T * w_b
+// bytes = w_b / u whole slots:
+//   step 1  (tile-local) each src tile of a cluster made of several runs is rewritten in place
+//           from record-major to blocked form (a one-run cluster already is);
+//   step 2  (slot permutation) every slot moves to the slot its (run, bytes) occupy in the dst
+//           layout's blocked form, by following the permutation's cycles (split into segments
+//           so that warps work in parallel; the last slot of each segment is saved first);
+//   step 3  (tile-local) each dst tile of a cluster made of several runs is rewritten from
+//           blocked to record-major form.
 // Clusters whose member set is the same in both layouts are moved as raw slots (no rewrite),
 // and not at all when their region base is the same (fixed points).  The last N mod T records
 // (the tail) are saved to the workspace first and written to their dst positions last.
