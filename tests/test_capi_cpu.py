@@ -603,3 +603,25 @@ def test_inplace_plan_errors():
     with pytest.raises(A.AdhaError) as e:
         _ip([1] * 1000, [0] * 1000, list(range(1000)), 10)
     assert e.value.name == "ADHA_ERR_UNSUPPORTED"
+
+
+def test_inplace_plan_runs_skip_tile_passes():
+    """Runs (fields contiguous in both cluster records) are moved as blocks: a cluster that is one
+    run needs no tile rewrite.  K-Means 4xAoS8 -> AoS rewrites only the dst AoS tiles; Medical
+    AoS -> AoSV rewrites only the src AoS tiles ({V1,V2,V3} is one run on both sides); SoA -> AoS
+    has nothing to rewrite on the src side; identical hybrids nothing at all."""
+    km = [4] * 32
+    aos8 = [f // 8 for f in range(32)]
+    d = _ip(km, aos8, [0] * 32, 1 << 20).describe()
+    assert (d["pre_clusters"], d["post_clusters"]) == (0, 1)
+    d = _ip(km, [0] * 32, aos8, 1 << 20).describe()
+    assert (d["pre_clusters"], d["post_clusters"]) == (1, 0)
+    med = [4] * 9
+    d = _ip(med, [0] * 9, [0, 0, 0, 1, 2, 3, 4, 5, 6], 1 << 20).describe()
+    assert (d["pre_clusters"], d["post_clusters"]) == (1, 0)
+    w = [8 if i % 4 == 3 else 4 for i in range(16)]
+    d = _ip(w, list(range(16)), [0] * 16, 10_000_000).describe()
+    assert (d["pre_clusters"], d["post_clusters"]) == (0, 1)
+    # a hybrid whose clusters interleave: {f0,f2} -> {f0,f1,f2} splits into the runs f0 | f2
+    d = _ip([4, 4, 4], [0, 1, 0], [0, 0, 0], 4096).describe()
+    assert (d["pre_clusters"], d["post_clusters"]) == (1, 1)
