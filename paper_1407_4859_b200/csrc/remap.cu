@@ -230,6 +230,24 @@ uint64_t small_bytes() {
     return e && *e ? (uint64_t)std::strtoull(e, nullptr, 10) : (uint64_t)(64u << 10);
 }
 
+// Payload up to which a remap takes the direct kernel instead of the tiled one.  The tiled kernel
+// has a fixed cost per launch (pipeline fill, per-component setup: 5-8 us for one component,
+// ~12 us for 7, ~50 us for C3's 24 components, 20-30 us in 2-byte byte-group mode; CUDA-graph
+// replay, tools/small_path_probe.py, profiles/r01k_small_path.log) while the direct kernel
+// streams at ~1 TB/s for 4-byte units and ~0.3-0.5 TB/s for 1-/2-byte units after ~2 us.
+// Crossovers measured on B200: 4-8 MB (one component, 4-byte units), 8-16 MB (>= 4
+// components or 2-byte units), > 32 MB (24 components), 1-4 MB (1-byte units).
+// ADHA_SMALL_BYTES, when set, overrides this (tests force either path with it).
+uint64_t direct_bytes(const RemapPlan& p) {
+    const char* e = std::getenv("ADHA_SMALL_BYTES");
+    if (e && *e) return (uint64_t)std::strtoull(e, nullptr, 10);
+    const size_t k = p.comps.size();
+    if (p.unit == 1) return 2ull << 20;
+    if (k >= 16) return 32ull << 20;
+    if (k >= 4 || p.unit == 2) return 8ull << 20;
+    return 4ull << 20;
+}
+
 
 adha_status validate(const void* src, const adha_layout* hs, const void* dst, const adha_layout* hd, int64_t n,
                      Checked* out, bool device_buffers) {
@@ -256,8 +274,11 @@ adha_status remap_checked(const uint8_t* src, const Layout& ls, uint8_t* dst, co
                           const Checked& ck, cudaStream_t st) {
     if (n == 0) return ADHA_OK;
     auto plan = get_plan(ls, ld);
-    // small remaps (<= ADHA_SMALL_BYTES of payload, 64 KB by default) are latency-bound: direct kernel
-    if (!plan->tiled || (uint64_t)n * ls.record_bytes <= small_bytes())
+    // small and mid-size remaps (direct_bytes above) run faster on the direct kernel; a dst in
+    // pinned host or peer memory keeps the latency-only threshold (the tiled kernel's 16-byte
+    // stores suit PCIe / NVLink writes better than the direct kernel's per-field stores)
+    const uint64_t thr = ck.dst_local ? direct_bytes(*plan) : small_bytes();
+    if (!plan->tiled || (uint64_t)n * ls.record_bytes <= thr)
         return launch_naive(src, ls, ck.bs, dst, ld, ck.bd, 0, n, st);
 
     int n_sm = 0;

@@ -28,7 +28,8 @@ import paper_1407_4859_b200 as A  # noqa: E402
 @pytest.fixture(params=["tiled", "direct-small"])
 def small_path(request, monkeypatch):
     """Run a test twice: with every remap on the tiled kernel (ADHA_SMALL_BYTES=0), and with the
-    default routing where remaps of <= 64 KB take the direct latency kernel."""
+    default routing where small and mid-size remaps (up to 2-32 MB of payload, remap.cu
+    direct_bytes) take the direct kernel."""
     if request.param == "tiled":
         monkeypatch.setenv("ADHA_SMALL_BYTES", "0")
     else:
