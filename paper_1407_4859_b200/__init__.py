@@ -244,6 +244,9 @@ def _ptr(x) -> int:
 def _stream(stream) -> int:
     if stream is None:
         import torch
+        raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+        if raw is not None:         # 0.3 us instead of 3 us for building a Stream object per call
+            return int(raw(torch.cuda.current_device()))
         return int(torch.cuda.current_stream().cuda_stream)
     if isinstance(stream, int):
         return stream
