@@ -277,9 +277,11 @@ ADHA_API adha_status adha_remap_host(const void* src_host, const adha_layout* sr
  * can still change layout.  Packed, unblocked layouts only (no ADHA_LAYOUT_ALIGNED, no
  * AoSoA blocks).  Cost: the buffer is cut into S-byte slots (S in 256..4096); tiles of
  * T = S/u records (u = largest power of two <= 16 dividing every width) of each cluster whose
- * member set changes are transposed in place, every slot is moved along the cycles of a slot
- * permutation, and the dst tiles are transposed back.  Clusters that keep their member set
- * and their region base move no byte (the moved-subset rule).
+ * member set changes are rewritten in place, every slot is moved along the cycles of a slot
+ * permutation, and the dst tiles are rewritten back.  Clusters that keep their member set
+ * and their region base move no byte (the moved-subset rule).  Buffers of at
+ * most 16 MB (ADHA_INPLACE_STAGED_BYTES at plan creation) are instead remapped out of place
+ * into the workspace and copied back ("staged" mode: the workspace then holds bytes(Ld, N)).
  *
  * Usage: plan = create(Ls, Ld, N) [host only]; upload(plan, workspace) once; then
  * adha_remap_inplace(buf, ...) any number of times (each call remaps the buffer's current

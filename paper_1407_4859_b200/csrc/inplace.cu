@@ -527,6 +527,15 @@ extern "C" adha_status adha_remap_inplace(void* buf, uint64_t buf_bytes, const a
     cudaStream_t st = (cudaStream_t)stream;
     uint8_t* b = (uint8_t*)buf;
     uint8_t* ws = (uint8_t*)workspace;
+    if (P.staged) {   // small buffer: out-of-place remap into the workspace, then copy back
+        // adha_layout is {Layout L}: the plan's own layout copies serve as handles
+        const adha_layout* hs = reinterpret_cast<const adha_layout*>(&P.ls);
+        const adha_layout* hd = reinterpret_cast<const adha_layout*>(&P.ld);
+        adha_status s = adha_remap(b, hs, ws + P.ws_stage, hd, P.n, stream);
+        if (s != ADHA_OK) return s;
+        e = cudaMemcpyAsync(b, ws + P.ws_stage, P.bytes_d, cudaMemcpyDeviceToDevice, st);
+        return e == cudaSuccess ? ADHA_OK : cuda_err(e, "cudaMemcpyAsync (staged in-place remap)");
+    }
     adha_status s = launch_tail(P, b, ws, false, st);
     if (s != ADHA_OK) return s;
     s = launch_tiles(P, b, ws, false, dev, sms, st);

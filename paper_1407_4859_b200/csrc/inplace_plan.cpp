@@ -6,6 +6,7 @@
 // with dst and src the same buffer.  This file computes, once per (Ls, Ld, N), which S-byte
 // slot goes where (a permutation of slot indices), its cycles, and the workspace layout.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <thread>
@@ -273,6 +274,27 @@ adha_status inplace_plan_build(const Layout& ls, const Layout& ld, int64_t n, In
     p->u = u;
     const uint32_t atom = u % 4 == 0 ? 4 : 1;
 
+    // Small buffers: remap out of place into the workspace and copy back (two launches, a few
+    // microseconds) instead of the tile / cycle passes, whose fixed costs dominate there.
+    {
+        const char* e = std::getenv("ADHA_INPLACE_STAGED_BYTES");
+        const uint64_t lim = e && *e ? std::strtoull(e, nullptr, 10) : IP_STAGED_BYTES;
+        p->staged = lim > 0 && std::max(p->bytes_s, p->bytes_d) <= lim;
+        p->pre.clear(); p->post.clear(); p->cols.clear(); p->seq.clear(); p->segs.clear(); p->tail_fields.clear();
+        p->content_slots = p->moved_slots = p->fixed_slots = p->junk_slots = p->cycles = 0;
+        if (p->staged) {
+            p->S = p->T = 0;
+            p->m = 0;
+            p->tail = 0;
+            p->ws_pieces = p->ws_cols = p->ws_tailf = p->ws_seq = p->ws_segs = p->ws_save = p->ws_tail = 0;
+            p->ws_stage = 0;
+            p->ws_bytes = std::max<uint64_t>(align256(p->bytes_d), 256);
+            p->uploaded = nullptr;
+            p->uploaded_device = -1;
+            return ADHA_OK;
+        }
+    }
+
     // clusters kept as raw slots: same member set in both layouts
     const int32_t Cs = ls.n_clusters(), Cd = ld.n_clusters();
     std::vector<int32_t> twin_s(Cs, -1), twin_d(Cd, -1);
@@ -452,6 +474,7 @@ std::string inplace_plan_json(const InplacePlan& p) {
     auto u64 = [](uint64_t v) { return std::to_string(v); };
     std::string s = "{";
     s += "\"n_records\":" + std::to_string(p.n);
+    s += std::string(",\"mode\":\"") + (p.staged ? "staged" : "permute") + "\"";
     s += ",\"unit\":" + u64(p.u) + ",\"slot_bytes\":" + u64(p.S) + ",\"T\":" + u64(p.T);
     s += ",\"body_tiles\":" + std::to_string(p.m) + ",\"tail_records\":" + std::to_string(p.tail);
     s += ",\"src_bytes\":" + u64(p.bytes_s) + ",\"dst_bytes\":" + u64(p.bytes_d);
@@ -465,8 +488,9 @@ std::string inplace_plan_json(const InplacePlan& p) {
     for (const auto& x : p.pre) pre_b += (uint64_t)p.m * p.T * x.stride;
     for (const auto& x : p.post) post_b += (uint64_t)p.m * p.T * x.stride;
     // device traffic of one run: read + write of every transposed tile and moved slot
-    s += ",\"traffic_bytes\":" + u64(2 * (pre_b + post_b + (p.moved_slots + p.segs.size()) * p.S +
-                                          2 * (uint64_t)p.tail * p.ls.record_bytes));
+    s += ",\"traffic_bytes\":" + u64(p.staged ? 2 * ((uint64_t)p.n * p.ls.record_bytes + p.bytes_d)
+                                             : 2 * (pre_b + post_b + (p.moved_slots + p.segs.size()) * p.S +
+                                                    2 * (uint64_t)p.tail * p.ls.record_bytes));
     s += ",\"workspace_bytes\":" + u64(p.ws_bytes);
     s += "}";
     return s;

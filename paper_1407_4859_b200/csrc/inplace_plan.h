@@ -86,11 +86,15 @@ struct InplacePlan {
     uint64_t content_slots = 0, moved_slots = 0, fixed_slots = 0, junk_slots = 0, cycles = 0;
     // workspace layout (byte offsets, each 256-aligned) and total size
     uint64_t ws_pieces = 0, ws_cols = 0, ws_tailf = 0, ws_seq = 0, ws_segs = 0, ws_save = 0, ws_tail = 0, ws_bytes = 0;
+    bool staged = false;                 // small buffer: out-of-place remap into the workspace + copy back
+    uint64_t ws_stage = 0;
     // upload state (adha_inplace_plan_upload)
     const void* uploaded = nullptr;
     int uploaded_device = -1;
 };
 
+// Buffers up to this many bytes are remapped through the workspace (ADHA_INPLACE_STAGED_BYTES).
+constexpr uint64_t IP_STAGED_BYTES = 16ull << 20;
 // Segment length: positions per segment (a warp group walks one segment).
 constexpr uint32_t IP_SEG = 64;
 // Largest transposed tile (shared memory of one CTA, with row padding).

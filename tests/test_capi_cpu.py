@@ -548,7 +548,12 @@ def _ip(widths, ls, ld, n):
     return A.InplacePlan(A.Layout(widths, ls), A.Layout(widths, ld), n)
 
 
-def test_inplace_plan_counts_and_sizes():
+@pytest.fixture
+def permute_mode(monkeypatch):
+    monkeypatch.setenv("ADHA_INPLACE_STAGED_BYTES", "0")
+
+
+def test_inplace_plan_counts_and_sizes(permute_mode):
     """Host plan of adha_remap_inplace: the buffer needs max(bytes(Ls), bytes(Ld)) (not the sum);
     every body slot of the src layout is content; the permutation closes on src u dst slots
     (moved + fixed = content + junk); the slot size divides every region base of both layouts."""
@@ -573,7 +578,7 @@ def test_inplace_plan_counts_and_sizes():
             assert p.workspace_bytes >= d["segments"] * S
 
 
-def test_inplace_plan_identity_and_moved_subset():
+def test_inplace_plan_identity_and_moved_subset(permute_mode):
     widths = [4] * 9
     aosv, soa = [0, 0, 0, 1, 2, 3, 4, 5, 6], list(range(9))
     d = _ip(widths, aosv, aosv, 1 << 16).describe()
@@ -585,7 +590,21 @@ def test_inplace_plan_identity_and_moved_subset():
     assert d["moved_slots"] + d["fixed_slots"] == 9 * 4 * (1 << 20) // S
 
 
-def test_inplace_plan_errors():
+def test_inplace_plan_staged_mode(monkeypatch):
+    """Small buffers (<= ADHA_INPLACE_STAGED_BYTES, 16 MB by default) go through the workspace:
+    the workspace holds the dst layout, no slot tables."""
+    monkeypatch.delenv("ADHA_INPLACE_STAGED_BYTES", raising=False)
+    w = [8 if i % 4 == 3 else 4 for i in range(16)]
+    p = _ip(w, [0] * 16, list(range(16)), 100_000)
+    d = p.describe()
+    assert d["mode"] == "staged" and d["moved_slots"] == 0 and d["segments"] == 0
+    assert p.workspace_bytes >= O.layout_bytes(w, list(range(16)), 100_000)
+    assert _ip(w, [0] * 16, list(range(16)), 1_000_000).describe()["mode"] == "permute"
+    monkeypatch.setenv("ADHA_INPLACE_STAGED_BYTES", "0")
+    assert _ip(w, [0] * 16, list(range(16)), 100_000).describe()["mode"] == "permute"
+
+
+def test_inplace_plan_errors(permute_mode):
     w = [4, 4, 8]
     with pytest.raises(A.AdhaError) as e:
         _ip(w, [0, 0, 0], [0, 1, 2], -1)
@@ -605,7 +624,7 @@ def test_inplace_plan_errors():
     assert e.value.name == "ADHA_ERR_UNSUPPORTED"
 
 
-def test_inplace_plan_runs_skip_tile_passes():
+def test_inplace_plan_runs_skip_tile_passes(permute_mode):
     """Runs (fields contiguous in both cluster records) are moved as blocks: a cluster that is one
     run needs no tile rewrite.  K-Means 4xAoS8 -> AoS rewrites only the dst AoS tiles; Medical
     AoS -> AoSV rewrites only the src AoS tiles ({V1,V2,V3} is one run on both sides); SoA -> AoS

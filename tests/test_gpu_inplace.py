@@ -23,6 +23,13 @@ if not torch.cuda.is_available():
 import paper_1407_4859_b200 as A  # noqa: E402
 
 
+@pytest.fixture(autouse=True)
+def permute_mode(monkeypatch):
+    """Every test here exercises the slot-permutation kernels (tile rewrite + cycles), also at
+    the small sizes that would otherwise go through the staged mode (ADHA_INPLACE_STAGED_BYTES)."""
+    monkeypatch.setenv("ADHA_INPLACE_STAGED_BYTES", "0")
+
+
 def oracle_dst(src, ls, ld, widths, n):
     dst = np.zeros(O.layout_bytes(widths, ld, n), np.uint8)
     O.remap(src, ls, dst, ld, widths, n, threads=min(8, os.cpu_count() or 1))
@@ -229,3 +236,17 @@ def test_c3_shape_in_place_sampled(variant):
     bd, sd, od, _ = O.field_addresses(widths, ld, n)
     after = gather_fields_dev(buf, widths, bd, sd, od, recs)
     assert np.array_equal(before, after)
+
+
+def test_staged_mode_small_buffers(monkeypatch):
+    """Buffers up to ADHA_INPLACE_STAGED_BYTES (16 MB by default) are remapped out of place into
+    the workspace and copied back; same result on every dst payload byte."""
+    monkeypatch.delenv("ADHA_INPLACE_STAGED_BYTES", raising=False)
+    widths = config_widths(16)
+    for ls, ld, n in [([0] * 16, list(range(16)), 1000), (list(range(16)), [0] * 16, 100_003),
+                      ([0, 0, 1, 1, 2, 2, 3, 3] * 2, [i % 5 for i in range(16)], 65_537)]:
+        plan = check_inplace(widths, ls, ld, n, seed=n)
+        d = plan.describe()
+        assert d["mode"] == "staged" and plan.workspace_bytes >= d["dst_bytes"]
+    big = A.InplacePlan(A.Layout(widths, [0] * 16), A.Layout(widths, list(range(16))), 1_000_000)
+    assert big.describe()["mode"] == "permute"

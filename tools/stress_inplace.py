@@ -15,6 +15,12 @@ from adha_inputs import field_columns  # noqa: E402
 from oracle import remap as O  # noqa: E402
 
 CASES = int(sys.argv[1]) if len(sys.argv) > 1 else 300
+# the slot-permutation kernels at every size (small buffers would otherwise take the staged mode,
+# an out-of-place remap through the workspace; ADHA_INPLACE_STAGED_BYTES=-1 keeps the default)
+if os.environ.get("ADHA_INPLACE_STAGED_BYTES") != "-1":
+    os.environ["ADHA_INPLACE_STAGED_BYTES"] = "0"
+else:
+    os.environ.pop("ADHA_INPLACE_STAGED_BYTES")
 rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 14074859)
 fails = 0
 stats = {}
