@@ -186,3 +186,42 @@ def test_capi_planner_rejects_malformed_json_cleanly(data):
             call()
         except A.AdhaError as e:
             assert e.name in ("ADHA_ERR_PARSE", "ADHA_ERR_PLANNER", "ADHA_ERR_CAPACITY", "ADHA_ERR_INVALID_ARG"), e
+
+
+@st.composite
+def inplace_case(draw):
+    F = draw(st.integers(1, 12))
+    widths = draw(st.lists(st.sampled_from([1, 2, 3, 4, 4, 8, 8, 12, 16]), min_size=F, max_size=F))
+    ls = draw(st.lists(st.integers(0, F - 1), min_size=F, max_size=F))
+    ld = draw(st.lists(st.integers(0, F - 1), min_size=F, max_size=F))
+    n = draw(st.one_of(st.sampled_from([0, 1, 63, 64, 65, 255, 256, 257, 4096]), st.integers(0, 300_000)))
+    return widths, ls, ld, n
+
+
+@SET
+@given(inplace_case())
+def test_inplace_plan_invariants(case):
+    """Host plan of the in-place remap (slot-permutation mode) on random packed layout pairs:
+    never crashes; the buffer is max(bytes(Ls), bytes(Ld)) by the oracle's address model; every
+    src body slot is content; the permutation closes on src u dst slots; segments cover the moved
+    slots in pieces of at most 64; the workspace holds a saved slot per segment."""
+    import os
+    widths, ls, ld, n = case
+    os.environ["ADHA_INPLACE_STAGED_BYTES"] = "0"
+    try:
+        try:
+            p = A.InplacePlan(A.Layout(widths, ls), A.Layout(widths, ld), n)
+        except A.AdhaError as e:   # a record too wide for a tile in shared memory
+            assert e.name == "ADHA_ERR_UNSUPPORTED"
+            return
+        d = p.describe()
+    finally:
+        os.environ.pop("ADHA_INPLACE_STAGED_BYTES", None)
+    assert p.buffer_bytes == max(O.layout_bytes(widths, ls, n), O.layout_bytes(widths, ld, n))
+    u, S, T = d["unit"], d["slot_bytes"], d["T"]
+    assert S == T * u and all(w % u == 0 for w in widths)
+    assert d["body_tiles"] == n // T and d["tail_records"] == n % T
+    assert d["content_slots"] == (n // T) * sum(widths) // u
+    assert d["moved_slots"] + d["fixed_slots"] == d["content_slots"] + d["junk_slots"]
+    assert d["segments"] * 64 >= d["moved_slots"] and (d["moved_slots"] == 0) == (d["segments"] == 0)
+    assert p.workspace_bytes >= d["segments"] * S
