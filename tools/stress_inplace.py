@@ -1,9 +1,9 @@
 """Randomised GPU stress of the in-place remap (adha_remap_inplace): many random packed layout
 pairs (widths from 1 to 16 bytes, so u = 1, 2, 4, 8 and 16 all occur), random N (tile boundaries,
-ragged tails, tiny and large), each plan run forwards and then backwards on the same buffer.
+ragged tails, tiny and large; up to MAX_N), each plan run forwards and then backwards on the same buffer.
 Every dst payload byte is compared with the CPU oracle's out-of-place remap, and the round trip
 with the original records.  Not part of the test suite (minutes of run time); prints the number
-of cases and the first failure.   usage: python tools/stress_inplace.py [cases] [seed]"""
+of cases and the first failure.   usage: python tools/stress_inplace.py [cases] [seed] [max_n]"""
 import os
 import sys
 
@@ -22,6 +22,7 @@ if os.environ.get("ADHA_INPLACE_STAGED_BYTES") != "-1":
 else:
     os.environ.pop("ADHA_INPLACE_STAGED_BYTES")
 rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 14074859)
+MAX_N = int(sys.argv[3]) if len(sys.argv) > 3 else 400_000
 fails = 0
 stats = {}
 for case in range(CASES):
@@ -33,7 +34,7 @@ for case in range(CASES):
         return [int(x) for x in rng.integers(0, max(1, F // int(rng.integers(1, 5))), size=F)]
 
     ls, ld = rand_labels(), rand_labels()
-    n = int(rng.choice([1, 63, 64, 65, 255, 256, 257, 1000, 4097, int(rng.integers(1, 400_000))]))
+    n = int(rng.choice([1, 63, 64, 65, 255, 256, 257, 1000, 4097, int(rng.integers(1, MAX_N))]))
     Ls, Ld = A.Layout(widths, ls), A.Layout(widths, ld)
     try:
         fwd, bwd = A.InplacePlan(Ls, Ld, n), A.InplacePlan(Ld, Ls, n)
