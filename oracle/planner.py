@@ -386,12 +386,17 @@ def remap_cost(l1: Layout, d1: str, l2: Layout, d2: str, common: FrozenSet[str],
     return nbytes / lk.bandwidth_bytes_per_ns + lk.latency_ns, moved
 
 
-def combine_loss(s1: Section, s2: Section, d: Device, p: Program, prof: Optional[Profile] = None
-                 ) -> float:
-    """loss from combining two sections under the merged ODS layout."""
-    lm = ods(merge_sections([s1, s2]), d, p)
+def combine_loss(s1: Section, s2: Section, d: Device, p: Program, prof: Optional[Profile] = None,
+                 ods_fn=None) -> float:
+    """loss from combining two sections under the merged ODS layout:
+    L_m = ods(merge(s1, s2)); loss = [exec(s1, L_m) + exec(s2, L_m)] - [exec(s1, ods(s1)) +
+    exec(s2, ods(s2))].  ods_fn(s, d, p) -> Layout replaces the greedy ODS (SPEC.md:237 states
+    loss >= 0 when it is the optimal, brute-force ODS)."""
+    ods_fn = ods if ods_fn is None else ods_fn
+    lm = ods_fn(merge_sections([s1, s2]), d, p)
     merged = exec_cost(s1, lm, d, p, prof)[2] + exec_cost(s2, lm, d, p, prof)[2]
-    separate = exec_cost(s1, ods(s1, d, p), d, p, prof)[2] + exec_cost(s2, ods(s2, d, p), d, p, prof)[2]
+    separate = (exec_cost(s1, ods_fn(s1, d, p), d, p, prof)[2]
+                + exec_cost(s2, ods_fn(s2, d, p), d, p, prof)[2])
     return merged - separate
 
 

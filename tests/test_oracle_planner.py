@@ -258,6 +258,49 @@ def test_combine_loss_trivial_cases():
     assert P.combine_loss(p2.sections[0], p2.sections[1], CPU, p2) == 0.0
 
 
+@pytest.mark.parametrize("t2,loss", [(500.0, 62.5), (3000.0, 1000.0)])
+def test_combine_loss_positive_instance(t2, loss):
+    """s1 favours an {A,B} cluster (irregular), s2 streams {A,B} on a coalescing
+    device (penalised clusters) -> loss > 0.  Values derived by hand from SPEC.md:205-207 with
+    line 64 B, line time 1 ns, penalty 2, 4-byte A and B, s1 trip 1000:
+      ods(s1) = {A,B} (weight +1000), exec 1000 (one line per access);
+      ods(s2) = {A}|{B} (weight -t2), exec t2 * (4/64 + 4/64) = t2 / 8.
+      t2 = 500:  merged weight +500 -> {A,B}: s1 1000, s2 500 * 8/64 * 2 = 125
+                 -> loss = 1125 - (1000 + 62.5) = 62.5
+      t2 = 3000: merged weight -2000 -> {A}|{B}: s1 2 * 1000 (two lines), s2 375
+                 -> loss = 2375 - (1000 + 375) = 1000
+    The two cases go through the two merged layouts, so a swapped term or sign fails one."""
+    dev = P.Device("gpu", 64, 1.0, 1.0, True, 2.0, 64)
+    p = P.Program("t", 100, [P.Field("A", 4, 0), P.Field("B", 4, 1)],
+                  [P.Section("s1", 1000.0, (P.AccessGroup(("A", "B"), 1.0, "irregular"),), ("gpu",)),
+                   P.Section("s2", t2, (P.AccessGroup(("A", "B"), 1.0, "streaming"),), ("gpu",))],
+                  ["s1", "s2"])
+    got = P.combine_loss(p.sections[0], p.sections[1], dev, p)
+    assert got == pytest.approx(loss, rel=1e-15) and got > 0
+    # the loss is not symmetric in general, but here exchanging s1 and s2 only reorders sums
+    assert P.combine_loss(p.sections[1], p.sections[0], dev, p) == pytest.approx(loss, rel=1e-15)
+
+
+def test_combine_loss_nonnegative_under_optimal_ods():
+    """combine_loss >= 0 when the greedy ODS is replaced by the optimal
+    (brute-force) ODS and exec costs come from the model -- the merged layout cannot beat
+    each section's own optimum.  300 random section pairs of <= 6 fields."""
+    rng = random.Random(237)
+    opt = lambda s, d, p: P.brute_force_ods(s, d, p)[0]          # noqa: E731
+    checked = 0
+    while checked < 300:
+        p, a = random_program(rng, k_max=4, f_max=6), random_arch(rng)
+        if len(p.sections) < 2:
+            continue
+        s1, s2 = p.sections[0], p.sections[1]
+        for dname in set(s1.allowed_devices) & set(s2.allowed_devices):
+            loss = P.combine_loss(s1, s2, a.device(dname), p, ods_fn=opt)
+            scale = sum(P.exec_cost(s, P.brute_force_ods(s, a.device(dname), p)[0], a.device(dname), p)[2]
+                        for s in (s1, s2))
+            assert loss >= -1e-12 * max(scale, 1.0), (loss, dname)
+            checked += 1
+
+
 # ---------------------------------------------------------------- random instances
 
 def random_program(rng, k_max=5, f_max=8):
