@@ -1,13 +1,16 @@
 #!/usr/bin/env python
 """bench.py -- ADHA layout remap on B200: remap GB/s (read+write), bit-exact path.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl adha|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--impl adha|reference]
 
 One step = one pass of the hot path over the configuration's records (SURVEY.md
-8(d)): for C2 one AoS->SoA remap of 10M 80-byte records.  Multi-GPU (torchrun,
-one process per GPU): the record array is sharded by contiguous index range
-(adha_shard_range) with no collective on the data path; each rank remaps its
-own shard ("weak" for C2: 10M records per rank; "strong" for C5: 8 GiB total).
+8(d)).  The default is C5, the configuration BASELINE.json's metric is quoted on
+("at 1/2/4/8 B200"): one AoS->SoA remap of 8 GiB of 80-byte records, split over
+the GPUs.  Multi-GPU: one process per GPU (torchrun; `--gpus N` without torchrun
+re-launches itself through torch.distributed.run with N ranks); the record array
+is sharded by contiguous index range (adha_shard_range) with no collective on the
+data path; each rank remaps its own shard ("strong" for C5: 8 GiB in total;
+"weak" for the other configs, e.g. C2: 10M records per rank).
 Timing: CUDA events on the launching stream, barrier + synchronize on both
 sides, max over ranks.  Prints ONE JSON line on rank 0.
 """
@@ -36,6 +39,9 @@ CONFIGS = {
     "C3R": ("64-field record, SoA->ODS hybrid of the seeded random program (SURVEY 8(d)), 50M records", "c3r",
             50_000_000, "weak"),
     "C4": ("Medical 9x fp32, PDL chain AoS->AoSV->SoA->AoS over 2 GiB of records", "c4", (2 ** 31) // 36, "weak"),
+    "C4M": ("Medical 9x fp32, the paper's remap edge AoSV->SoA as a moved subset (adha_remap_regions: the six "
+            "unchanged singleton regions aliased, only {V1,V2,V3} move), 2 GiB of records", "c4m", (2 ** 31) // 36,
+            "weak"),
     "C5": ("8 GiB mixed-width record array AoS->SoA, sharded across GPUs", "c2", (2 ** 33) // 80, "strong"),
     "P1": ("Medical 256^3 voxels x 9 fp32: AoS->AoSV->SoA", "p1", 256 ** 3, "weak"),
     "P2": ("K-Means 2^23 points x 32 fp32: SoA->4xAoS8->AoS", "p2", 2 ** 23, "weak"),
@@ -72,6 +78,8 @@ def chain_for(kind):
         return w, [list(range(64)), c3_labels("c3_random_program.json", "c3r")[0]]
     if kind == "c4":
         return [4] * 9, [[0] * 9, [0, 0, 0, 1, 2, 3, 4, 5, 6], list(range(9)), [0] * 9]
+    if kind == "c4m":
+        return [4] * 9, [[0, 0, 0, 1, 2, 3, 4, 5, 6], list(range(9))]
     if kind == "p1":
         return [4] * 9, [[0] * 9, [0, 0, 0, 1, 2, 3, 4, 5, 6], list(range(9))]
     if kind == "p2":
@@ -429,12 +437,33 @@ def run_inplace(args, rank, world, local, share):
 
 # ----------------------------------------------------------------------------------------- adha arm
 
+def free_port():
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def spawn_ranks(n):
+    """`--gpus N` without torchrun: re-launch this script as N ranks (one process per GPU) through
+    torch.distributed.run on 127.0.0.1; rank 0 prints the JSON line.  Exit code: the launcher's."""
+    if os.environ.get("ADHA_BENCH_SHARE_GPU") != "1":
+        import torch
+        have = torch.cuda.device_count()
+        if have < n:
+            print(f"bench.py: --gpus {n} but only {have} CUDA device(s) visible", file=sys.stderr)
+            return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="C5", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="adha", choices=["adha", "reference"])
     ap.add_argument("--inplace", action="store_true",
                     help="remap in place (adha_remap_inplace): one buffer of max(bytes) per rank")
@@ -450,9 +479,19 @@ def main():
                          "(power-capped sustained regime, reported as `sustained`; 0 disables)")
     args = ap.parse_args()
 
+    if args.gpus < 1:
+        print("bench.py: --gpus must be >= 1", file=sys.stderr)
+        return 2
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        if args.impl == "reference":
+            return run_reference(args, 0, args.gpus)     # the CPU oracle: rank 0's work only
+        return spawn_ranks(args.gpus)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        return 2
     if args.impl == "reference":
         return run_reference(args, rank, world)
 
@@ -486,17 +525,45 @@ def main():
     n_total, lo, hi = shard_for(n_cfg, world, rank, scaling)
     n = hi - lo
     layouts = [A.Layout(widths, lab) for lab in chain]
-    bufs = [torch.empty(max(l.nbytes(n), 1), dtype=torch.uint8, device=dev) for l in layouts]
-    fill_random_device(bufs[0], SEED_BASE + 1 + rank)
-    for b in bufs[1:]:
-        b.fill_(0xA5)
-    stream = torch.cuda.current_stream(dev)
-    n_remaps = len(chain) - 1
-    bytes_step_rank = 2 * n * R * n_remaps
     plan = A.plan_describe(layouts[0], layouts[1])
+    moved = kind == "c4m"          # the remap edge as a moved subset (adha_remap_regions, NEXT N1)
+    n_remaps = len(chain) - 1
+    if moved:
+        # dst regions of identity components alias the src regions (nothing moves there); the other
+        # dst clusters get their own regions in one buffer; the metric counts the moved bytes
+        L0, L1 = layouts
+        keep_src = {c["src_clusters"][0]: c["dst_clusters"][0] for c in plan["components"] if c["identity"]}
+        keep_dst = {d: s_ for s_, d in keep_src.items()}
+        R_moved = sum(c["R"] for c in plan["components"] if not c["identity"])
+        co0, co1 = L0.cluster_of, L1.cluster_of
+        src_off = [L0.field_address(co0.index(c), n)[0] for c in range(L0.n_clusters)]
+        new_c = [c for c in range(L1.n_clusters) if c not in keep_dst]
+        new_bytes = [-(-n * sum(w for w, cc in zip(widths, co1) if cc == c) // 256) * 256 for c in new_c]
+        bufs = [torch.empty(max(L0.nbytes(n), 1), dtype=torch.uint8, device=dev),
+                torch.empty(max(sum(new_bytes), 1), dtype=torch.uint8, device=dev)]
+        fill_random_device(bufs[0], SEED_BASE + 1 + rank)
+        bufs[1].fill_(0xA5)
+        base0 = bufs[0].data_ptr()
+        src_regions = [base0 + o for o in src_off]
+        dst_regions, acc = [0] * L1.n_clusters, 0
+        for c, nb in zip(new_c, new_bytes):
+            dst_regions[c] = bufs[1].data_ptr() + acc
+            acc += nb
+        for d, s_ in keep_dst.items():
+            dst_regions[d] = src_regions[s_]
+    else:
+        R_moved = R
+        bufs = [torch.empty(max(l.nbytes(n), 1), dtype=torch.uint8, device=dev) for l in layouts]
+        fill_random_device(bufs[0], SEED_BASE + 1 + rank)
+        for b in bufs[1:]:
+            b.fill_(0xA5)
+    stream = torch.cuda.current_stream(dev)
+    bytes_step_rank = 2 * n * R_moved * n_remaps
 
     def step_direct():
-        if n_remaps == 1:
+        if moved:
+            A.remap_regions(src_regions, layouts[0], dst_regions, layouts[1], n, stream=None)
+        elif n_remaps == 1:
             A.remap(bufs[0], layouts[0], bufs[1], layouts[1], n, stream=None)       # torch's current stream
         else:       # a PDL chain: adha_remap_chain (one launch for latency-bound chains like C1)
             A.remap_chain(bufs, layouts, n, stream=None)
@@ -579,7 +646,7 @@ def main():
     ms_total = t0.elapsed_time(t1)
     ms_max = max_over_ranks(ms_total, dev)
     wall_max = max_over_ranks(wall_ms, dev)
-    value = aggregate_gbs(n_total, R, n_remaps, args.steps, ms_max)
+    value = aggregate_gbs(n_total, R_moved, n_remaps, args.steps, ms_max)
 
     # per-step spread, measured AFTER the timed region with an event pair around each step
     # (not part of `value`; the per-step events would add their own gaps inside the timed loop)
@@ -598,7 +665,7 @@ def main():
     copy_gbs = None
     ca = cb = None
     if n > 0 and not args.no_copy_ref:
-        ca = torch.empty(n * R, dtype=torch.uint8, device=dev)
+        ca = torch.empty(n * R_moved, dtype=torch.uint8, device=dev)
         cb = torch.empty_like(ca)
         for _ in range(3):
             cb.copy_(ca)
@@ -609,7 +676,7 @@ def main():
             cb.copy_(ca)
         c1.record(stream)
         torch.cuda.synchronize(dev)
-        copy_gbs = 2 * n * R * args.steps / (c0.elapsed_time(c1) * 1e-3) / 1e9
+        copy_gbs = 2 * n * R_moved * args.steps / (c0.elapsed_time(c1) * 1e-3) / 1e9
 
     def sustained_leg(fn, bytes_per_call):
         """fn back to back for --sustained-s seconds (untimed; the board reaches its power-capped
@@ -639,12 +706,12 @@ def main():
 
     sustained = None
     if args.sustained_s > 0 and n > 0:
-        v_s, clk_s = sustained_leg(step, 2 * n * R * n_remaps)
+        v_s, clk_s = sustained_leg(step, 2 * n * R_moved * n_remaps)
         sustained = {"value": v_s, "unit": "GB/s", "clocks": clk_s,
                      "note": f"after {args.sustained_s:.1f} s of untimed load (board power cap engaged); "
                              "K steps timed with events, max over ranks"}
         if ca is not None:
-            c_s, cclk_s = sustained_leg(lambda: cb.copy_(ca), 2 * n * R)
+            c_s, cclk_s = sustained_leg(lambda: cb.copy_(ca), 2 * n * R_moved)
             sustained["copy_gbs"] = c_s / world
             sustained["copy_clocks"] = cclk_s
     del ca, cb
@@ -658,10 +725,15 @@ def main():
     fused_chain = (n_remaps > 1 and os.environ.get("ADHA_CHAIN_FUSE", "1") != "0" and n * R <= small
                    and len(widths) <= 16 and n_remaps <= 4)
     launches_per_step = 1 if fused_chain else n_remaps
+    # routing of adha_remap (remap.cu): payload <= the plan's direct_bytes takes the direct kernel
+    direct = (not fused_chain) and n * R <= plan["direct_bytes"]
+    kernel_name = ("remap_chain_small_kernel (fused chain of latency-bound hops)" if fused_chain
+                   else "remap_naive_kernel (direct path for remaps <= the plan's direct_bytes)" if direct
+                   else "remap_tiled_kernel")
     # the step is those back-to-back launches and nothing else, so the kernel's average launch
     # duration is this rank's event time over the K steps / (K * launches per step)
     avg_launch_ms = ms_total / (args.steps * launches_per_step)
-    bytes_per_launch = 2 * n * R * n_remaps // launches_per_step
+    bytes_per_launch = 2 * n * R_moved * n_remaps // launches_per_step
     achieved = bytes_per_launch / (avg_launch_ms * 1e-3) / 1e9
     traffic = ncu_traffic(name)
 
@@ -670,10 +742,15 @@ def main():
     if not args.no_e2e and n > 0:
         h_src = torch.empty(layouts[0].nbytes(n), dtype=torch.uint8).pin_memory()
         h_src.copy_(bufs[0].cpu())
-        h_out = torch.empty(layouts[-1].nbytes(n), dtype=torch.uint8).pin_memory()
+        h_out = torch.empty(bufs[1].numel() if moved else layouts[-1].nbytes(n), dtype=torch.uint8).pin_memory()
         scratch = torch.empty(min(1 << 30, max(64 << 20, 2 * (layouts[0].nbytes(n) + layouts[-1].nbytes(n)))),
                               dtype=torch.uint8, device=dev)
-        if n_remaps == 1:
+        if moved:   # host AoSV in -> moved-subset remap -> the new {V1},{V2},{V3} regions out
+            def e2e_step():
+                bufs[0].copy_(h_src, non_blocking=True)
+                step_direct()
+                h_out.copy_(bufs[1], non_blocking=True)
+        elif n_remaps == 1:
             def e2e_step():
                 A.remap_host(h_src, layouts[0], h_out, layouts[1], n, scratch, stream=stream)
         else:       # a chain: host in -> device chain -> host out
@@ -695,9 +772,11 @@ def main():
         torch.cuda.synchronize(dev)
         barrier()
         e_ms = max_over_ranks(e0.elapsed_time(e1), dev)
-        e2e = {"value": aggregate_gbs(n_total, R, n_remaps, e2e_steps, e_ms), "unit": "GB/s",
-               "h2d_bytes_per_step": n * R, "d2h_bytes_per_step": n * R,
-               "api": "adha_remap_host" if n_remaps == 1 else "H2D copy + adha_remap x%d + D2H copy" % n_remaps,
+        e2e = {"value": aggregate_gbs(n_total, R_moved, n_remaps, e2e_steps, e_ms), "unit": "GB/s",
+               "h2d_bytes_per_step": h_src.numel(), "d2h_bytes_per_step": h_out.numel(),
+               "api": ("H2D copy + adha_remap_regions + D2H copy of the new regions" if moved
+                       else "adha_remap_host" if n_remaps == 1
+                       else "H2D copy + adha_remap x%d + D2H copy" % n_remaps),
                "ms_per_step": e_ms / e2e_steps}
         del h_src, h_out, scratch
 
@@ -709,7 +788,9 @@ def main():
         v_1, s_1 = oracle_rate(widths, chain, sample, 4.0, 1)
         cpu = {"value": v_all, "unit": "GB/s", "cores": cores, "kind": "oracle",
                "sample": f"first {sample} records of {name}, repeated for {s_all:.1f} s "
-                         f"(oracle/remap_oracle.c, record-range split over {cores} threads)",
+                         f"(oracle/remap_oracle.c, record-range split over {cores} threads)"
+                         + ("; the oracle remaps every field (no aliasing), GB/s of the bytes it moves"
+                            if moved else ""),
                "single_thread_value": v_1, "cpu_model": cpu_model()}
 
     if rank == 0:
@@ -721,11 +802,12 @@ def main():
             "config": {
                 "workload": f"{name}: {desc}", "n_records_total": n_total, "n_records_per_rank": n,
                 "record_bytes": R, "remaps_per_step": n_remaps,
+                "moved_bytes_per_record": R_moved,
                 "layouts": [l.to_string() for l in layouts],
-                "bytes_per_step_total": 2 * n_total * R * n_remaps,
-                "l2": (f"inputs larger than L2 ({2 * n * R / 1e9:.2f} GB moved per remap per GPU vs 126 MB L2); no flush"
-                       if 2 * n * R > (252 << 20) else
-                       f"inputs fit in L2 ({2 * n * R} B per remap; no flush): latency-bound config, not a "
+                "bytes_per_step_total": 2 * n_total * R_moved * n_remaps,
+                "l2": (f"inputs larger than L2 ({2 * n * R_moved / 1e9:.2f} GB moved per remap per GPU vs 126 MB L2); "
+                       "no flush" if 2 * n * R_moved > (252 << 20) else
+                       f"inputs fit in L2 ({2 * n * R_moved} B per remap; no flush): latency-bound config, not a "
                        "bandwidth claim"),
                 "timing_regime": ("burst: timed right after the warm-up, like the burst copy peak"
                                   if args.soak_s <= 0 else f"after a {args.soak_s:.1f} s untimed soak"),
@@ -745,9 +827,7 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "peak_source": peak_src,
-                         "kernel": ("remap_chain_small_kernel (fused chain of latency-bound hops)" if fused_chain
-                                    else "remap_naive_kernel (direct path for remaps <= ADHA_SMALL_BYTES)"
-                                    if n * R <= small else "remap_tiled_kernel"),
+                         "kernel": kernel_name,
                          "algorithmic_bytes_per_launch": bytes_per_launch,
                          "avg_launch_ms": avg_launch_ms},
             "sustained": sustained,

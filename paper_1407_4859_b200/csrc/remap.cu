@@ -166,6 +166,14 @@ adha_status device_setup(const void* fn, int* n_sm, int threads = NTHREADS) {
 // Direct global->global kernel: the fallback beyond the tiled kernel's limits, and the
 // latency path for small remaps (a handful of KB, where one launch with small parameters
 // and one load/store per unit beats staging through shared memory).
+// a dst cluster whose region IS the region of its src cluster (adha_remap_regions aliasing, only
+// accepted for identity components): nothing moves there, so the direct path leaves its fields
+// and its region alone (adha.h: "left untouched")
+inline bool aliased(const uint8_t* src, const Layout& ls, const std::vector<uint64_t>& bs, const uint8_t* dst,
+                    const Layout& ld, const std::vector<uint64_t>& bd, int f) {
+    return (uintptr_t)src + bs[ls.cluster[f]] == (uintptr_t)dst + bd[ld.cluster[f]];
+}
+
 template <int NF>
 adha_status launch_naive_t(const uint8_t* src, const Layout& ls, const std::vector<uint64_t>& bs, uint8_t* dst,
                            const Layout& ld, const std::vector<uint64_t>& bd, int64_t lo, int64_t hi,
@@ -173,17 +181,20 @@ adha_status launch_naive_t(const uint8_t* src, const Layout& ls, const std::vect
     int n_sm = 0;
     adha_status s = device_setup(nullptr, &n_sm);
     if (s != ADHA_OK) return s;
+    std::vector<int> moved;
+    for (int f = 0; f < ls.n_fields; ++f)
+        if (!aliased(src, ls, bs, dst, ld, bd, f)) moved.push_back(f);
     auto P = std::make_unique<NaiveParamsT<NF>>();
-    for (int f0 = 0; f0 < ls.n_fields; f0 += NF) {
+    for (size_t f0 = 0; f0 < moved.size(); f0 += NF) {
         std::memset(P.get(), 0, sizeof(NaiveParamsT<NF>));
         P->src = (uint64_t)(uintptr_t)src;
         P->dst = (uint64_t)(uintptr_t)dst;
         P->n_records = hi - lo;
         P->lo = lo;
-        const int nf = std::min(NF, ls.n_fields - f0);
+        const int nf = (int)std::min<size_t>(NF, moved.size() - f0);
         P->n_fields = (uint32_t)nf;
         for (int k = 0; k < nf; ++k) {
-            const int f = f0 + k;
+            const int f = moved[f0 + k];
             const int cs = ls.cluster[f], cd = ld.cluster[f];
             uint32_t sbl = 0, dbl = 0;
             while ((1u << sbl) < ls.block[cs]) ++sbl;
@@ -203,11 +214,13 @@ adha_status launch_naive_t(const uint8_t* src, const Layout& ls, const std::vect
 adha_status launch_naive(const uint8_t* src, const Layout& ls, const std::vector<uint64_t>& bs, uint8_t* dst,
                          const Layout& ld, const std::vector<uint64_t>& bd, int64_t lo, int64_t hi,
                          cudaStream_t st) {
-    // dst clusters with padding or AoSoA blocks: zero their regions first (the copy fills the payload)
+    // dst clusters with padding or AoSoA blocks: zero their regions first (the copy fills the
+    // payload); an aliased cluster is the caller's src data and is not touched
     ZeroParams Z;
     std::memset(&Z, 0, sizeof Z);
     for (int c = 0; c < ld.n_clusters(); ++c) {
         if (ld.stride[c] == ld.payload(c) && ld.block[c] == 1) continue;
+        if (aliased(src, ls, bs, dst, ld, bd, ld.members[c][0])) continue;
         if (Z.n == ZMAX) {
             zero_kernel<<<256, 256, 0, st>>>(Z);
             Z.n = 0;
@@ -433,25 +446,32 @@ extern "C" adha_status adha_remap_regions(const void* const* src_regions, const 
         if (!a) return fail(ADHA_ERR_INVALID_ARG, "null src region " + std::to_string(c));
         if (a & 255) return fail(ADHA_ERR_ALIGNMENT, "src region " + std::to_string(c) + " not 256-byte aligned");
         ck.bs[c] = a;
-        spans.push_back({a, a + (uint64_t)n * ls.stride[c], 0, c});
+        spans.push_back({a, a + ls.region_bytes(c, n), 0, c});
     }
     for (int c = 0; c < ld.n_clusters(); ++c) {
         const uint64_t a = (uint64_t)(uintptr_t)dst_regions[c];
         if (!a) return fail(ADHA_ERR_INVALID_ARG, "null dst region " + std::to_string(c));
         if (a & 255) return fail(ADHA_ERR_ALIGNMENT, "dst region " + std::to_string(c) + " not 256-byte aligned");
         ck.bd[c] = a;
-        spans.push_back({a, a + (uint64_t)n * ld.stride[c], 1, c});
+        spans.push_back({a, a + ld.region_bytes(c, n), 1, c});
     }
+    // a dst region may BE the src region of its cluster only when the plan's component for that
+    // pair is an identity (same members, offsets, stride and block, no padding): nothing moves there
+    auto plan = get_plan(ls, ld);
+    auto identity_pair = [&](int cs, int cd) {
+        for (const auto& K : plan->comps)
+            if (K.identity && K.src_clusters[0] == cs && K.dst_clusters[0] == cd) return true;
+        return false;
+    };
     for (size_t i = 0; i < spans.size(); ++i)
         for (size_t j = i + 1; j < spans.size(); ++j) {
             const Span& x = spans[i];
             const Span& y = spans[j];
             if (!(x.lo < y.hi && y.lo < x.hi)) continue;
             if (x.side == 0 && y.side == 0) continue;                  // src regions may share memory
-            // a dst region may BE the src region of an identical cluster: nothing moves there
             const bool alias = x.side != y.side && x.lo == y.lo &&
-                               ls.members[x.side == 0 ? x.c : y.c] == ld.members[x.side == 0 ? y.c : x.c];
-            if (!alias) return fail(ADHA_ERR_OVERLAP, "regions overlap (only identical clusters may alias)");
+                               identity_pair(x.side == 0 ? x.c : y.c, x.side == 0 ? y.c : x.c);
+            if (!alias) return fail(ADHA_ERR_OVERLAP, "regions overlap (only identity clusters may alias)");
         }
     return remap_checked(nullptr, ls, nullptr, ld, n, ck, (cudaStream_t)stream);
 }
@@ -643,6 +663,10 @@ extern "C" adha_status adha_remap_plan_describe(const adha_layout* hs, const adh
         if (hs->L.width[f] != hd->L.width[f]) return fail(ADHA_ERR_LAYOUT_MISMATCH, "widths differ");
     auto plan = get_plan(hs->L, hd->L);
     std::string s = describe_plan(*plan, hs->L, hd->L);
+    // routing threshold of adha_remap for this pair (device dst): payload <= direct_bytes takes the
+    // direct kernel (ADHA_SMALL_BYTES overrides, read now)
+    s.pop_back();
+    s += ",\"direct_bytes\":" + std::to_string(direct_bytes(*plan)) + "}";
     *json_out = (char*)std::malloc(s.size() + 1);
     if (!*json_out) return fail(ADHA_ERR_OOM, "out of host memory");
     std::memcpy(*json_out, s.c_str(), s.size() + 1);

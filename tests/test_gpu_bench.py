@@ -36,7 +36,7 @@ def run_bench(args, env=None, torchrun=0):
 
 
 def test_bench_c2_contract():
-    d = run_bench(["--steps", "20", "--warmup", "3", "--sustained-s", "0.3", "--no-cpu-baseline"])
+    d = run_bench(["--config", "C2", "--steps", "20", "--warmup", "3", "--sustained-s", "0.3", "--no-cpu-baseline"])
     for k in KEYS:
         assert k in d, k
     assert d["metric"] == "remap GB/s (read+write)" and d["unit"] == "GB/s" and d["dtype"] == "u8"
@@ -59,10 +59,44 @@ def test_bench_c1_graph():
 
 
 def test_bench_two_ranks_share_gpu():
-    d = run_bench(["--gpus", "2", "--steps", "5", "--warmup", "3", "--sustained-s", "0", "--no-e2e",
-                   "--no-copy-ref"], env={"ADHA_BENCH_SHARE_GPU": "1"}, torchrun=2)
+    d = run_bench(["--config", "C2", "--gpus", "2", "--steps", "5", "--warmup", "3", "--sustained-s", "0",
+                   "--no-e2e", "--no-copy-ref"], env={"ADHA_BENCH_SHARE_GPU": "1"}, torchrun=2)
     assert d["n_gpus"] == 2 and d["scaling"] == "weak"
     assert d["config"]["n_records_total"] == 2 * d["config"]["n_records_per_rank"]
+
+
+def test_bench_default_is_c5_and_gpus_spawns_ranks():
+    """No --config: C5 (BASELINE.json's metric, "at 1/2/4/8 B200"), strong-scaled.  `--gpus 2`
+    WITHOUT torchrun re-launches bench.py as two ranks (here sharing the one GPU through
+    ADHA_BENCH_SHARE_GPU): n_gpus == 2 and the 8 GiB array is split two ways."""
+    d = run_bench(["--gpus", "2", "--steps", "5", "--warmup", "3", "--sustained-s", "0", "--no-e2e",
+                   "--no-copy-ref"], env={"ADHA_BENCH_SHARE_GPU": "1"})
+    assert d["config"]["workload"].startswith("C5") and d["scaling"] == "strong"
+    assert d["n_gpus"] == 2
+    c = d["config"]
+    assert c["n_records_total"] == 2 ** 33 // 80 and c["n_records_per_rank"] == c["n_records_total"] // 2
+    assert d["roofline"]["kernel"] == "remap_tiled_kernel" and d["value"] > 1000
+
+
+def test_bench_gpus_mismatch_fails():
+    """--gpus N under a launcher with another WORLD_SIZE is an error, not a silent 1-rank run."""
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "3"]
+    e = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT, env=e)
+    assert out.returncode != 0 and "WORLD_SIZE" in out.stderr
+
+
+def test_bench_c4m_moved_subset():
+    """C4M: the Medical AoSV->SoA edge through adha_remap_regions; 12 of 36 bytes per record move
+    (SPEC.md:221), and the line counts exactly those bytes."""
+    d = run_bench(["--config", "C4M", "--steps", "10", "--warmup", "3", "--sustained-s", "0",
+                   "--no-cpu-baseline"])
+    c = d["config"]
+    assert c["moved_bytes_per_record"] == 12 and c["record_bytes"] == 36
+    assert c["bytes_per_step_total"] == 2 * 12 * (2 ** 31 // 36)
+    assert d["roofline"]["algorithmic_bytes_per_launch"] == 2 * 12 * (2 ** 31 // 36)
+    assert d["e2e"]["d2h_bytes_per_step"] < d["e2e"]["h2d_bytes_per_step"]
+    assert d["value"] > 1000 and d["gpu_launches"] == 10
 
 
 @pytest.mark.parametrize("cfg", ["C2", "C4"])

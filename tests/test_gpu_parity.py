@@ -2,9 +2,9 @@
 
 Bit-exact is the bar (integer/byte work; SURVEY.md 8(c) c1 -- the result is
 unique).  Small N: element by element over the whole dst buffer, including the
-sentinel-filled gaps between regions.  Full BASELINE sizes: every byte at C2,
-sampled records (one output at a time from the oracle's address model) at C3,
-C4, C5, in the launch configuration bench.py times.
+sentinel-filled gaps between regions.  Full BASELINE sizes (C2, C3, C3R, each
+C4 hop, C5): every payload byte, C3/C4/C5 by record-range chunks against the
+oracle (exact by record locality), in the launch configuration bench.py times.
 """
 import os
 
@@ -13,7 +13,7 @@ import pytest
 
 from adha_inputs import config_widths, field_columns, tagged_columns, fill_random_device, SEED_BASE
 from oracle import remap as O
-from tests.gpu_util import SENT, run_remap, sample_records, gather_fields_dev, sentinel_dev, to_dev
+from tests.gpu_util import SENT, run_remap, sample_records, gather_fields_dev, sentinel_dev, to_dev, exact_chunked_check
 from tests.test_oracle_remap import set_partitions
 
 pytestmark = pytest.mark.gpu
@@ -216,19 +216,23 @@ def sampled_check(src, Ls_lab, dst, Ld_lab, widths, n, T, seed=0, extra=()):
             assert bool((gap == SENT).all())
 
 
-@pytest.mark.parametrize("cfg", ["C3", "C5"])
-def test_full_size_sampled(cfg):
-    if cfg == "C3":
-        widths, n, ls, ld = config_widths(64), 50_000_000, list(range(64)), c3_labels()
+@pytest.mark.parametrize("cfg", ["C3", "C3R", "C5"])
+def test_full_size_exact(cfg):
+    """The bench workloads at full size, EVERY payload byte against the oracle by record-range
+    chunks: C3 (50M x 320 B, SoA -> the 24-cluster hybrid), C3R (the seeded
+    random-program hybrid) and C5 (8 GiB AoS -> SoA), in the launch configuration bench.py times."""
+    if cfg in ("C3", "C3R"):
+        widths, n, ls = config_widths(64), 50_000_000, list(range(64))
+        ld = c3_labels() if cfg == "C3" else c3r_labels()
     else:
         widths, n, ls, ld = config_widths(16), 107_374_182, [0] * 16, list(range(16))
     Ls, Ld = A.Layout(widths, ls), A.Layout(widths, ld)
     src = torch.empty(Ls.nbytes(n), dtype=torch.uint8, device="cuda")
-    fill_random_device(src, SEED_BASE + (2 if cfg == "C3" else 4))
+    fill_random_device(src, SEED_BASE + {"C3": 2, "C3R": 6, "C5": 4}[cfg])
     dst = sentinel_dev(Ld.nbytes(n))
     A.remap(src, Ls, dst, Ld, n)
     torch.cuda.synchronize()
-    sampled_check(src, ls, dst, ld, widths, n, plan_T(widths, ls, ld))
+    assert exact_chunked_check(O, src, ls, dst, ld, widths, n) == n * sum(widths)
     del src, dst
     torch.cuda.empty_cache()
 
@@ -338,9 +342,8 @@ def test_c4_pdl_chain_full_size():
         b.fill_(SENT)
     A.remap_chain(bufs, lays, n)
     torch.cuda.synchronize()
-    for k in range(3):
-        sampled_check(bufs[k], labs[k], bufs[k + 1], labs[k + 1], widths, n, plan_T(widths, labs[k], labs[k + 1]),
-                      seed=k)
+    for k in range(3):       # every hop, every payload byte, against the oracle (record-range chunks)
+        assert exact_chunked_check(O, bufs[k], labs[k], bufs[k + 1], labs[k + 1], widths, n) == n * 36
     assert torch.equal(bufs[3], bufs[0])                    # AoS -> AoSV -> SoA -> AoS is the identity
 
 
@@ -407,6 +410,91 @@ def test_remap_regions_moves_only_changed_fields():
     # a non-identical alias is rejected
     with pytest.raises(A.AdhaError) as e:
         A.remap_regions([v_reg] + singles, Lv, [v_reg] + dst_v[1:] + singles, Ls, n)
+    assert e.value.name == "ADHA_ERR_OVERLAP"
+
+
+@pytest.mark.parametrize("n", [50_003, 1_000_003])
+def test_remap_regions_medical_edge_both_paths(n, small_path):
+    """The Medical AoSV -> SoA edge through adha_remap_regions at a size the default routing
+    sends to the direct kernel (1.8 MB) and one it sends to the tiled kernel (36 MB), both
+    forced tiled too: the six aliased singleton regions keep their bytes, V1..V3 match the
+    oracle (PAPER.md:56-57, 146; SPEC.md:221)."""
+    widths = [4] * 9
+    aosv, soa = [0, 0, 0, 1, 2, 3, 4, 5, 6], list(range(9))
+    Lv, Ls = A.Layout(widths, aosv), A.Layout(widths, soa)
+    cols = field_columns(22 + n, n, widths)
+    exp_cols = O.unpack(oracle_dst(O.pack(cols, widths, aosv, n), aosv, soa, widths, n), widths, soa, n)
+    v_reg = to_dev(np.ascontiguousarray(np.concatenate([cols[0], cols[1], cols[2]], 1)).reshape(-1))
+    singles = [to_dev(np.ascontiguousarray(cols[f]).reshape(-1)) for f in range(3, 9)]
+    dst_v = [sentinel_dev(4 * n) for _ in range(3)]
+    A.remap_regions([v_reg] + singles, Lv, dst_v + singles, Ls, n)
+    torch.cuda.synchronize()
+    for f in range(3):
+        assert np.array_equal(dst_v[f].cpu().numpy().reshape(n, 4), exp_cols[f])
+    for k, f in enumerate(range(3, 9)):
+        assert np.array_equal(singles[k].cpu().numpy().reshape(n, 4), exp_cols[f])
+
+
+@pytest.mark.parametrize("n", [1003, 200_003])
+def test_remap_regions_blocked_alias_untouched(n, small_path):
+    """An aliased identity cluster with AoSoA blocks ({a,b}@8 on both sides) is left untouched
+    by both kernel paths -- including the slots past N in its last block, which a zero pass
+    would overwrite (adha.h adha_remap_regions: "left untouched") -- while {c},{d} -> {c,d}
+    matches the oracle."""
+    widths = [4, 4, 4, 4]
+    ls, bs = [0, 0, 1, 2], [8, 8, 1, 1]
+    ld, bd = [0, 0, 1, 1], [8, 8, 1, 1]
+    Ls, Ld = A.Layout(widths, ls, blocks=bs), A.Layout(widths, ld, blocks=bd)
+    cols = field_columns(77 + n, n, widths)
+    ab = O.pack_ex(cols[:2], [4, 4], [0, 0], n, [8, 8], False)
+    d = O.field_addresses_ex([4, 4], [0, 0], n, [8, 8], False)
+    payload = np.zeros(ab.size, bool)
+    i = np.arange(n, dtype=np.int64)
+    for f in range(2):
+        a = O.addr_ex(d, f, i)
+        payload[(a[:, None] + np.arange(4)[None, :]).reshape(-1)] = True
+    ab[~payload] = 0x77                        # slots past N in the last block: must survive
+    x = to_dev(ab)
+    c, dd = to_dev(np.ascontiguousarray(cols[2]).reshape(-1)), to_dev(np.ascontiguousarray(cols[3]).reshape(-1))
+    cd = sentinel_dev(8 * n)
+    A.remap_regions([x, c, dd], Ls, [x, cd], Ld, n)
+    torch.cuda.synchronize()
+    assert np.array_equal(x.cpu().numpy(), ab)
+    assert np.array_equal(cd.cpu().numpy().reshape(n, 8), np.concatenate([cols[2], cols[3]], 1))
+
+
+def test_remap_regions_rejects_non_identity_alias():
+    """Aliasing needs an identity component, not only equal member sets: a padded (aligned)
+    cluster, or one whose AoSoA block changes, is rejected with OVERLAP; overlap spans cover the
+    whole blocked region (ceil(N/B)*B records), not N*stride."""
+    n = 1000
+    t = torch
+    w = [1, 4, 4]
+    # {a,b} aligned (stride 8, padding) -> {a,b} packed: same members, not an identity
+    La = A.Layout(w, [0, 0, 1], aligned=True)
+    Lp = A.Layout(w, [0, 0, 1])
+    r0, r1 = t.zeros(8 * n, dtype=t.uint8, device="cuda"), t.zeros(4 * n, dtype=t.uint8, device="cuda")
+    o1 = t.zeros(4 * n, dtype=t.uint8, device="cuda")
+    with pytest.raises(A.AdhaError) as e:
+        A.remap_regions([r0, r1], La, [r0, o1], Lp, n)
+    assert e.value.name == "ADHA_ERR_OVERLAP"
+    # {a,b}@4 -> {a,b}@8: the block changes
+    w2 = [4, 4, 4]
+    L4 = A.Layout(w2, [0, 0, 1], blocks=[4, 4, 1])
+    L8 = A.Layout(w2, [0, 0, 1], blocks=[8, 8, 1])
+    s0 = t.zeros(8 * (n + 8), dtype=t.uint8, device="cuda")
+    with pytest.raises(A.AdhaError) as e:
+        A.remap_regions([s0, r1], L4, [s0, o1], L8, n)
+    assert e.value.name == "ADHA_ERR_OVERLAP"
+    # a 16-byte field in 32-record blocks: 1 record occupies 512 region bytes, so a region 256
+    # bytes further on overlaps it (N*stride = 16 would not see it)
+    w3 = [16, 4]
+    Lsrc = A.Layout(w3, [0, 1])
+    Ldst = A.Layout(w3, [0, 1], blocks=[32, 1])
+    big = t.zeros(4096, dtype=t.uint8, device="cuda")
+    s_a, s_b = t.zeros(256, dtype=t.uint8, device="cuda"), t.zeros(256, dtype=t.uint8, device="cuda")
+    with pytest.raises(A.AdhaError) as e:
+        A.remap_regions([s_a, s_b], Lsrc, [big[:512], big[256:512]], Ldst, 1)
     assert e.value.name == "ADHA_ERR_OVERLAP"
 
 
