@@ -48,6 +48,18 @@ cases = [
     ("g2 AoS->SoA (byte groups)", [2, 4, 6, 4] * 4, [0] * 16, list(range(16)), 20_000_000),
     ("b24 SoA->AoS (byte groups)", [1] * 24 + [8], list(range(25)), [0] * 25, 20_000_000),
 ]
+if "--small" in sys.argv:
+    # small and mid-size remaps forced onto the tiled kernel: where does the fixed cost go?
+    os.environ["ADHA_SMALL_BYTES"] = "0"
+    import bench
+    c3 = bench.c3_labels()[0]
+    w64 = [8 if i % 4 == 3 else 4 for i in range(64)]
+    cases = [(f"{nm} {mb} MB", w, ls, ld, max(1, (mb << 20) // sum(w)))
+             for nm, w, ls, ld in [("C2 AoS->SoA", w16, [0] * 16, list(range(16))),
+                                   ("C3 SoA->hybrid", w64, list(range(64)), c3),
+                                   ("g2 AoS->SoA", [2, 4, 6, 4] * 4, [0] * 16, list(range(16))),
+                                   ("Medical AoSV->SoA", [4] * 9, [0, 0, 0, 1, 2, 3, 4, 5, 6], list(range(9)))]
+             for mb in (1, 32)]
 stream = torch.cuda.current_stream().cuda_stream
 for name, w, ls, ld, n in cases:
     Ls, Ld = layout(w, ls), layout(w, ld)
@@ -73,6 +85,7 @@ for name, w, ls, ld, n in cases:
     print(f"{name:28s} {2 * n * R / ms / 1e6:6.0f} GB/s  per tile & warp (clk): wait_full {per[0]:7.0f}  "
           f"permute {per[1]:6.0f}  barrier {per[2]:6.0f}  copy_out {per[3]:6.0f}  (sum {tot:6.0f}; "
           f"{100 * per[0] / tot:4.1f}% waiting for data)  producer wait_empty/tile {p[5] / (tiles / 8):7.0f}  "
-          f"tails/warp {p[7] / 8 / 148 / reps:6.0f}", flush=True)
+          f"tails/warp {p[7] / 8 / 148 / reps:6.0f}  tiles/CTA {tiles / 8 / 148 / reps:5.1f}  "
+          f"{ms * 1e3:7.1f} us/remap", flush=True)
     del a, b
     torch.cuda.empty_cache()
