@@ -173,83 +173,166 @@ inline bool is_cut(uint32_t x) {   // pseudo-random 1-in-512 cut points along th
 }
 
 // The permutation's cycles as segments of at most IP_SEG positions.  Cycles are cut at pseudo-
-// random cut points; the walks from the cut points are independent (one per thread chunk, so the
-// random accesses of many walks overlap); cycles without a cut point are walked afterwards.
-// Fixed points are dropped.  P is consumed (entries set to NONE_SLOT as they are placed).
-void build_segments(std::vector<uint32_t>& P, uint64_t nslot, unsigned nthr, InplacePlan* p) {
+// random cut points (1 in 512 slots); the walk from each cut point to the next one on its cycle
+// is independent of the others.  Walking is a chain of dependent random loads of P, so each host
+// thread advances WALK_LANES walks in turn (that many cache misses in flight instead of one); the
+// walks' positions are then placed in cut order with prefix sums, in parallel.  Cycles without a
+// cut point (short ones) are walked afterwards.  Fixed points are dropped.  Entries of P are set
+// to NONE_SLOT as they are placed by the cut walks.
+constexpr unsigned WALK_LANES = 16;
+
+void build_segments(uvector<uint32_t>& P, uint64_t nslot, unsigned nthr, InplacePlan* p) {
+    // cut points and fixed points, per thread chunk (concatenated in chunk order: cuts ascend)
+    std::vector<std::vector<uint32_t>> cut_parts(nthr);
+    std::vector<uint64_t> fixed_parts(nthr, 0);
+    parallel_for(nthr, nslot, [&](unsigned chunk, uint64_t x0, uint64_t x1) {
+        auto& cp = cut_parts[chunk];
+        uint64_t fx = 0;
+        for (uint64_t x = x0; x < x1; ++x) {
+            const uint32_t y = P[x];
+            if (y == NONE_SLOT) continue;
+            if (y == (uint32_t)x) { P[x] = NONE_SLOT; ++fx; continue; }
+            if (is_cut((uint32_t)x)) cp.push_back((uint32_t)x);
+        }
+        fixed_parts[chunk] = fx;
+    });
     std::vector<uint32_t> cuts;
-    for (uint64_t x = 0; x < nslot; ++x) {
-        if (P[x] == NONE_SLOT) continue;
-        if (P[x] == (uint32_t)x) { P[x] = NONE_SLOT; ++p->fixed_slots; continue; }
-        if (is_cut((uint32_t)x)) cuts.push_back((uint32_t)x);
+    for (unsigned c = 0; c < nthr; ++c) {
+        cuts.insert(cuts.end(), cut_parts[c].begin(), cut_parts[c].end());
+        p->fixed_slots += fixed_parts[c];
+        std::vector<uint32_t>().swap(cut_parts[c]);
     }
+    const uint64_t nc = cuts.size();
     // walk from every cut point up to (not including) the next cut point on its cycle
-    struct Walk { std::vector<uint32_t> pos; std::vector<uint32_t> len; std::vector<uint32_t> next_cut; };
-    const unsigned nw = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(nthr, cuts.size()));
-    std::vector<Walk> walks(nw);
-    parallel_for(nw, cuts.size(), [&](unsigned chunk, uint64_t i0, uint64_t i1) {
-        Walk& w = walks[chunk];
-        for (uint64_t i = i0; i < i1; ++i) {
-            uint32_t y = cuts[i];
-            uint32_t L = 0;
-            do {
-                w.pos.push_back(y);
-                ++L;
-                y = P[y];
-            } while (!is_cut(y));
-            w.len.push_back(L);
-            w.next_cut.push_back(y);
+    struct Walked { uint32_t ci, len; uint64_t off; };        // cut index, length, offset in pos
+    struct Out { std::vector<uint32_t> pos; std::vector<Walked> w; };
+    const unsigned nw = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(nthr, nc));
+    std::vector<Out> outs(nw);
+    std::vector<uint32_t> len(nc), next_cut(nc);
+    parallel_for(nw, nc, [&](unsigned chunk, uint64_t i0, uint64_t i1) {
+        Out& o = outs[chunk];
+        o.pos.reserve((i1 - i0) * 600);
+        o.w.reserve(i1 - i0);
+        struct Lane { uint32_t ci, y; std::vector<uint32_t> buf; bool live; };
+        Lane lane[WALK_LANES];
+        uint64_t next = i0;
+        unsigned live = 0;
+        auto start = [&](Lane& L) {
+            L.live = next < i1;
+            if (!L.live) return;
+            L.ci = (uint32_t)next++;
+            L.y = cuts[L.ci];
+            L.buf.clear();
+            ++live;
+        };
+        for (auto& L : lane) { L.buf.reserve(1024); start(L); }
+        while (live) {
+            for (auto& L : lane) {
+                if (!L.live) continue;
+                L.buf.push_back(L.y);
+                const uint32_t ny = P[L.y];
+                P[L.y] = NONE_SLOT;                  // placed (no other walk visits this slot)
+                __builtin_prefetch(&P[ny]);
+                L.y = ny;
+                if (is_cut(ny)) {
+                    o.w.push_back({L.ci, (uint32_t)L.buf.size(), (uint64_t)o.pos.size()});
+                    o.pos.insert(o.pos.end(), L.buf.begin(), L.buf.end());
+                    len[L.ci] = (uint32_t)L.buf.size();
+                    next_cut[L.ci] = ny;
+                    --live;
+                    start(L);
+                }
+            }
         }
     });
-    for (const Walk& w : walks)
-        for (uint32_t y : w.pos) P[y] = NONE_SLOT;        // placed
-    // concatenate in cut order; split long walks into segments of <= IP_SEG
-    std::vector<uint32_t> first_seg(cuts.size()), last_seg(cuts.size());
+    // placement in cut order: seq offset and first segment of every walk (prefix sums)
+    std::vector<uint64_t> seq_at(nc + 1, 0), seg_at(nc + 1, 0);
+    for (uint64_t i = 0; i < nc; ++i) {
+        seq_at[i + 1] = seq_at[i] + len[i];
+        seg_at[i + 1] = seg_at[i] + (len[i] + IP_SEG - 1) / IP_SEG;
+    }
     p->seq.reserve(p->content_slots + p->junk_slots);
-    size_t ci = 0;
-    for (const Walk& w : walks) {
-        size_t off = 0;
-        for (size_t k = 0; k < w.len.size(); ++k, ++ci) {
-            const uint32_t L = w.len[k];
-            const uint32_t start = (uint32_t)p->seq.size();
-            p->seq.insert(p->seq.end(), w.pos.begin() + off, w.pos.begin() + off + L);
-            off += L;
-            first_seg[ci] = (uint32_t)p->segs.size();
-            for (uint32_t a = 0; a < L; a += IP_SEG) {
-                const uint32_t sidx = (uint32_t)p->segs.size();
-                p->segs.push_back({start + a, std::min<uint32_t>(IP_SEG, L - a), a ? sidx - 1 : 0u, 0});
+    p->seq.resize(seq_at[nc]);
+    p->segs.resize(seg_at[nc]);
+    parallel_for(nw, nw, [&](unsigned, uint64_t c0, uint64_t c1) {
+        for (uint64_t c = c0; c < c1; ++c)
+            for (const Walked& w : outs[c].w) {
+                const uint32_t* src = outs[c].pos.data() + w.off;
+                std::memcpy(p->seq.data() + seq_at[w.ci], src, (size_t)w.len * 4);
+                const uint32_t s0 = (uint32_t)seg_at[w.ci], start = (uint32_t)seq_at[w.ci];
+                for (uint32_t a = 0, si = s0; a < w.len; a += IP_SEG, ++si)
+                    p->segs[si] = {start + a, std::min<uint32_t>(IP_SEG, w.len - a), a ? si - 1 : 0u, 0};
             }
-            last_seg[ci] = (uint32_t)p->segs.size() - 1;
+    });
+    // the last slot of walk i precedes the first slot of the walk starting at next_cut[i]
+    // (after the placement above: the first segment of that walk must exist before its pred is set)
+    parallel_for(nw, nc, [&](unsigned, uint64_t i0, uint64_t i1) {
+        for (uint64_t i = i0; i < i1; ++i) {
+            const uint64_t nxt = (uint64_t)(std::lower_bound(cuts.begin(), cuts.end(), next_cut[i]) - cuts.begin());
+            p->segs[seg_at[nxt]].pred = (uint32_t)(seg_at[i + 1] - 1);
         }
-    }
-    // the first segment of cut i's walk receives the last slot of the walk that reaches cut i
-    ci = 0;
-    for (const Walk& w : walks)
-        for (size_t k = 0; k < w.len.size(); ++k, ++ci) {
-            const size_t nxt = (size_t)(std::lower_bound(cuts.begin(), cuts.end(), w.next_cut[k]) - cuts.begin());
-            p->segs[first_seg[nxt]].pred = last_seg[ci];
-        }
+    });
+    outs.clear();
     p->cycles = 0;   // cut walks do not count cycles; the uncut ones below do
-    // cycles with no cut point
-    for (uint64_t x0 = 0; x0 < nslot; ++x0) {
-        if (P[x0] == NONE_SLOT) continue;
-        const uint32_t start = (uint32_t)p->seq.size();
-        uint64_t y = x0;
-        do {
-            p->seq.push_back((uint32_t)y);
-            const uint32_t ny = P[y];
-            P[y] = NONE_SLOT;
-            y = ny;
-        } while (y != x0);
-        const uint32_t L = (uint32_t)p->seq.size() - start;
-        const uint32_t first = (uint32_t)p->segs.size();
-        const uint32_t ns = (L + IP_SEG - 1) / IP_SEG;
-        for (uint32_t s = 0; s < ns; ++s) {
-            const uint32_t a = start + s * IP_SEG;
-            p->segs.push_back({a, std::min<uint32_t>(IP_SEG, start + L - a), s == 0 ? first + ns - 1 : first + s - 1, 0});
+    // Cycles with no cut point (shorter ones): the slot with the smallest index leads its cycle.
+    // Every thread tests the unplaced slots of its range -- a walk that meets a smaller index
+    // stops: not the leader -- and walks the cycles it leads into a local list; P is only read
+    // here and the lists are concatenated in range order afterwards.
+    struct Cyc { std::vector<uint32_t> pos, len; };
+    std::vector<Cyc> cyc(nthr);
+    parallel_for(nthr, nslot, [&](unsigned chunk, uint64_t x0, uint64_t x1) {
+        Cyc& c = cyc[chunk];
+        for (uint64_t x = x0; x < x1; ++x) {
+            if (P[x] == NONE_SLOT) continue;
+            uint32_t y = P[x];
+            while (y != (uint32_t)x && y > (uint32_t)x) y = P[y];
+            if (y != (uint32_t)x) continue;          // a smaller slot on the cycle leads it
+            const size_t at = c.pos.size();
+            y = (uint32_t)x;
+            do {
+                c.pos.push_back(y);
+                y = P[y];
+            } while (y != (uint32_t)x);
+            c.len.push_back((uint32_t)(c.pos.size() - at));
         }
-        ++p->cycles;
+    });
+    for (const Cyc& c : cyc) {
+        size_t off = 0;
+        for (uint32_t L : c.len) {
+            const uint32_t start = (uint32_t)p->seq.size();
+            p->seq.insert(p->seq.end(), c.pos.begin() + off, c.pos.begin() + off + L);
+            off += L;
+            const uint32_t first = (uint32_t)p->segs.size();
+            const uint32_t ns = (L + IP_SEG - 1) / IP_SEG;
+            for (uint32_t s = 0; s < ns; ++s) {
+                const uint32_t a = start + s * IP_SEG;
+                p->segs.push_back({a, std::min<uint32_t>(IP_SEG, start + L - a), s == 0 ? first + ns - 1 : first + s - 1, 0});
+            }
+            ++p->cycles;
+        }
     }
+    // (P is not consumed by the uncut pass; the caller drops it)
+}
+
+// ADHA_IP_VERIFY=1 (tests): the segments against the permutation they were built from -- every
+// moved slot once, consecutive positions of a segment consecutive on the cycle, and every
+// segment's predecessor ending on the slot whose content its first position receives.
+std::string verify_segments(const uvector<uint32_t>& P0, const InplacePlan& p) {
+    std::vector<uint8_t> seen(P0.size(), 0);
+    for (uint32_t x : p.seq) {
+        if (x >= P0.size() || seen[x]) return "slot listed twice or out of range";
+        seen[x] = 1;
+    }
+    for (uint64_t x = 0; x < P0.size(); ++x)
+        if (P0[x] != NONE_SLOT && P0[x] != (uint32_t)x && !seen[x]) return "moved slot missing from the segments";
+    for (const IpSeg& sg : p.segs) {
+        if (sg.len < 1 || sg.len > IP_SEG || (uint64_t)sg.start + sg.len > p.seq.size()) return "segment bounds";
+        for (uint32_t k = 0; k + 1 < sg.len; ++k)
+            if (P0[p.seq[sg.start + k]] != p.seq[sg.start + k + 1]) return "segment not along its cycle";
+        const IpSeg& pr = p.segs.at(sg.pred);
+        if (P0[p.seq[pr.start + pr.len - 1]] != p.seq[sg.start]) return "predecessor segment mismatch";
+    }
+    return "";
 }
 
 }  // namespace
@@ -385,15 +468,19 @@ adha_status inplace_plan_build(const Layout& ls, const Layout& ld, int64_t n, In
     const uint64_t nslot = (total + S - 1) / S;
     if (nslot >= 0xFFFFFFFFull) return fail(ADHA_ERR_TOO_LARGE, "in-place remap: more than 2^32 slots");
     constexpr uint32_t NONE = NONE_SLOT;
-    std::vector<uint32_t> P;
-    std::vector<uint8_t> in_d;
+    uvector<uint32_t> P;
+    uvector<uint8_t> in_d;
     p->seq.clear();
     p->segs.clear();
     p->content_slots = p->moved_slots = p->fixed_slots = p->junk_slots = p->cycles = 0;
     if (m > 0) {
         const unsigned nthr = plan_threads(nslot);
-        P.assign(nslot, NONE);
-        in_d.assign(nslot, 0);
+        P.resize(nslot);
+        in_d.resize(nslot);
+        parallel_for(nthr, nslot, [&](unsigned, uint64_t x0, uint64_t x1) {
+            std::fill(P.begin() + x0, P.begin() + x1, NONE);
+            std::fill(in_d.begin() + x0, in_d.begin() + x1, (uint8_t)0);
+        });
         // per src cluster, per unit column k: slots s0 + t*K + k (t < m) -> d0 + t*Kd (+ k when raw)
         struct Col { uint64_t s0, d0; uint32_t K, Kd, k; bool raw; };
         std::vector<Col> colv;
@@ -426,18 +513,35 @@ adha_status inplace_plan_build(const Layout& ls, const Layout& ld, int64_t n, In
             cnt[chunk] = k;
         });
         for (uint64_t k : cnt) p->content_slots += k;
-        std::vector<uint32_t> free_in, free_out;   // dst-only slots, src-only slots
-        for (uint64_t x = 0; x < nslot; ++x) {
-            const bool ins = P[x] != NONE;
-            if (in_d[x] && !ins) free_in.push_back((uint32_t)x);
-            if (ins && !in_d[x]) free_out.push_back((uint32_t)x);
+        std::vector<uint32_t> free_in, free_out;   // dst-only slots, src-only slots (ascending)
+        {
+            std::vector<std::vector<uint32_t>> fi(nthr), fo(nthr);
+            parallel_for(nthr, nslot, [&](unsigned chunk, uint64_t x0, uint64_t x1) {
+                for (uint64_t x = x0; x < x1; ++x) {
+                    const bool ins = P[x] != NONE;
+                    if (in_d[x] && !ins) fi[chunk].push_back((uint32_t)x);
+                    if (ins && !in_d[x]) fo[chunk].push_back((uint32_t)x);
+                }
+            });
+            for (unsigned c = 0; c < nthr; ++c) {
+                free_in.insert(free_in.end(), fi[c].begin(), fi[c].end());
+                free_out.insert(free_out.end(), fo[c].begin(), fo[c].end());
+            }
         }
         if (free_in.size() != free_out.size()) return fail(ADHA_ERR_UNSUPPORTED, "in-place plan: slot count mismatch");
         // a dst slot whose old bytes are not content (src tail, gap) receives content; its junk goes
         // to a src-only slot (which becomes dst tail / gap): the permutation closes on U
         for (size_t i = 0; i < free_in.size(); ++i) P[free_in[i]] = free_out[i];
         p->junk_slots = free_in.size();
+        const char* ve = std::getenv("ADHA_IP_VERIFY");
+        const bool verify = ve && *ve == '1';
+        uvector<uint32_t> P0;
+        if (verify) P0 = P;
         build_segments(P, nslot, nthr, p);
+        if (verify) {
+            const std::string why = verify_segments(P0, *p);
+            if (!why.empty()) return fail(ADHA_ERR_PLANNER, "in-place plan verification: " + why);
+        }
         p->moved_slots = p->seq.size();
         if (p->seq.size() >= 0xFFFFFFFFull) return fail(ADHA_ERR_TOO_LARGE, "in-place remap: too many slots");
     }

@@ -19,6 +19,28 @@
 // (the tail) are saved to the workspace first and written to their dst positions last.
 #pragma once
 
+#include <memory>
+#include <utility>
+#include <vector>
+
+namespace adha {
+// std::allocator whose default construction leaves trivial values uninitialised: the plan's
+// large index arrays (tens of MB at C3's size) are filled in parallel, not zeroed serially first
+template <class T>
+struct UninitAlloc : std::allocator<T> {
+    using std::allocator<T>::allocator;
+    template <class U>
+    struct rebind { using other = UninitAlloc<U>; };
+    template <class U, class... Args>
+    void construct(U* p, Args&&... args) {
+        if constexpr (sizeof...(Args) == 0) ::new ((void*)p) U;
+        else ::new ((void*)p) U(std::forward<Args>(args)...);
+    }
+};
+template <class T>
+using uvector = std::vector<T, UninitAlloc<T>>;
+}  // namespace adha
+
 #include <cstdint>
 #include <vector>
 
@@ -79,7 +101,7 @@ struct InplacePlan {
     std::vector<IpCol> cols;             // column tables of pre then post clusters
     uint32_t max_tile = 0;               // shared memory of the largest rewritten tile (with padding)
     uint32_t max_tab = 0;                // shared memory of the largest column table
-    std::vector<uint32_t> seq;           // slot indices, cycles in order (slot j -> next on its cycle)
+    uvector<uint32_t> seq;               // slot indices, cycles in order (slot j -> next on its cycle)
     std::vector<IpSeg> segs;
     std::vector<IpTailField> tail_fields;
     // statistics

@@ -25,10 +25,26 @@ using namespace adha::ptx;
 constexpr uint32_t PMAX = 4;                   // bulk-load pieces per producer lane per tile
 constexpr uint32_t VMAX = 12;                  // 12 * 16 B * 256 threads = 49152 B >= stage_bytes
 
-__device__ __forceinline__ uint32_t copy_plan(const TiledParams& p, uint32_t c_lo, uint32_t T, uint32_t total,
-                                              uint32_t tid, uint64_t (&gofs)[VMAX], uint32_t (&gstep)[VMAX]) {
+// dst cluster descriptor c: from the shared-memory copy (dcl != 0, unit mode) or the parameters
+struct DstDesc {
+    uint64_t region;
+    uint32_t stride, smem;
+};
+__device__ __forceinline__ DstDesc dst_desc(const TiledParams& p, uint32_t dcl, uint32_t c) {
+    if (dcl) {
+        const uint4 v = lds128(dcl + 16 * c);
+        return {(uint64_t)v.x | ((uint64_t)v.y << 32), v.z, v.w};
+    }
+    return {p.dstc[c].region, p.dstc[c].stride, p.dstc[c].smem};
+}
+
+__device__ __forceinline__ uint32_t copy_plan(const TiledParams& p, uint32_t dcl, uint32_t c_lo, uint32_t T,
+                                              uint32_t total, uint32_t tid, uint64_t (&gofs)[VMAX],
+                                              uint32_t (&gstep)[VMAX]) {
     constexpr uint32_t NT = NCONS * 32;
-    uint32_t c = c_lo, cbeg = 0, cend = T * p.dstc[c].stride;
+    uint32_t c = c_lo;
+    DstDesc d = dst_desc(p, dcl, c);
+    uint32_t cbeg = 0, cend = T * d.stride;
     uint32_t nv = 0;
 #pragma unroll
     for (uint32_t u = 0; u < VMAX; ++u) {
@@ -38,13 +54,14 @@ __device__ __forceinline__ uint32_t copy_plan(const TiledParams& p, uint32_t c_l
         if (b < total) {
             while (b >= cend) {
                 ++c;
+                d = dst_desc(p, dcl, c);
                 cbeg = cend;
-                cend = cbeg + T * p.dstc[c].stride;
+                cend = cbeg + T * d.stride;
             }
-            gofs[u] = p.dstc[c].region + (b - cbeg);
+            gofs[u] = d.region + (b - cbeg);
             // the per-tile step T*stride is a multiple of 128; its low 7 bits carry the chunk's
             // padding in the output stage / 32 (smem offset - packed offset = 32 * chunk index)
-            gstep[u] = (cend - cbeg) | ((p.dstc[c].smem - cbeg) >> 5);
+            gstep[u] = (cend - cbeg) | ((d.smem - cbeg) >> 5);
             nv = u + 1;
         }
     }
@@ -221,15 +238,32 @@ __global__ void __launch_bounds__(TMAC ? NTHREADS_TMA : NTHREADS, 1)
             ADHA_PT(const long long pt0 = clock64());
             mbar_wait(empty0 + 8 * stage, phase ^ 1);
             ADHA_PT(const long long pt1 = clock64(); pw += pt1 - pt0);
-            if (lane == 0) mbar_arrive_expect_tx(full0 + 8 * stage, p.comp[k].tile_bytes);
-            __syncwarp();
             const uint32_t ib = in0 + stage * p.stage_bytes;
+            if (p.comp[k].flags & CF_LDGSTS) {
+                // Small src chunks (many SoA regions, short tiles): each TMA bulk copy has a fixed
+                // cost in the SM's TMA unit (64 chunks of 128 B took ~8 us per tile), so the warp
+                // copies the tile itself with 16-byte cp.async, 512 bytes per instruction; each
+                // lane's copies arrive on `full` when they land, lane 0's arrive closes the count.
+                const uint32_t T = p.comp[k].T;
+                for (uint32_t c = p.comp[k].sc_lo; c < p.comp[k].sc_hi; ++c) {
+                    const uint32_t bytes = T * p.srcc[c].stride;
+                    const uint8_t* g = (const uint8_t*)(p.src + p.srcc[c].region) + (uint64_t)lt * bytes;
+                    const uint32_t sm = ib + p.srcc[c].smem;
+                    for (uint32_t o = lane * 16; o < bytes; o += 32 * 16) cp_async16(sm + o, g + o);
+                }
+                cp_async_mbar_arrive(full0 + 8 * stage);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(full0 + 8 * stage);
+            } else {
+                if (lane == 0) mbar_arrive_expect_tx(full0 + 8 * stage, p.comp[k].tile_bytes);
+                __syncwarp();
 #pragma unroll
-            for (uint32_t q = 0; q < PMAX; ++q) {
-                if (q < np) {
-                    const void* g = (const void*)(pg[q] + (uint64_t)lt * pstep[q]);
-                    if (p.l2_hints & 1) bulk_load_hint(ib + psm[q], g, pbytes[q], full0 + 8 * stage, pol);
-                    else bulk_load(ib + psm[q], g, pbytes[q], full0 + 8 * stage);
+                for (uint32_t q = 0; q < PMAX; ++q) {
+                    if (q < np) {
+                        const void* g = (const void*)(pg[q] + (uint64_t)lt * pstep[q]);
+                        if (p.l2_hints & 1) bulk_load_hint(ib + psm[q], g, pbytes[q], full0 + 8 * stage, pol);
+                        else bulk_load(ib + psm[q], g, pbytes[q], full0 + 8 * stage);
+                    }
                 }
             }
             ADHA_PT(pi += clock64() - pt1);
@@ -241,6 +275,40 @@ __global__ void __launch_bounds__(TMAC ? NTHREADS_TMA : NTHREADS, 1)
 
     // ---------------------------------------------------------------- consumers
     const uint32_t tid = threadIdx.x;
+    // Unit mode: copy the entry table (off | sc | dc, the n_ent entries in use) and the cluster
+    // descriptors from the kernel parameters into shared memory once.  A component switch then
+    // reads its lanes' entries with LDS; from the parameters every lane-divergent index is a
+    // serialised constant-bank load (7 per entry: ~50 us for C3's 24 components at small N).
+    // The copy overlaps the producer's first TMA loads.
+    // Byte-group mode: the ByteGroups in use (13 words each) and the cluster descriptors, likewise.
+    // 128-bit loads: a lane-divergent constant load costs one access per distinct address, so
+    // 16 bytes per access instead of 4 (the tables and descriptors are 16-byte aligned).
+    uint32_t tbl = out0 + p.s_out * p.stage_bytes, scl, dcl, n4 = 0;
+    if constexpr (NG == 0) {
+        n4 = (p.n_ent + 15) & ~15u;                    // <= NENT (a multiple of 16)
+        scl = tbl + 6 * n4;
+        const uint4* offv = reinterpret_cast<const uint4*>(et.off);
+        const uint4* scv = reinterpret_cast<const uint4*>(et.sc);
+        const uint4* dcv = reinterpret_cast<const uint4*>(et.dc);
+        for (uint32_t i = tid; i < n4 / 4; i += NCONS * 32) sts128(tbl + 16 * i, offv[i]);
+        for (uint32_t i = tid; i < n4 / 16; i += NCONS * 32) {
+            sts128(tbl + 4 * n4 + 16 * i, scv[i]);
+            sts128(tbl + 5 * n4 + 16 * i, dcv[i]);
+        }
+    } else {
+        const uint32_t gbytes = ((uint32_t)sizeof(ByteGroup) * p.n_ent + 15) & ~15u;   // <= sizeof(et.g)
+        const uint4* gv = reinterpret_cast<const uint4*>(et.g);
+        for (uint32_t i = tid; i < gbytes / 16; i += NCONS * 32) sts128(tbl + 16 * i, gv[i]);
+        scl = tbl + gbytes;
+    }
+    dcl = scl + 16 * p.n_srcc;
+    {
+        const uint4* sv = reinterpret_cast<const uint4*>(p.srcc);
+        const uint4* dv = reinterpret_cast<const uint4*>(p.dstc);
+        for (uint32_t i = tid; i < p.n_srcc; i += NCONS * 32) sts128(scl + 16 * i, sv[i]);
+        for (uint32_t i = tid; i < p.n_dstc; i += NCONS * 32) sts128(dcl + 16 * i, dv[i]);
+        named_bar_sync(1, NCONS * 32);
+    }
     const uint64_t spol = policy_evict_first();
     uint32_t ioff[EMAX], ooff[EMAX], din[EMAX], dout[EMAX];
     // byte-group mode: per slot j, source words m and output words o of this lane's group
@@ -259,6 +327,7 @@ __global__ void __launch_bounds__(TMAC ? NTHREADS_TMA : NTHREADS, 1)
     {
         const int64_t gid = (int64_t)blockIdx.x * (NCONS * 32) + tid;
         const int64_t gstride = (int64_t)gridDim.x * (NCONS * 32);
+        int64_t acc = 0;     // tail items of the previous components: each tail starts where the last ended
         for (uint32_t kk = 0; kk < p.n_comp; ++kk) {
             const CompDesc& K = p.comp[kk];
             if (K.flags & CF_SKIP) continue;
@@ -266,8 +335,12 @@ __global__ void __launch_bounds__(TMAC ? NTHREADS_TMA : NTHREADS, 1)
             const int64_t n_tail = p.n_records - lo;
             if (n_tail <= 0) continue;
             const bool own = (K.flags & CF_TAIL_ZERO) != 0;
+            const int64_t items = n_tail * (int64_t)(K.f_hi - K.f_lo);
+            // (short tails of many components would otherwise all land on the first CTAs)
+            const int64_t gfirst = (gid - acc % gstride + gstride) % gstride;
+            if (!own) acc += items;
             if (own && gridDim.x - 1 - (kk % gridDim.x) != blockIdx.x) continue;
-            const int64_t first = own ? tid : gid, step = own ? (int64_t)(NCONS * 32) : gstride;
+            const int64_t first = own ? tid : gfirst, step = own ? (int64_t)(NCONS * 32) : gstride;
             if (own) {
                 // every dst cluster of the component: bytes [lo*stride, ceil(N/B)*B*stride) := 0
                 for (uint32_t f = K.f_lo; f < K.f_hi; ++f) {
@@ -280,7 +353,7 @@ __global__ void __launch_bounds__(TMAC ? NTHREADS_TMA : NTHREADS, 1)
                 }
                 named_bar_sync(2, NCONS * 32);
             }
-            const int64_t total = n_tail * (int64_t)(K.f_hi - K.f_lo);
+            const int64_t total = items;
             for (int64_t x0 = first; x0 < total; x0 += 4 * step) {
                 const U* sp[4];
                 U* dp[4];
@@ -290,8 +363,10 @@ __global__ void __launch_bounds__(TMAC ? NTHREADS_TMA : NTHREADS, 1)
                     const int64_t x = x0 + m * step;
                     nu[m] = 0;
                     if (x < total) {
-                        const uint32_t f = K.f_lo + (uint32_t)(x / n_tail);
-                        const uint64_t r = (uint64_t)(lo + (x % n_tail));
+                        // tails are shorter than a tile (< 16384 records): 32-bit division
+                        const uint32_t q = (uint32_t)x / (uint32_t)n_tail;
+                        const uint32_t f = K.f_lo + q;
+                        const uint64_t r = (uint64_t)(lo + ((uint32_t)x - q * (uint32_t)n_tail));
                         const FieldDesc fd = et.fields[f];
                         const uint64_t ss = p.srcc[fd.sc].stride, ds = p.dstc[fd.dc].stride;
                         sp[m] = (const U*)(p.src + p.srcc[fd.sc].region + (r >> fd.sbl) * (ss << fd.sbl) +
@@ -329,7 +404,7 @@ __global__ void __launch_bounds__(TMAC ? NTHREADS_TMA : NTHREADS, 1)
             // this warp's instructions of component k: i = warp + NCONS*e; lane's unit = entry i*32 + lane
             k_cur = (int)k;
             zeroed = 0;
-            if (!tmac) nv = copy_plan(p, p.comp[k].dc_lo, T, p.comp[k].out_bytes, tid, gofs, gstep);
+            if (!tmac) nv = copy_plan(p, dcl, p.comp[k].dc_lo, T, p.comp[k].out_bytes, tid, gofs, gstep);
             if (!tmac && (p.comp[k].flags & CF_ZERO_OUT)) {
                 // dst records have padding the permutation never writes: zero both output buffers
                 // once for this component (the same positions stay untouched in every tile)
@@ -354,19 +429,30 @@ __global__ void __launch_bounds__(TMAC ? NTHREADS_TMA : NTHREADS, 1)
                         const uint32_t i = slot % I, gi = i * 32 + lane;
                         grho[j] = slot / I;
                         if (gi < G) {
-                            const ByteGroup& gr = et.g[p.comp[k].instr_base + gi];
-                            gns[j] = gr.n_src;
-                            gno[j] = gr.n_out;
+                            // the group from its shared-memory copy (13 words, ByteGroup layout)
+                            const uint32_t ga = tbl + (uint32_t)sizeof(ByteGroup) * (p.comp[k].instr_base + gi);
+                            uint32_t w[13];
+#pragma unroll
+                            for (int q = 0; q < 13; ++q) w[q] = lds<uint32_t>(ga + 4 * q);
+                            // words: out_off 0-1, src_off 2-3, sel 4-9, out_dc 10, src_sc 11, n_out|n_src 12
+                            gno[j] = w[12] & 0xFFu;
+                            gns[j] = (w[12] >> 8) & 0xFFu;
 #pragma unroll
                             for (int m = 0; m < 4; ++m) {
-                                const ClusterDesc& cs = p.srcc[gr.src_sc[m]];
-                                const ClusterDesc& cd = p.dstc[gr.out_dc[m]];
-                                gsrc[j][m] = cs.smem + gr.src_off[m];
-                                gsst[j][m] = 32u * cs.stride;
-                                gout[j][m] = cd.smem + gr.out_off[m];
-                                gost[j][m] = 32u * cd.stride;
-                                gsel[j][m][0] = (uint32_t)gr.sel[m][0] | ((uint32_t)gr.sel[m][1] << 16);
-                                gsel[j][m][1] = gr.sel[m][2];
+                                const uint32_t sc = (w[11] >> (8 * m)) & 0xFFu, dc = (w[10] >> (8 * m)) & 0xFFu;
+                                const uint32_t out_off = (w[m >> 1] >> (16 * (m & 1))) & 0xFFFFu;
+                                const uint32_t src_off = (w[2 + (m >> 1)] >> (16 * (m & 1))) & 0xFFFFu;
+                                // sel[m][t] is halfword 3m+t of words 4..9
+                                const uint32_t h0 = 3 * m, h1 = 3 * m + 1, h2 = 3 * m + 2;
+                                const uint32_t s0 = (w[4 + (h0 >> 1)] >> (16 * (h0 & 1))) & 0xFFFFu;
+                                const uint32_t s1 = (w[4 + (h1 >> 1)] >> (16 * (h1 & 1))) & 0xFFFFu;
+                                const uint32_t s2 = (w[4 + (h2 >> 1)] >> (16 * (h2 & 1))) & 0xFFFFu;
+                                gsrc[j][m] = lds<uint32_t>(scl + 16 * sc + 12) + src_off;
+                                gsst[j][m] = 32u * lds<uint32_t>(scl + 16 * sc + 8);
+                                gout[j][m] = lds<uint32_t>(dcl + 16 * dc + 12) + out_off;
+                                gost[j][m] = 32u * lds<uint32_t>(dcl + 16 * dc + 8);
+                                gsel[j][m][0] = s0 | (s1 << 16);
+                                gsel[j][m][1] = s2;
                             }
                         }
                     }
@@ -379,13 +465,15 @@ __global__ void __launch_bounds__(TMAC ? NTHREADS_TMA : NTHREADS, 1)
                 ioff[e] = ooff[e] = din[e] = dout[e] = 0;
                 if ((uint32_t)e < ne) {
                     const uint32_t idx = (p.comp[k].instr_base + warp + NCONS * e) * 32 + lane;
-                    const uint32_t v = et.off[idx];
-                    const ClusterDesc& cs = p.srcc[et.sc[idx]];
-                    const ClusterDesc& cd = p.dstc[et.dc[idx]];
-                    ioff[e] = cs.smem + (v & 0xFFFFu) * (uint32_t)sizeof(U);
-                    ooff[e] = cd.smem + (v >> 16) * (uint32_t)sizeof(U);
-                    din[e] = 32u * cs.stride;
-                    dout[e] = 32u * cd.stride;
+                    const uint32_t v = lds<uint32_t>(tbl + 4 * idx);
+                    const uint32_t sc = lds<uint8_t>(tbl + 4 * n4 + idx);
+                    const uint32_t dc = lds<uint8_t>(tbl + 5 * n4 + idx);
+                    const uint32_t s_stride = lds<uint32_t>(scl + 16 * sc + 8), s_smem = lds<uint32_t>(scl + 16 * sc + 12);
+                    const uint32_t d_stride = lds<uint32_t>(dcl + 16 * dc + 8), d_smem = lds<uint32_t>(dcl + 16 * dc + 12);
+                    ioff[e] = s_smem + (v & 0xFFFFu) * (uint32_t)sizeof(U);
+                    ooff[e] = d_smem + (v >> 16) * (uint32_t)sizeof(U);
+                    din[e] = 32u * s_stride;
+                    dout[e] = 32u * d_stride;
                 }
             }
             }

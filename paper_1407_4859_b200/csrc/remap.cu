@@ -109,7 +109,7 @@ TiledLauncher pick(uint32_t unit, int cls, bool tma, const void** fn) {
 
 struct PlanCache {
     std::mutex mu;
-    std::map<std::pair<uint64_t, uint64_t>, std::shared_ptr<const RemapPlan>> plans;
+    std::map<std::tuple<uint64_t, uint64_t, bool>, std::shared_ptr<const RemapPlan>> plans;
     std::set<std::tuple<int, const void*>> attr_done;
     std::map<int, int> sm_count;
 };
@@ -118,14 +118,14 @@ PlanCache& cache() {
     return c;
 }
 
-std::shared_ptr<const RemapPlan> get_plan(const Layout& ls, const Layout& ld) {
+std::shared_ptr<const RemapPlan> get_plan(const Layout& ls, const Layout& ld, bool merged = false) {
     PlanCache& c = cache();
     std::lock_guard<std::mutex> g(c.mu);
-    auto key = std::make_pair(ls.id, ld.id);
+    auto key = std::make_tuple(ls.id, ld.id, merged);
     auto it = c.plans.find(key);
     if (it != c.plans.end()) return it->second;
     if (c.plans.size() > 4096) c.plans.clear();
-    auto p = std::make_shared<const RemapPlan>(compile_plan(ls, ld));
+    auto p = std::make_shared<const RemapPlan>(compile_plan(ls, ld, merged));
     c.plans.emplace(key, p);
     return p;
 }
@@ -262,6 +262,23 @@ uint64_t direct_bytes(const RemapPlan& p) {
 }
 
 
+// Average src chunk bytes per tile below which a component's tiles are loaded with 16-byte cp.async
+// by the producer warp instead of TMA bulk copies (ADHA_LDGSTS_BYTES overrides; 0 = always TMA).
+uint64_t ldgsts_bytes() {
+    const char* e = std::getenv("ADHA_LDGSTS_BYTES");
+    if (e && *e) return (uint64_t)std::strtoull(e, nullptr, 10);
+    return 1024;
+}
+
+// Payload up to which a multi-component remap uses the merged plan (ADHA_MERGE_BYTES overrides;
+// 0 disables).  Per-component tiles keep every tile near 48 KB at large N; at small and mid N
+// they leave a CTA one short tile per component, each paying the pipeline's latency.
+uint64_t merge_bytes() {
+    const char* e = std::getenv("ADHA_MERGE_BYTES");
+    if (e && *e) return (uint64_t)std::strtoull(e, nullptr, 10);
+    return 256ull << 20;
+}
+
 adha_status validate(const void* src, const adha_layout* hs, const void* dst, const adha_layout* hd, int64_t n,
                      Checked* out, bool device_buffers) {
     if (!hs || !hd) return fail(ADHA_ERR_INVALID_ARG, "null layout");
@@ -287,6 +304,19 @@ adha_status remap_checked(const uint8_t* src, const Layout& ls, uint8_t* dst, co
                           const Checked& ck, cudaStream_t st) {
     if (n == 0) return ADHA_OK;
     auto plan = get_plan(ls, ld);
+    // Multi-component remaps of up to merge_bytes() run on the merged plan (one component, whole
+    // records per tile) unless a dst region aliases its src region (remap_regions: those
+    // clusters must stay untouched, which needs their own skipped component).
+    if (plan->comps.size() > 1 && (uint64_t)n * ls.record_bytes <= merge_bytes()) {
+        bool alias = false;
+        for (const auto& K : plan->comps)
+            alias = alias || (K.identity && (uintptr_t)src + ck.bs[K.src_clusters[0]] ==
+                                                (uintptr_t)dst + ck.bd[K.dst_clusters[0]]);
+        if (!alias) {
+            auto mp = get_plan(ls, ld, true);
+            if (mp->tiled) plan = mp;
+        }
+    }
     // small and mid-size remaps (direct_bytes above) run faster on the direct kernel; a dst in
     // pinned host or peer memory keeps the latency-only threshold (the tiled kernel's 16-byte
     // stores suit PCIe / NVLink writes better than the direct kernel's per-field stores)
@@ -326,7 +356,10 @@ adha_status remap_checked(const uint8_t* src, const Layout& ls, uint8_t* dst, co
         D.out_bytes = D.T * K.Rd;
         // an identity component whose dst region is its src region moves nothing (NEXT N1)
         const bool skip = K.identity && P->src + ck.bs[K.src_clusters[0]] == P->dst + ck.bd[K.dst_clusters[0]];
-        D.flags = (uint16_t)((skip ? CF_SKIP : 0) | (K.zero_out ? CF_ZERO_OUT : 0) | (K.tail_zero ? CF_TAIL_ZERO : 0));
+        // LDGSTS loads when the component's src chunks per tile average below ldgsts_bytes()
+        const bool ldg = (uint64_t)D.tile_bytes < ldgsts_bytes() * K.src_clusters.size();
+        D.flags = (uint16_t)((skip ? CF_SKIP : 0) | (K.zero_out ? CF_ZERO_OUT : 0) | (K.tail_zero ? CF_TAIL_ZERO : 0) |
+                             (ldg ? CF_LDGSTS : 0));
         D.n_tiles = skip ? 0 : n / D.T;
         D.tile_base = tiles;
         tiles += D.n_tiles;
@@ -357,6 +390,9 @@ adha_status remap_checked(const uint8_t* src, const Layout& ls, uint8_t* dst, co
         D.f_hi = (uint16_t)fi;
     }
     P->total_tiles = tiles;
+    P->n_ent = plan->byte_groups ? plan->n_groups_total : (uint32_t)plan->ent_off.size();
+    P->n_srcc = sc;
+    P->n_dstc = dc;
     // Write-back mode (unit mode).  TMA bulk stores by a 10th warp when every component with
     // tiles has ONE dst chunk of >= 32 KB per tile and at most 8 src chunks: K-Means SoA->4xAoS8
     // +1.3 %, 4xAoS8->AoS +3 % (profiles/r01_notes.md).  Many small dst chunks queue behind the
@@ -666,7 +702,8 @@ extern "C" adha_status adha_remap_plan_describe(const adha_layout* hs, const adh
     // routing threshold of adha_remap for this pair (device dst): payload <= direct_bytes takes the
     // direct kernel (ADHA_SMALL_BYTES overrides, read now)
     s.pop_back();
-    s += ",\"direct_bytes\":" + std::to_string(direct_bytes(*plan)) + "}";
+    s += ",\"direct_bytes\":" + std::to_string(direct_bytes(*plan)) + ",\"merge_bytes\":" +
+         std::to_string(plan->comps.size() > 1 ? merge_bytes() : 0) + "}";
     *json_out = (char*)std::malloc(s.size() + 1);
     if (!*json_out) return fail(ADHA_ERR_OOM, "out of host memory");
     std::memcpy(*json_out, s.c_str(), s.size() + 1);

@@ -161,8 +161,9 @@ uint32_t call_tile(const RemapPlan& p, int k, int64_t n, int n_sm) {
     return best;
 }
 
-RemapPlan compile_plan(const Layout& ls, const Layout& ld) {
+RemapPlan compile_plan(const Layout& ls, const Layout& ld, bool merge) {
     RemapPlan P;
+    P.merged = merge;
     const int F = ls.n_fields;
     const int Cs = ls.n_clusters(), Cd = ld.n_clusters();
 
@@ -197,6 +198,10 @@ RemapPlan compile_plan(const Layout& ls, const Layout& ld) {
         int a = find(ls.cluster[f]), b = find(Cs + ld.cluster[f]);
         if (a != b) parent[std::max(a, b)] = std::min(a, b);
     }
+    // merged plan (small and mid-size remaps): ONE component over all clusters, so a tile carries
+    // whole records and a CTA meets a handful of tiles instead of one short tile per component
+    if (merge)
+        for (int x = 0; x < Cs + Cd; ++x) parent[x] = 0;
     std::map<int, int> comp_of_root;   // ordered by root = min src cluster of the component
     for (int c = 0; c < Cs; ++c) {
         int r = find(c);
@@ -238,8 +243,19 @@ RemapPlan compile_plan(const Layout& ls, const Layout& ld) {
         }
     }
 
+    // unit mode: the consumers copy the entry table (off | sc | dc) and the cluster descriptors
+    // into shared memory once per CTA, so a component switch reads its entries with LDS instead of
+    // lane-divergent (serialised) constant-bank loads from the kernel parameters
+    {
+        uint64_t w = 0;
+        for (auto& K : P.comps)
+            if (!K.identity) w += K.R / g;
+        const uint64_t n4 = (32 * w + 15) / 16 * 16;   // the kernel's copy rounds to 16 entries
+        // (beyond the largest table class unit mode is impossible anyway: byte groups or naive)
+        if (32 * w <= (uint64_t)CLASS_NENT[3]) P.tbl_bytes = (uint32_t)((6 * n4 + 16ull * (Cs + Cd) + 127) / 128 * 128);
+    }
     // tile sizes and stages
-    const uint32_t budget = 232448 - HDR_BYTES - 128;   // sm_100 opt-in dynamic smem per block
+    const uint32_t budget = 232448 - HDR_BYTES - 128 - P.tbl_bytes;   // sm_100 opt-in dynamic smem per block
     const uint32_t target = env_u32("ADHA_STAGE_BYTES", 49152);
     const uint32_t t_cap = env_u32("ADHA_TILE_CAP", 16384);
     uint32_t s_in = std::min<uint32_t>(env_u32("ADHA_STAGES", 4), MAX_S_IN);
@@ -269,7 +285,7 @@ RemapPlan compile_plan(const Layout& ls, const Layout& ld) {
     P.s_in = s_in;
     P.s_out = S_OUT;
     P.stage_bytes = (uint32_t)stage;
-    P.smem_bytes = HDR_BYTES + 128 + (s_in + S_OUT) * P.stage_bytes;
+    P.smem_bytes = HDR_BYTES + 128 + (s_in + S_OUT) * P.stage_bytes + P.tbl_bytes;
 
     // ---- byte-group mode for unit sizes below 4 bytes (see ByteGroup in remap_plan.h)
     const char* bg_env = std::getenv("ADHA_BYTE_GROUPS");
@@ -643,10 +659,14 @@ RemapPlan compile_plan(const Layout& ls, const Layout& ld) {
                 stage2 = std::max<uint64_t>(stage2, (uint64_t)K.T_max * std::max(K.Rs, K.Rd) + 32 * max_chunks);
             }
             stage2 = (stage2 + 127) / 128 * 128;
-            if ((P.s_in + P.s_out) * stage2 > budget) gcls = -1;
+            // shared-memory copy of the groups in use and of the cluster descriptors (see unit mode)
+            const uint32_t bg_tbl = (uint32_t)((((uint64_t)sizeof(ByteGroup) * groups.size() + 15) / 16 * 16 +
+                                                16ull * (Cs + Cd) + 127) / 128 * 128);
+            if ((P.s_in + P.s_out) * stage2 + bg_tbl > budget + P.tbl_bytes) gcls = -1;
             else {
                 P.stage_bytes = (uint32_t)stage2;
-                P.smem_bytes = HDR_BYTES + 128 + (P.s_in + P.s_out) * P.stage_bytes;
+                P.tbl_bytes = bg_tbl;
+                P.smem_bytes = HDR_BYTES + 128 + (P.s_in + P.s_out) * P.stage_bytes + P.tbl_bytes;
             }
         }
         if (gcls >= 0) {
@@ -665,6 +685,7 @@ RemapPlan compile_plan(const Layout& ls, const Layout& ld) {
             for (auto& K : P.comps)
                 for (int f : K.fields) fd[fi++] = field_desc(P, ls, ld, f);
             P.byte_groups = true;
+            P.n_groups_total = (uint32_t)groups.size();
             P.group_class = gcls;
             P.matched = false;
             P.tiled = true;

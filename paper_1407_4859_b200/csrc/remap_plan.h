@@ -50,7 +50,7 @@ constexpr int HDR_BYTES = 1024;                // barrier header at the start of
 constexpr int MAX_S_IN = 8;
 constexpr uint32_t STAGE_MAX = 12 * 16 * NCONS * 32;   // copy-out covers 12 16-byte vectors per thread
 
-struct ClusterDesc {
+struct alignas(16) ClusterDesc {   // 16-byte aligned: the kernel copies descriptors with 128-bit loads
     uint64_t region;    // region base in the buffer for this N (bytes)
     uint32_t stride;    // bytes per cluster record
     uint32_t smem;      // chunk offset inside its component's staged tile (bytes), for this call's T
@@ -80,6 +80,8 @@ struct CompDesc {
 constexpr uint16_t CF_SKIP = 1;       // identity component whose dst region IS its src region (nothing moves)
 constexpr uint16_t CF_ZERO_OUT = 2;   // dst records have padding: output buffers pre-zeroed at component start
 constexpr uint16_t CF_TAIL_ZERO = 4;  // dst padding or AoSoA blocks: tail area zeroed before the tail copy
+constexpr uint16_t CF_LDGSTS = 8;     // tiles of small src chunks: loaded with 16-byte cp.async (LDGSTS) by
+                                      // the producer warp instead of one TMA bulk copy per chunk
 
 struct TiledParams {
     uint64_t src;         // base address: src region c starts at src + srcc[c].region
@@ -95,6 +97,9 @@ struct TiledParams {
     uint32_t blocked;     // 1: CTA b processes a contiguous tile range, 0: tiles b, b+G, b+2G, ...
     uint32_t tma_split;   // 0: one bulk load per src chunk; else pieces of at most this many bytes
     uint32_t tma_copy;    // 1: tiles written back by the write-back warp with TMA bulk stores, else STG by the consumers
+    uint32_t n_ent;       // entries used: unit mode 32 * instructions of all components, byte-group mode groups
+    uint32_t n_srcc;      // clusters used in srcc / dstc
+    uint32_t n_dstc;
     CompDesc comp[MAXK];
     ClusterDesc srcc[MAXC];
     ClusterDesc dstc[MAXC];
@@ -103,7 +108,7 @@ struct TiledParams {
 // per-(instruction, lane) table: entry i*32+lane of instruction i (instructions of all
 // components concatenated); offsets are units inside period 0 of the unit's chunk
 template <int NENT>
-struct EntryTable {
+struct alignas(16) EntryTable {   // 16-byte aligned: copied to shared memory with 128-bit loads
     uint32_t off[NENT];   // src local unit offset (low 16 bits) | dst local unit offset (high 16 bits)
     uint8_t sc[NENT];     // src cluster of the unit
     uint8_t dc[NENT];     // dst cluster of the unit
@@ -123,7 +128,7 @@ struct ByteGroup {
     uint8_t n_out, n_src, pad0, pad1;
 };
 template <int NG>
-struct GroupTable {
+struct alignas(16) GroupTable {
     ByteGroup g[NG];
     FieldDesc fields[MAXF];
 };
@@ -177,15 +182,18 @@ struct RemapPlan {
         uint32_t n_groups = 0;        // byte-group mode: groups of one period
     };
     bool tiled = false;
+    bool merged = false;              // compiled with every cluster in one component
     std::string why_naive;            // reason when not tiled
     uint32_t unit = 1;                // g
     uint32_t s_in = 0, s_out = 2, stage_bytes = 0;
     uint32_t smem_bytes = 0;
+    uint32_t tbl_bytes = 0;           // unit mode: shared-memory copy of the entry table + cluster descriptors
     int table_class = 0;
     bool matched = false;             // conflict-free matching used (g = 4)
     bool byte_groups = false;         // g < 4: PRMT byte-group mode (GroupTable) instead of units
     uint32_t tile_quantum = 32;       // tile sizes are multiples of this many records
     int group_class = 0;
+    uint32_t n_groups_total = 0;      // byte-group mode: groups in the table
     std::vector<Comp> comps;
     std::vector<int> src_order, dst_order;   // kernel cluster index -> canonical cluster
     std::vector<int> src_slot, dst_slot;     // canonical cluster -> kernel cluster index
@@ -195,7 +203,8 @@ struct RemapPlan {
 };
 
 struct Layout;
-RemapPlan compile_plan(const Layout& ls, const Layout& ld);
+// merge: one component over all clusters (the small / mid-size variant, see remap.cu)
+RemapPlan compile_plan(const Layout& ls, const Layout& ld, bool merge = false);
 std::string describe_plan(const RemapPlan& p, const Layout& ls, const Layout& ld);
 // records per tile of component k for an N-record call on n_sm SMs
 uint32_t call_tile(const RemapPlan& p, int k, int64_t n, int n_sm);

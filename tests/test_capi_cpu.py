@@ -644,3 +644,27 @@ def test_inplace_plan_runs_skip_tile_passes(permute_mode):
     # a hybrid whose clusters interleave: {f0,f2} -> {f0,f1,f2} splits into the runs f0 | f2
     d = _ip([4, 4, 4], [0, 1, 0], [0, 0, 0], 4096).describe()
     assert (d["pre_clusters"], d["post_clusters"]) == (1, 1)
+
+
+@pytest.mark.parametrize("shape", ["C2", "C3", "C3-back", "Medical AoSV->SoA"])
+def test_inplace_plan_segments_verified_large(shape, monkeypatch):
+    """The parallel cycle decomposition (cut walks advanced 16 at a time per host thread, placed
+    by prefix sums; uncut cycles by their smallest slot) checked by the library itself against the
+    permutation (ADHA_IP_VERIFY=1) at sizes with hundreds of thousands of slots."""
+    monkeypatch.setenv("ADHA_INPLACE_STAGED_BYTES", "0")
+    monkeypatch.setenv("ADHA_IP_VERIFY", "1")
+    from tests.conftest import golden
+    from oracle import planner as P
+    w16 = [8 if i % 4 == 3 else 4 for i in range(16)]
+    w64 = [8 if i % 4 == 3 else 4 for i in range(64)]
+    hyb = P.parse_layout(golden("expected.json")["c3_hybrid"]["value"], {f"f{i}": i for i in range(64)})
+    c3 = [0] * 64
+    for c, cl in enumerate(hyb):
+        for nm in cl:
+            c3[int(nm[1:])] = c
+    cases = {"C2": (w16, [0] * 16, list(range(16)), 2_000_003), "C3": (w64, list(range(64)), c3, 1_000_003),
+             "C3-back": (w64, c3, list(range(64)), 1_000_003),
+             "Medical AoSV->SoA": ([4] * 9, [0, 0, 0, 1, 2, 3, 4, 5, 6], list(range(9)), 3_000_001)}
+    widths, ls, ld, n = cases[shape]
+    d = _ip(widths, ls, ld, n).describe()
+    assert d["moved_slots"] > 0 and d["segments"] * 64 >= d["moved_slots"]

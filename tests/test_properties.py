@@ -204,10 +204,13 @@ def test_inplace_plan_invariants(case):
     """Host plan of the in-place remap (slot-permutation mode) on random packed layout pairs:
     never crashes; the buffer is max(bytes(Ls), bytes(Ld)) by the oracle's address model; every
     src body slot is content; the permutation closes on src u dst slots; segments cover the moved
-    slots in pieces of at most 64; the workspace holds a saved slot per segment."""
+    slots in pieces of at most 64; the workspace holds a saved slot per segment; and (ADHA_IP_VERIFY)
+    every moved slot sits in exactly one segment, in cycle order, each segment's predecessor ending
+    on the slot whose content its first position receives."""
     import os
     widths, ls, ld, n = case
     os.environ["ADHA_INPLACE_STAGED_BYTES"] = "0"
+    os.environ["ADHA_IP_VERIFY"] = "1"        # the library checks its segments against the permutation
     try:
         try:
             p = A.InplacePlan(A.Layout(widths, ls), A.Layout(widths, ld), n)
@@ -217,6 +220,7 @@ def test_inplace_plan_invariants(case):
         d = p.describe()
     finally:
         os.environ.pop("ADHA_INPLACE_STAGED_BYTES", None)
+        os.environ.pop("ADHA_IP_VERIFY", None)
     assert p.buffer_bytes == max(O.layout_bytes(widths, ls, n), O.layout_bytes(widths, ld, n))
     u, S, T = d["unit"], d["slot_bytes"], d["T"]
     assert S == T * u and all(w % u == 0 for w in widths)

@@ -57,16 +57,25 @@ def main():
             ls = bench.c3_labels()[0]
         R = sum(w)
         Ls, Ld = A.Layout(w, ls), A.Layout(w, ld)
-        for payload in (256 << 10, 1 << 20, 4 << 20, 8 << 20, 16 << 20, 32 << 20):
+        for payload in (256 << 10, 1 << 20, 4 << 20, 8 << 20, 16 << 20, 32 << 20, 128 << 20, 512 << 20):
             n = max(1, payload // R)
             src = torch.zeros(Ls.nbytes(n), dtype=torch.uint8, device="cuda")
             dst = torch.zeros(Ld.nbytes(n), dtype=torch.uint8, device="cuda")
             out = {"shape": name, "payload_MB": round(n * R / 2 ** 20, 2),
                    "components": len(A.plan_describe(Ls, Ld)["components"])}
-            for path, sb in (("tiled", "0"), ("direct", str(1 << 40))):
-                os.environ["ADHA_SMALL_BYTES"] = sb
+            # tiled: default plan choice; tiled_tma: TMA bulk loads only; tiled_components: the
+            # per-component (large-N) plan with TMA loads; direct: the direct kernel
+            for path, env in (("tiled", {"ADHA_SMALL_BYTES": "0"}),
+                              ("tiled_tma", {"ADHA_SMALL_BYTES": "0", "ADHA_LDGSTS_BYTES": "0"}),
+                              ("tiled_components", {"ADHA_SMALL_BYTES": "0", "ADHA_MERGE_BYTES": "0",
+                                                    "ADHA_LDGSTS_BYTES": "0"}),
+                              ("direct", {"ADHA_SMALL_BYTES": str(1 << 40)})):
+                for k in ("ADHA_SMALL_BYTES", "ADHA_MERGE_BYTES", "ADHA_LDGSTS_BYTES"):
+                    os.environ.pop(k, None)
+                os.environ.update(env)
                 out[path + "_us"] = round(graph_us(lambda: A.remap(src, Ls, dst, Ld, n)), 2)
-            os.environ.pop("ADHA_SMALL_BYTES", None)
+            for k in ("ADHA_SMALL_BYTES", "ADHA_MERGE_BYTES", "ADHA_LDGSTS_BYTES"):
+                os.environ.pop(k, None)
             out["default_us"] = round(graph_us(lambda: A.remap(src, Ls, dst, Ld, n)), 2)
             print(json.dumps(out), flush=True)
             del src, dst
