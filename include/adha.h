@@ -190,14 +190,18 @@ ADHA_API adha_status adha_remap(const void* src, const adha_layout* src_layout,
 
 /* The remap between layout instances given REGION BY REGION (SURVEY.md 8(f) N1,
  * "moved subset"): src_regions[c] is the device address of src cluster c's region
- * (canonical cluster order, n_records * stride(c) bytes), dst_regions[c] likewise.
+ * (canonical cluster order), dst_regions[c] likewise.
  * Regions need not be parts of one buffer.  A dst region that is the very same
- * memory as the src region of an IDENTICAL cluster (same fields in the same
- * order) is left untouched: its records are already in place, so only the fields
- * whose cluster changes move -- the paper's remap cost "based on the number of
- * common fields" (Medical AoSV -> SoA moves
- * only {V1,V2,V3}).  Every region must be 256-byte aligned; dst regions must not
- * overlap each other or any src region except by that exact aliasing.
+ * memory as the src region of an IDENTICAL cluster (same fields at the same
+ * offsets, same stride and AoSoA block, no alignment padding: the plan's identity
+ * component) is left untouched by both kernel paths, bytes past N in its last block
+ * included: its records are already in place, so only the fields whose cluster
+ * changes move -- the paper's remap cost "based on the number of common fields"
+ * (Medical AoSV -> SoA moves only {V1,V2,V3}).
+ * Every region must be 256-byte aligned; a region spans its whole blocks
+ * (ceil(N / B) * B * stride(c) bytes); dst regions must not overlap each other or
+ * any src region except by that exact aliasing (a member-equal cluster that is not
+ * an identity -- padded, or another block size -- is OVERLAP).
  * Asynchronous on `stream` like adha_remap.
  * Errors: INVALID_ARG, LAYOUT_MISMATCH, ALIGNMENT, OVERLAP, TOO_LARGE, CUDA. */
 ADHA_API adha_status adha_remap_regions(const void* const* src_regions, const adha_layout* src_layout,
@@ -250,8 +254,10 @@ ADHA_API adha_status adha_remap_peer(const void* src, const adha_layout* src_lay
 
 /* End-to-end remap of HOST buffers through the current device: src_host holds
  * bytes(Ls, N), dst_host receives bytes(Ld, N) (only payload bytes written).
- * Strategy (ADHA_HOST_MODE = auto | hybrid | zero | staged; auto = hybrid when dst_host
- * is pinned, 256-byte aligned host memory and a scratch is given, else staged):
+ * Strategy (ADHA_HOST_MODE = auto | hybrid | zero | staged; auto = zero when both host
+ * buffers are pinned, 256-byte aligned and the src layout has >= 16 clusters (many small
+ * H2D copies per chunk otherwise), else hybrid when dst_host is pinned, 256-byte aligned host
+ * memory and a scratch is given, else staged):
  *   hybrid  record chunks (~16 MB) are copied host->device into `scratch` (one copy per
  *           src region, copy engine) and each chunk's remap kernel stores its records
  *           straight into dst_host over PCIe: H2D of chunk k+1 overlaps the kernel of k;

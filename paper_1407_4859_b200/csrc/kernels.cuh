@@ -239,31 +239,14 @@ __global__ void __launch_bounds__(TMAC ? NTHREADS_TMA : NTHREADS, 1)
             mbar_wait(empty0 + 8 * stage, phase ^ 1);
             ADHA_PT(const long long pt1 = clock64(); pw += pt1 - pt0);
             const uint32_t ib = in0 + stage * p.stage_bytes;
-            if (p.comp[k].flags & CF_LDGSTS) {
-                // Small src chunks (many SoA regions, short tiles): each TMA bulk copy has a fixed
-                // cost in the SM's TMA unit (64 chunks of 128 B took ~8 us per tile), so the warp
-                // copies the tile itself with 16-byte cp.async, 512 bytes per instruction; each
-                // lane's copies arrive on `full` when they land, lane 0's arrive closes the count.
-                const uint32_t T = p.comp[k].T;
-                for (uint32_t c = p.comp[k].sc_lo; c < p.comp[k].sc_hi; ++c) {
-                    const uint32_t bytes = T * p.srcc[c].stride;
-                    const uint8_t* g = (const uint8_t*)(p.src + p.srcc[c].region) + (uint64_t)lt * bytes;
-                    const uint32_t sm = ib + p.srcc[c].smem;
-                    for (uint32_t o = lane * 16; o < bytes; o += 32 * 16) cp_async16(sm + o, g + o);
-                }
-                cp_async_mbar_arrive(full0 + 8 * stage);
-                __syncwarp();
-                if (lane == 0) mbar_arrive(full0 + 8 * stage);
-            } else {
-                if (lane == 0) mbar_arrive_expect_tx(full0 + 8 * stage, p.comp[k].tile_bytes);
-                __syncwarp();
+            if (lane == 0) mbar_arrive_expect_tx(full0 + 8 * stage, p.comp[k].tile_bytes);
+            __syncwarp();
 #pragma unroll
-                for (uint32_t q = 0; q < PMAX; ++q) {
-                    if (q < np) {
-                        const void* g = (const void*)(pg[q] + (uint64_t)lt * pstep[q]);
-                        if (p.l2_hints & 1) bulk_load_hint(ib + psm[q], g, pbytes[q], full0 + 8 * stage, pol);
-                        else bulk_load(ib + psm[q], g, pbytes[q], full0 + 8 * stage);
-                    }
+            for (uint32_t q = 0; q < PMAX; ++q) {
+                if (q < np) {
+                    const void* g = (const void*)(pg[q] + (uint64_t)lt * pstep[q]);
+                    if (p.l2_hints & 1) bulk_load_hint(ib + psm[q], g, pbytes[q], full0 + 8 * stage, pol);
+                    else bulk_load(ib + psm[q], g, pbytes[q], full0 + 8 * stage);
                 }
             }
             ADHA_PT(pi += clock64() - pt1);

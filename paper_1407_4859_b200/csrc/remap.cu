@@ -262,21 +262,15 @@ uint64_t direct_bytes(const RemapPlan& p) {
 }
 
 
-// Average src chunk bytes per tile below which a component's tiles are loaded with 16-byte cp.async
-// by the producer warp instead of TMA bulk copies (ADHA_LDGSTS_BYTES overrides; 0 = always TMA).
-uint64_t ldgsts_bytes() {
-    const char* e = std::getenv("ADHA_LDGSTS_BYTES");
-    if (e && *e) return (uint64_t)std::strtoull(e, nullptr, 10);
-    return 1024;
-}
-
 // Payload up to which a multi-component remap uses the merged plan (ADHA_MERGE_BYTES overrides;
 // 0 disables).  Per-component tiles keep every tile near 48 KB at large N; at small and mid N
-// they leave a CTA one short tile per component, each paying the pipeline's latency.
+// they leave a CTA one short tile per component, each paying the pipeline's latency.  Measured
+// on B200 (profiles/r02f_small_path.log, CUDA-graph replay): C3's SoA -> hybrid 32 MB 35.5 us
+// merged vs 51.8 per component, 128 MB 95.3 vs 77.3; Medical AoSV -> SoA 1 MB 6.6 vs 15.2 us.
 uint64_t merge_bytes() {
     const char* e = std::getenv("ADHA_MERGE_BYTES");
     if (e && *e) return (uint64_t)std::strtoull(e, nullptr, 10);
-    return 256ull << 20;
+    return 64ull << 20;
 }
 
 adha_status validate(const void* src, const adha_layout* hs, const void* dst, const adha_layout* hd, int64_t n,
@@ -307,6 +301,9 @@ adha_status remap_checked(const uint8_t* src, const Layout& ls, uint8_t* dst, co
     // Multi-component remaps of up to merge_bytes() run on the merged plan (one component, whole
     // records per tile) unless a dst region aliases its src region (remap_regions: those
     // clusters must stay untouched, which needs their own skipped component).
+    // the direct-path threshold is the component plan's (its crossover with the tiled kernel
+    // was measured per component count; the merged plan only replaces the tiled side of it)
+    const uint64_t thr = ck.dst_local ? direct_bytes(*plan) : small_bytes();
     if (plan->comps.size() > 1 && (uint64_t)n * ls.record_bytes <= merge_bytes()) {
         bool alias = false;
         for (const auto& K : plan->comps)
@@ -320,7 +317,6 @@ adha_status remap_checked(const uint8_t* src, const Layout& ls, uint8_t* dst, co
     // small and mid-size remaps (direct_bytes above) run faster on the direct kernel; a dst in
     // pinned host or peer memory keeps the latency-only threshold (the tiled kernel's 16-byte
     // stores suit PCIe / NVLink writes better than the direct kernel's per-field stores)
-    const uint64_t thr = ck.dst_local ? direct_bytes(*plan) : small_bytes();
     if (!plan->tiled || (uint64_t)n * ls.record_bytes <= thr)
         return launch_naive(src, ls, ck.bs, dst, ld, ck.bd, 0, n, st);
 
@@ -356,10 +352,7 @@ adha_status remap_checked(const uint8_t* src, const Layout& ls, uint8_t* dst, co
         D.out_bytes = D.T * K.Rd;
         // an identity component whose dst region is its src region moves nothing (NEXT N1)
         const bool skip = K.identity && P->src + ck.bs[K.src_clusters[0]] == P->dst + ck.bd[K.dst_clusters[0]];
-        // LDGSTS loads when the component's src chunks per tile average below ldgsts_bytes()
-        const bool ldg = (uint64_t)D.tile_bytes < ldgsts_bytes() * K.src_clusters.size();
-        D.flags = (uint16_t)((skip ? CF_SKIP : 0) | (K.zero_out ? CF_ZERO_OUT : 0) | (K.tail_zero ? CF_TAIL_ZERO : 0) |
-                             (ldg ? CF_LDGSTS : 0));
+        D.flags = (uint16_t)((skip ? CF_SKIP : 0) | (K.zero_out ? CF_ZERO_OUT : 0) | (K.tail_zero ? CF_TAIL_ZERO : 0));
         D.n_tiles = skip ? 0 : n / D.T;
         D.tile_base = tiles;
         tiles += D.n_tiles;

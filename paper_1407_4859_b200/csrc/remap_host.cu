@@ -92,7 +92,14 @@ extern "C" adha_status adha_remap_host(const void* src_host, const adha_layout* 
     //           host dst directly, no scratch at all;
     //   staged  H2D per src region, remap in device memory, D2H per dst region (pageable memory).
     std::string mode = std::getenv("ADHA_HOST_MODE") ? std::getenv("ADHA_HOST_MODE") : "auto";
-    if (mode == "auto") mode = (dst_pinned && aligned && scratch) ? "hybrid" : "staged";
+    // auto: zero-copy when both sides are pinned and the src has many regions -- one H2D copy per
+    // src region and chunk then costs more than the kernel's own TMA reads over PCIe (C3, 64 SoA
+    // regions: zero 81.0 GB/s, hybrid 69.1, staged 63.1; C2, one AoS region: hybrid 88, zero 80;
+    // profiles/r02f_e2e_c3.log); else hybrid with a pinned dst, else staged
+    if (mode == "auto")
+        mode = (src_pinned && dst_pinned && aligned && ls.n_clusters() >= 16) ? "zero"
+               : (dst_pinned && aligned && scratch)                           ? "hybrid"
+                                                                              : "staged";
     if ((mode == "zero" && !(src_pinned && dst_pinned && aligned)) || (mode == "hybrid" && !(dst_pinned && aligned)))
         mode = "staged";
     if (mode == "zero") {

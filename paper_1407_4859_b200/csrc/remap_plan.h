@@ -80,8 +80,6 @@ struct CompDesc {
 constexpr uint16_t CF_SKIP = 1;       // identity component whose dst region IS its src region (nothing moves)
 constexpr uint16_t CF_ZERO_OUT = 2;   // dst records have padding: output buffers pre-zeroed at component start
 constexpr uint16_t CF_TAIL_ZERO = 4;  // dst padding or AoSoA blocks: tail area zeroed before the tail copy
-constexpr uint16_t CF_LDGSTS = 8;     // tiles of small src chunks: loaded with 16-byte cp.async (LDGSTS) by
-                                      // the producer warp instead of one TMA bulk copy per chunk
 
 struct TiledParams {
     uint64_t src;         // base address: src region c starts at src + srcc[c].region

@@ -25,25 +25,18 @@ if not torch.cuda.is_available():
 import paper_1407_4859_b200 as A  # noqa: E402
 
 
-@pytest.fixture(params=["tiled", "tiled-components", "tiled-ldgsts", "direct-small"])
+@pytest.fixture(params=["tiled", "tiled-components", "direct-small"])
 def small_path(request, monkeypatch):
-    """Run a test four times: with every remap on the tiled kernel (ADHA_SMALL_BYTES=0; remaps of
+    """Run a test three times: with every remap on the tiled kernel (ADHA_SMALL_BYTES=0; remaps of
     up to merge_bytes take the merged one-component plan), on the tiled kernel with per-component
-    tiles at every size (ADHA_MERGE_BYTES=0, the large-N plan) and TMA bulk loads only
-    (ADHA_LDGSTS_BYTES=0), on the tiled kernel with every tile loaded by the producer's cp.async
-    (LDGSTS) copies, and with the default routing where small remaps (remap.cu direct_bytes) take
-    the direct kernel."""
-    for k in ("ADHA_MERGE_BYTES", "ADHA_LDGSTS_BYTES"):
-        monkeypatch.delenv(k, raising=False)
+    tiles at every size (ADHA_MERGE_BYTES=0, the large-N plan), and with the default routing where
+    small remaps (remap.cu direct_bytes) take the direct kernel."""
+    monkeypatch.delenv("ADHA_MERGE_BYTES", raising=False)
     if request.param == "tiled":
         monkeypatch.setenv("ADHA_SMALL_BYTES", "0")
     elif request.param == "tiled-components":
         monkeypatch.setenv("ADHA_SMALL_BYTES", "0")
         monkeypatch.setenv("ADHA_MERGE_BYTES", "0")
-        monkeypatch.setenv("ADHA_LDGSTS_BYTES", "0")
-    elif request.param == "tiled-ldgsts":
-        monkeypatch.setenv("ADHA_SMALL_BYTES", "0")
-        monkeypatch.setenv("ADHA_LDGSTS_BYTES", str(1 << 30))
     else:
         monkeypatch.delenv("ADHA_SMALL_BYTES", raising=False)
     return request.param

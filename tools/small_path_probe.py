@@ -63,18 +63,18 @@ def main():
             dst = torch.zeros(Ld.nbytes(n), dtype=torch.uint8, device="cuda")
             out = {"shape": name, "payload_MB": round(n * R / 2 ** 20, 2),
                    "components": len(A.plan_describe(Ls, Ld)["components"])}
-            # tiled: default plan choice; tiled_tma: TMA bulk loads only; tiled_components: the
-            # per-component (large-N) plan with TMA loads; direct: the direct kernel
+            # tiled: the default plan choice (merged plan up to merge_bytes); tiled_merged: the
+            # merged plan at every size; tiled_components: the per-component (large-N) plan;
+            # direct: the direct kernel
             for path, env in (("tiled", {"ADHA_SMALL_BYTES": "0"}),
-                              ("tiled_tma", {"ADHA_SMALL_BYTES": "0", "ADHA_LDGSTS_BYTES": "0"}),
-                              ("tiled_components", {"ADHA_SMALL_BYTES": "0", "ADHA_MERGE_BYTES": "0",
-                                                    "ADHA_LDGSTS_BYTES": "0"}),
+                              ("tiled_merged", {"ADHA_SMALL_BYTES": "0", "ADHA_MERGE_BYTES": str(1 << 40)}),
+                              ("tiled_components", {"ADHA_SMALL_BYTES": "0", "ADHA_MERGE_BYTES": "0"}),
                               ("direct", {"ADHA_SMALL_BYTES": str(1 << 40)})):
-                for k in ("ADHA_SMALL_BYTES", "ADHA_MERGE_BYTES", "ADHA_LDGSTS_BYTES"):
+                for k in ("ADHA_SMALL_BYTES", "ADHA_MERGE_BYTES"):
                     os.environ.pop(k, None)
                 os.environ.update(env)
                 out[path + "_us"] = round(graph_us(lambda: A.remap(src, Ls, dst, Ld, n)), 2)
-            for k in ("ADHA_SMALL_BYTES", "ADHA_MERGE_BYTES", "ADHA_LDGSTS_BYTES"):
+            for k in ("ADHA_SMALL_BYTES", "ADHA_MERGE_BYTES"):
                 os.environ.pop(k, None)
             out["default_us"] = round(graph_us(lambda: A.remap(src, Ls, dst, Ld, n)), 2)
             print(json.dumps(out), flush=True)
