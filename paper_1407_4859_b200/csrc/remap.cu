@@ -303,8 +303,9 @@ adha_status remap_checked(const uint8_t* src, const Layout& ls, uint8_t* dst, co
     // clusters must stay untouched, which needs their own skipped component).
     // the direct-path threshold is the component plan's (its crossover with the tiled kernel
     // was measured per component count; the merged plan only replaces the tiled side of it)
-    const uint64_t thr = ck.dst_local ? direct_bytes(*plan) : small_bytes();
-    if (plan->comps.size() > 1 && (uint64_t)n * ls.record_bytes <= merge_bytes()) {
+    const uint64_t thr = (ck.dst_local && ck.src_local) ? direct_bytes(*plan) : small_bytes();
+    // (a src in host memory keeps the component plan: its tiles read larger chunks over PCIe)
+    if (plan->comps.size() > 1 && ck.src_local && (uint64_t)n * ls.record_bytes <= merge_bytes()) {
         bool alias = false;
         for (const auto& K : plan->comps)
             alias = alias || (K.identity && (uintptr_t)src + ck.bs[K.src_clusters[0]] ==

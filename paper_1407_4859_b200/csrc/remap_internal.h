@@ -17,6 +17,7 @@ struct Checked {
     uint64_t bytes_s = 0, bytes_d = 0;
     std::vector<uint64_t> bs, bd;   // region offsets (relative to the buffer pointers)
     bool dst_local = true;          // dst is this device's HBM (not pinned host or peer memory)
+    bool src_local = true;          // src is this device's HBM (not pinned host memory)
 };
 
 adha_status cuda_fail(cudaError_t e, const char* what);
