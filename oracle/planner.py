@@ -15,10 +15,13 @@ Readings (DESIGN.md "Readings"): Q11-Q14 (affinity = trip*freq-weighted
 co-occurrence, sign rule, Kruskal with inclusive cap, tie-break), Q18 (run
 graph over contiguous runs), Q19 (remap cost = bytes/bandwidth + overhead).
 
-Parity notes: exec_cost's analytic constants are invented by SPEC.md:202
-("model branch invented") -- parity unpinned for absolute values; only the
-structural pins (SPEC examples, paper table shapes) and brute-force equalities
-apply.
+Parity notes: exec_cost's model branch is SPEC.md's own ("model
+branch invented"); its constants (line bytes and time, throughput, penalty) are
+architecture INPUTS, not outputs.  The formula is pinned by SPEC.md:210-212's
+worked examples (3000 vs 1000 line times, linearity, partition invariance of
+streaming bytes) and by properties of the definition (coalescing penalty ratio,
+layout-independent compute term; tests/test_oracle_planner.py); the paper's own
+absolute timings (Tables 3-4) are out of scope.
 """
 from __future__ import annotations
 
@@ -320,7 +323,8 @@ def merge_sections(ss: Sequence[Section]) -> Section:
 def exec_cost(s: Section, l: Layout, d: Device, p: Program, prof: Optional[Profile] = None
               ) -> Tuple[float, float, float, str]:
     """(memory_ns, compute_ns, total_ns, source).  Profile first (PAPER.md:59-60 'tuning
-    profile'); else the analytic model of SPEC.md:205-207 (constants invented: parity unpinned)."""
+    profile'); else the analytic model of SPEC.md:205-207 (its constants are architecture inputs;
+    pinned by SPEC.md:210-212's examples and the tests' invariants)."""
     covered = sorted(x for c in l for x in c)
     if covered != sorted(f.name for f in p.fields):
         raise PlannerError("layout does not span the program fields")

@@ -266,17 +266,22 @@ __global__ void __launch_bounds__(TMAC ? NTHREADS_TMA : NTHREADS, 1)
     // Byte-group mode: the ByteGroups in use (13 words each) and the cluster descriptors, likewise.
     // 128-bit loads: a lane-divergent constant load costs one access per distinct address, so
     // 16 bytes per access instead of 4 (the tables and descriptors are 16-byte aligned).
+    // A one-component unit-mode plan switches component once per CTA: its lanes read their entries
+    // straight from the parameters then, and only the cluster descriptors are copied.
     uint32_t tbl = out0 + p.s_out * p.stage_bytes, scl, dcl, n4 = 0;
+    const bool stbl = NG > 0 || p.n_comp > 1;
     if constexpr (NG == 0) {
         n4 = (p.n_ent + 15) & ~15u;                    // <= NENT (a multiple of 16)
         scl = tbl + 6 * n4;
-        const uint4* offv = reinterpret_cast<const uint4*>(et.off);
-        const uint4* scv = reinterpret_cast<const uint4*>(et.sc);
-        const uint4* dcv = reinterpret_cast<const uint4*>(et.dc);
-        for (uint32_t i = tid; i < n4 / 4; i += NCONS * 32) sts128(tbl + 16 * i, offv[i]);
-        for (uint32_t i = tid; i < n4 / 16; i += NCONS * 32) {
-            sts128(tbl + 4 * n4 + 16 * i, scv[i]);
-            sts128(tbl + 5 * n4 + 16 * i, dcv[i]);
+        if (stbl) {
+            const uint4* offv = reinterpret_cast<const uint4*>(et.off);
+            const uint4* scv = reinterpret_cast<const uint4*>(et.sc);
+            const uint4* dcv = reinterpret_cast<const uint4*>(et.dc);
+            for (uint32_t i = tid; i < n4 / 4; i += NCONS * 32) sts128(tbl + 16 * i, offv[i]);
+            for (uint32_t i = tid; i < n4 / 16; i += NCONS * 32) {
+                sts128(tbl + 4 * n4 + 16 * i, scv[i]);
+                sts128(tbl + 5 * n4 + 16 * i, dcv[i]);
+            }
         }
     } else {
         const uint32_t gbytes = ((uint32_t)sizeof(ByteGroup) * p.n_ent + 15) & ~15u;   // <= sizeof(et.g)
@@ -448,9 +453,9 @@ __global__ void __launch_bounds__(TMAC ? NTHREADS_TMA : NTHREADS, 1)
                 ioff[e] = ooff[e] = din[e] = dout[e] = 0;
                 if ((uint32_t)e < ne) {
                     const uint32_t idx = (p.comp[k].instr_base + warp + NCONS * e) * 32 + lane;
-                    const uint32_t v = lds<uint32_t>(tbl + 4 * idx);
-                    const uint32_t sc = lds<uint8_t>(tbl + 4 * n4 + idx);
-                    const uint32_t dc = lds<uint8_t>(tbl + 5 * n4 + idx);
+                    const uint32_t v = stbl ? lds<uint32_t>(tbl + 4 * idx) : et.off[idx];
+                    const uint32_t sc = stbl ? (uint32_t)lds<uint8_t>(tbl + 4 * n4 + idx) : (uint32_t)et.sc[idx];
+                    const uint32_t dc = stbl ? (uint32_t)lds<uint8_t>(tbl + 5 * n4 + idx) : (uint32_t)et.dc[idx];
                     const uint32_t s_stride = lds<uint32_t>(scl + 16 * sc + 8), s_smem = lds<uint32_t>(scl + 16 * sc + 12);
                     const uint32_t d_stride = lds<uint32_t>(dcl + 16 * dc + 8), d_smem = lds<uint32_t>(dcl + 16 * dc + 12);
                     ioff[e] = s_smem + (v & 0xFFFFu) * (uint32_t)sizeof(U);

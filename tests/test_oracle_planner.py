@@ -247,6 +247,45 @@ def test_streaming_all_fields_partition_invariant_bytes():
         P.exec_cost(p.sections[0], aos, dev, p)[0], rel=1e-15)
 
 
+def test_streaming_coalescing_penalty_and_compute_term():
+    """The two terms of exec_cost that SPEC.md:205-207 defines without a worked example, pinned by
+    properties of the definition rather than by re-evaluating it:
+    (a) on a COALESCING device a fully co-accessed streaming group costs the same bytes under AoS
+        and SoA (SPEC.md:212's invariance), so memory(AoS) / memory(SoA) is exactly the
+        stream_cluster_penalty -- the reason Table 3's GPU side prefers SoA (PAPER.md:131-132);
+        on a non-coalescing device the ratio is 1;
+    (b) compute_ns counts operations, not memory: it is the same under every one of the 52
+        partitions of a 5-field record, for any group pattern, and it is linear in ops and
+        inversely proportional to the device throughput."""
+    names = [f"f{i}" for i in range(32)]
+    p = P.Program("k", 10, [P.Field(n, 4, i) for i, n in enumerate(names)],
+                  [P.Section("k", 7, (P.AccessGroup(tuple(names), 1.0, "streaming"),), ("gpu",))], ["k"])
+    decl = p.decl()
+    soa = P.parse_layout(",".join(names), decl)
+    aos = P.parse_layout("{" + ",".join(names) + "}", decl)
+    for coal, pen in ((True, 3.0), (True, 1.5), (False, 3.0)):
+        dev = P.Device("gpu", 128, 2.0, 1.0, coal, pen, 128)
+        ratio = P.exec_cost(p.sections[0], aos, dev, p)[0] / P.exec_cost(p.sections[0], soa, dev, p)[0]
+        assert ratio == pytest.approx(pen if coal else 1.0, rel=1e-12)
+    # (b) compute term
+    five = ["a", "b", "c", "d", "e"]
+    groups = (P.AccessGroup(("a", "b", "e"), 2.0, "irregular", 6.0), P.AccessGroup(("c", "d"), 0.5, "streaming", 10.0))
+    q = P.Program("q", 10, [P.Field(n, w, i) for i, (n, w) in enumerate(zip(five, [4, 8, 4, 2, 4]))],
+                  [P.Section("s", 1000, groups, ("cpu", "gpu"))], ["s"])
+    layouts = P.enumerate_layouts(five, q.elem_bytes(), None, q.decl())
+    assert len(layouts) == 52
+    for dev in (P.Device("cpu", 64, 1.0, 4.0, False, 1.0, 64), P.Device("gpu", 128, 3.0, 0.5, True, 2.0, 128)):
+        comp = {P.exec_cost(q.sections[0], l, dev, q)[1] for l in layouts}
+        assert len(comp) == 1 and next(iter(comp)) > 0
+    base = P.exec_cost(q.sections[0], layouts[0], P.Device("cpu", 64, 1.0, 4.0, False, 1.0, 64), q)[1]
+    g2 = tuple(P.AccessGroup(g.fields, g.freq, g.pattern, 2 * g.ops) for g in groups)
+    q2 = P.Program("q", 10, q.fields, [P.Section("s", 1000, g2, ("cpu",))], ["s"])
+    assert P.exec_cost(q2.sections[0], layouts[0], P.Device("cpu", 64, 1.0, 4.0, False, 1.0, 64), q2)[1] == \
+        pytest.approx(2 * base, rel=1e-15)
+    assert P.exec_cost(q.sections[0], layouts[0], P.Device("cpu", 64, 1.0, 8.0, False, 1.0, 64), q)[1] == \
+        pytest.approx(base / 2, rel=1e-15)
+
+
 def test_combine_loss_trivial_cases():
     p = simple_program([P.AccessGroup(("A", "B"), 1.0, "irregular")])
     s = p.sections[0]
