@@ -254,15 +254,13 @@ ADHA_API adha_status adha_remap_peer(const void* src, const adha_layout* src_lay
 
 /* End-to-end remap of HOST buffers through the current device: src_host holds
  * bytes(Ls, N), dst_host receives bytes(Ld, N) (only payload bytes written).
- * Strategy (ADHA_HOST_MODE = auto | hybrid | mirror | zero | staged; auto = zero when both host
+ * Strategy (ADHA_HOST_MODE = auto | hybrid | zero | staged; auto = zero when both host
  * buffers are pinned, 256-byte aligned and the src layout has >= 16 clusters (many small
  * H2D copies per chunk otherwise), else hybrid when dst_host is pinned, 256-byte aligned host
  * memory and a scratch is given, else staged):
  *   hybrid  record chunks (~16 MB) are copied host->device into `scratch` (one copy per
  *           src region, copy engine) and each chunk's remap kernel stores its records
  *           straight into dst_host over PCIe: H2D of chunk k+1 overlaps the kernel of k;
- *   mirror  each chunk's remap kernel reads its records straight from src_host (pinned;
- *           TMA over PCIe) into `scratch`, and one D2H copy per dst region writes it back;
  *   zero    one remap kernel reads src_host and writes dst_host directly (both pinned);
  *   staged  H2D per src region, remap in `scratch`, D2H per dst region (pageable memory).
  * `scratch` is a DEVICE buffer of scratch_bytes, 256-byte aligned (may be NULL only

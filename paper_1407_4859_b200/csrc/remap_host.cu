@@ -88,10 +88,6 @@ extern "C" adha_status adha_remap_host(const void* src_host, const adha_layout* 
     //   hybrid  the copy engine streams src chunks into the device scratch (one H2D per src region),
     //           the remap kernel of each chunk writes its records straight into the pinned host dst
     //           over PCIe -- both PCIe directions busy, no D2H copies;
-    //   mirror  the mirror image of hybrid: each chunk's remap kernel reads its records straight
-    //           from the pinned host src (TMA over PCIe) into the device scratch, and the copy
-    //           engine writes the chunk back (one D2H per dst region) -- for layouts with many
-    //           src regions and fewer dst regions;
     //   zero    one remap kernel reads the pinned host src (TMA over PCIe) and writes the pinned
     //           host dst directly, no scratch at all;
     //   staged  H2D per src region, remap in device memory, D2H per dst region (pageable memory).
@@ -104,8 +100,7 @@ extern "C" adha_status adha_remap_host(const void* src_host, const adha_layout* 
         mode = (src_pinned && dst_pinned && aligned && ls.n_clusters() >= 16) ? "zero"
                : (dst_pinned && aligned && scratch)                           ? "hybrid"
                                                                               : "staged";
-    if ((mode == "zero" && !(src_pinned && dst_pinned && aligned)) || (mode == "hybrid" && !(dst_pinned && aligned)) ||
-        (mode == "mirror" && !(src_pinned && aligned)))
+    if ((mode == "zero" && !(src_pinned && dst_pinned && aligned)) || (mode == "hybrid" && !(dst_pinned && aligned)))
         mode = "staged";
     if (mode == "zero") {
         ck.dst_local = false;                // dst is pinned host memory: STG write-back
@@ -114,7 +109,7 @@ extern "C" adha_status adha_remap_host(const void* src_host, const adha_layout* 
     }
 
     if (!scratch || ((uintptr_t)scratch & 255)) return fail(ADHA_ERR_ALIGNMENT, "scratch must be 256-byte aligned");
-    const bool hybrid = mode == "hybrid", mirror = mode == "mirror";
+    const bool hybrid = mode == "hybrid";
     // Records stream through the scratch in chunks of nc records (a multiple of 4096, so host
     // region offsets lo*stride stay 16-byte aligned); each chunk is its own layout instance
     // (record locality).  PIPE_SLOTS chunks are in flight on PIPE_SLOTS internal streams.
@@ -125,7 +120,7 @@ extern "C" adha_status adha_remap_host(const void* src_host, const adha_layout* 
     // region alignment (256 B per region) and a partial last AoSoA block (< 32 records)
     const uint64_t pad = 256ull * (ls.n_clusters() + ld.n_clusters() + 2) + 32 * (Rs + Rd);
     const uint64_t R = Rs;
-    const uint64_t per_rec = hybrid ? Rs : mirror ? Rd : Rs + Rd;
+    const uint64_t per_rec = hybrid ? Rs : Rs + Rd;
     uint64_t slot = 0;
     for (; slots >= 1; --slots) {
         slot = (scratch_bytes / slots) & ~uint64_t(255);
@@ -134,8 +129,7 @@ extern "C" adha_status adha_remap_host(const void* src_host, const adha_layout* 
     if (slots < 1) return fail(ADHA_ERR_INVALID_ARG, "scratch too small for a chunk of 4096 records");
     // chunk: ~16 MB (hybrid) / 64 MB (staged), but at least 4 MB per src region so every H2D
     // copy stays large (C3's 64 SoA regions -> 256 MB chunks)
-    const uint64_t dflt = mirror ? std::max<uint64_t>(16ull << 20, (4ull << 20) * ld.n_clusters())
-                                 : std::max<uint64_t>(hybrid ? (16ull << 20) : (64ull << 20), (4ull << 20) * ls.n_clusters());
+    const uint64_t dflt = std::max<uint64_t>(hybrid ? (16ull << 20) : (64ull << 20), (4ull << 20) * ls.n_clusters());
     const uint64_t chunk_bytes = env_bytes("ADHA_HOST_CHUNK_BYTES", dflt);
     int64_t nc = std::min<int64_t>((int64_t)((slot - pad) / per_rec), (int64_t)std::max<uint64_t>(1, chunk_bytes / R));
     nc = std::max<int64_t>(4096, nc / 4096 * 4096);
@@ -144,7 +138,7 @@ extern "C" adha_status adha_remap_host(const void* src_host, const adha_layout* 
     uint64_t cbytes_s = 0, cbytes_d = 0;
     ls.region_bases(nc, cbs, &cbytes_s);
     ld.region_bases(nc, cbd, &cbytes_d);
-    const uint64_t off_d = mirror ? 0 : align256(cbytes_s);
+    const uint64_t off_d = align256(cbytes_s);
     if ((hybrid ? cbytes_s : off_d + cbytes_d) > slot) return fail(ADHA_ERR_INVALID_ARG, "scratch too small");
 
     HostPipe* hp = nullptr;
@@ -169,27 +163,12 @@ extern "C" adha_status adha_remap_host(const void* src_host, const adha_layout* 
         uint64_t mbs = 0, mbd = 0;
         ls.region_bases(m, ms, &mbs);
         ld.region_bases(m, md, &mbd);
-        Checked cm;
-        if (mirror) {
-            // src regions of this chunk inside the pinned host buffer: base_c(N) + lo * stride_c
-            cm.bs.resize(ls.n_clusters());
-            for (int c = 0; c < ls.n_clusters(); ++c) cm.bs[c] = ck.bs[c] + (uint64_t)lo * ls.stride[c];
-            cm.src_local = false;            // the kernel's TMA loads read pinned host memory
-            cm.bd = md;
-            cm.bytes_d = mbd;
-            if ((s = remap_checked(hsrc, ls, ddst, ld, m, cm, st)) != ADHA_OK) return s;
-            for (int c = 0; c < ld.n_clusters(); ++c) {
-                e = cudaMemcpyAsync(hdst + ck.bd[c] + (uint64_t)lo * ld.stride[c], ddst + md[c],
-                                    ld.region_bytes(c, m), cudaMemcpyDeviceToHost, st);
-                if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync D2H");
-            }
-            continue;
-        }
         for (int c = 0; c < ls.n_clusters(); ++c) {
             e = cudaMemcpyAsync(dsrc + ms[c], hsrc + ck.bs[c] + (uint64_t)lo * ls.stride[c], ls.region_bytes(c, m),
                                 cudaMemcpyHostToDevice, st);
             if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync H2D");
         }
+        Checked cm;
         cm.bs = ms;
         cm.bytes_s = mbs;
         if (hybrid) {

@@ -568,11 +568,12 @@ def test_section_run_matches_numpy():
     assert e.value.name == "ADHA_ERR_UNSUPPORTED"
 
 
-@pytest.mark.parametrize("mode,pinned", [("auto", True), ("hybrid", True), ("mirror", True), ("zero", True),
-                                         ("staged", True), ("auto", False), ("mirror", False)])
+@pytest.mark.parametrize("mode,pinned", [("auto", True), ("hybrid", True), ("zero", True), ("staged", True),
+                                         ("auto", False)])
 def test_remap_host_modes(mode, pinned, monkeypatch):
-    """adha_remap_host in every strategy (hybrid / mirror / zero-copy / staged; pageable memory falls
-    back to staged) equals the oracle, C3-like multi-region layouts included."""
+    """adha_remap_host in every strategy (hybrid / zero-copy / staged; pageable memory falls back to
+    staged) equals the oracle, C3-like multi-region layouts included; auto picks zero-copy for the
+    64-region C3 src."""
     monkeypatch.setenv("ADHA_HOST_MODE", mode)
     monkeypatch.setenv("ADHA_HOST_CHUNK_BYTES", str(1 << 20))     # several chunks
     for widths, ls, ld, n in [(config_widths(16), [0] * 16, list(range(16)), 300_001),
