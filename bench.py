@@ -721,19 +721,24 @@ def main():
     # launches per step: one per remap, except a chain of latency-bound hops, which
     # adha_remap_chain runs as ONE fused launch (remap.cu chain_small: every hop <= ADHA_SMALL_BYTES,
     # <= 16 fields, <= 4 hops, packed layouts, disjoint buffers -- all true for C1)
-    small = int(os.environ.get("ADHA_SMALL_BYTES", 65536))
-    fused_chain = (n_remaps > 1 and os.environ.get("ADHA_CHAIN_FUSE", "1") != "0" and n * R <= small
-                   and len(widths) <= 16 and n_remaps <= 4)
-    launches_per_step = 1 if fused_chain else n_remaps
-    # routing of adha_remap (remap.cu): payload <= the plan's direct_bytes takes the direct kernel
-    direct = (not fused_chain) and n * R <= plan["direct_bytes"]
-    kernel_name = ("remap_chain_small_kernel (fused chain of latency-bound hops)" if fused_chain
+    # routing of adha_remap_chain (remap.cu): one fused launch (tiny chains, or large chains in the
+    # tiled kernel's chain mode) or one remap per hop; a single remap takes the direct kernel at
+    # payloads <= the plan's direct_bytes
+    route, launches_per_step = (A.remap_chain_route(layouts, n) if n_remaps > 1 and not moved
+                                else ("single", 1))
+    direct = route in ("single", "per_hop") and n * R <= plan["direct_bytes"]
+    kernel_name = ("remap_chain_small_kernel (fused chain of latency-bound hops)" if route == "fused_small"
+                   else "remap_tiled_kernel in chain mode (all hops in one launch; each intermediate "
+                        "read back from L2 while it is written to HBM)" if route == "fused_tiled"
                    else "remap_naive_kernel (direct path for remaps <= the plan's direct_bytes)" if direct
                    else "remap_tiled_kernel")
     # the step is those back-to-back launches and nothing else, so the kernel's average launch
     # duration is this rank's event time over the K steps / (K * launches per step)
     avg_launch_ms = ms_total / (args.steps * launches_per_step)
-    bytes_per_launch = 2 * n * R_moved * n_remaps // launches_per_step
+    # algorithmic HBM bytes per launch: 2 N R per remap; the fused tiled chain reads the src once and
+    # writes every intermediate and the dst once ((H + 1) N R), its intermediates come back from L2
+    bytes_per_launch = ((n_remaps + 1) * n * R_moved if route == "fused_tiled"
+                        else 2 * n * R_moved * n_remaps // launches_per_step)
     achieved = bytes_per_launch / (avg_launch_ms * 1e-3) / 1e9
     traffic = ncu_traffic(name)
 
@@ -813,6 +818,7 @@ def main():
                                   if args.soak_s <= 0 else f"after a {args.soak_s:.1f} s untimed soak"),
                 "parallelism": f"shard by contiguous record range over {world} GPU(s), no data-path collective",
                 "kernel": {k: plan[k] for k in ("tiled", "unit", "T", "s_in", "s_out", "smem_bytes", "matched")},
+                "chain_route": route,
                 "cuda_graph": use_graph,
                 "graph_steps_per_launch": GRAPH_STEPS if use_graph else None,
             },
@@ -829,6 +835,10 @@ def main():
                          "peak_source": peak_src,
                          "kernel": kernel_name,
                          "algorithmic_bytes_per_launch": bytes_per_launch,
+                         "algorithmic_bytes_note": ("(H+1) N R: the src read once, every intermediate and the dst "
+                                                    "written once to HBM; the metric's 2 N R per hop counts the "
+                                                    "intermediates' reads too, which come from L2"
+                                                    if route == "fused_tiled" else "2 N R per remap"),
                          "avg_launch_ms": avg_launch_ms},
             "sustained": sustained,
             "planner": planner_times(),

@@ -212,12 +212,27 @@ ADHA_API adha_status adha_remap_regions(const void* const* src_regions, const ad
  * PAPER.md:146): buffers[k] holds the records in layouts[k];
  * for k = 0..n_layouts-2: remap buffers[k] (layouts[k]) -> buffers[k+1]
  * (layouts[k+1]).  Every intermediate is materialised.  Same rules as adha_remap.
- * A chain of latency-bound hops (each <= ADHA_SMALL_BYTES of payload, <= 16 fields, <= 4 hops,
- * packed unblocked layouts, pairwise disjoint buffers) runs as ONE kernel launch with a
- * block-level barrier between hops (ADHA_CHAIN_FUSE=0 disables this); otherwise one remap per
- * hop, in order, on `stream`. */
+ * Routes (adha_remap_chain_route tells which one a call takes):
+ *   1 fused small  every hop <= ADHA_SMALL_BYTES of payload, <= 16 fields, <= 4 hops: ONE
+ *                  launch of the direct chain kernel, a block-level barrier between hops
+ *                  (ADHA_CHAIN_FUSE=0 disables it);
+ *   2 fused tiled  opt-in (ADHA_CHAIN_TILED_BYTES = the payload per hop from which it applies;
+ *                  unset or 0 = off): 2..8 hops, unit-mode plans of one unit size, >= eight tile
+ *                  bands per SM: ONE launch of the tiled kernel in chain mode -- a CTA runs groups
+ *                  of bands through every hop, so hop h reads hop h-1's output back from L2 while
+ *                  it is still written to HBM (HBM traffic (H+1) * N * R instead of 2 * H * N * R
+ *                  for H hops; about as fast as per hop on B200, whose SM side binds);
+ *   0 per hop      one remap per hop, in order, on `stream`.
+ * Both fused routes need packed unblocked layouts and pairwise disjoint buffers. */
 ADHA_API adha_status adha_remap_chain(void* const* buffers, const adha_layout* const* layouts,
                              int32_t n_layouts, int64_t n_records, void* stream);
+
+/* The route adha_remap_chain takes for these layouts and N with pairwise disjoint buffers:
+ * *route = 0 per hop, 1 fused small, 2 fused tiled; *launches = kernel launches of the chain's
+ * remap kernels (1 for the fused routes, n_layouts - 1 per hop).  Host only.
+ * Errors: INVALID_ARG, LAYOUT_MISMATCH, TOO_LARGE. */
+ADHA_API adha_status adha_remap_chain_route(const adha_layout* const* layouts, int32_t n_layouts,
+                                          int64_t n_records, int32_t* route, int32_t* launches);
 
 /* Contiguous shard of N records for shard g of G (reading Q10):
  *     lo = floor(g * N / G),  hi = floor((g + 1) * N / G).

@@ -56,6 +56,8 @@ _SIGS = {
     "adha_remap": (ctypes.c_int, [_vp, _L, _vp, _L, _i64, _vp]),
     "adha_remap_regions": (ctypes.c_int, [ctypes.POINTER(_vp), _L, ctypes.POINTER(_vp), _L, _i64, _vp]),
     "adha_remap_chain": (ctypes.c_int, [ctypes.POINTER(_vp), ctypes.POINTER(_L), _i32, _i64, _vp]),
+    "adha_remap_chain_route": (ctypes.c_int, [ctypes.POINTER(_L), _i32, _i64, ctypes.POINTER(_i32),
+                                              ctypes.POINTER(_i32)]),
     "adha_shard_range": (ctypes.c_int, [_i64, _i32, _i32, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
     "adha_remap_sharded": (ctypes.c_int, [ctypes.POINTER(_vp), _L, ctypes.POINTER(_vp), _L, _i64, _i32,
                                           ctypes.POINTER(_i32), ctypes.POINTER(_vp)]),
@@ -297,6 +299,18 @@ def remap_chain(buffers: Sequence, layouts: Sequence[Layout], n_records: int, st
     bufs = (_vp * len(buffers))(*[_ptr(b) for b in buffers])
     ls = (_L * len(layouts))(*[l.handle for l in layouts])
     _check(_lib.adha_remap_chain(bufs, ls, len(layouts), int(n_records), _stream(stream)))
+
+
+CHAIN_ROUTES = {0: "per_hop", 1: "fused_small", 2: "fused_tiled"}
+
+
+def remap_chain_route(layouts: Sequence[Layout], n_records: int):
+    """(route, launches) adha_remap_chain takes for these layouts and N (disjoint buffers):
+    route in CHAIN_ROUTES' values."""
+    ls = (_L * len(layouts))(*[l.handle for l in layouts])
+    r, k = _i32(), _i32()
+    _check(_lib.adha_remap_chain_route(ls, len(layouts), int(n_records), ctypes.byref(r), ctypes.byref(k)))
+    return CHAIN_ROUTES[r.value], k.value
 
 
 def shard_range(n_total: int, n_shards: int, shard: int):

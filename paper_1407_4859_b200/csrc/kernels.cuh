@@ -112,6 +112,62 @@ __device__ __forceinline__ int64_t t_end(const TiledParams& p) {
 }
 __device__ __forceinline__ int64_t t_step(const TiledParams& p) { return p.blocked ? 1 : (int64_t)gridDim.x; }
 
+// Fused chain (p.chain = H hops, component k = hop k, all with the same T and n_tiles = bands):
+// CTA b owns bands b, b+G, ... and runs them in groups of p.chain_group bands, hop by hop --
+// (j0,h0) (j1,h0) .. (j0,h1) (j1,h1) .. -- so the load of tile (j,h) depends on the store of
+// (j,h-1), issued one group earlier.  Hop h-1's output of band j is read back from L2.
+//
+// TileIter walks a CTA's tiles in either mode without divisions per tile: component k, local
+// tile lt, and (chain) dist = tiles since the same band's previous hop (its group's size, <= 8).
+struct TileIter {
+    int64_t t, lt;          // plain: global tile; both: local tile of component k
+    int64_t q0, bands;      // chain: first band index of the group (per-CTA numbering), bands of this CTA
+    uint32_t k, dist, bb, gsz;
+};
+__device__ __forceinline__ int64_t cta_tiles(const TiledParams& p, uint32_t H) {
+    if (H) {
+        const int64_t nb = p.comp[0].n_tiles;
+        const int64_t q = nb > (int64_t)blockIdx.x ? (nb - 1 - (int64_t)blockIdx.x) / gridDim.x + 1 : 0;
+        return q * H;
+    }
+    const int64_t a = t_first(p), e = t_end(p), st = t_step(p);
+    return a < e ? (e - a + st - 1) / st : 0;
+}
+__device__ __forceinline__ void tile_begin(const TiledParams& p, uint32_t H, TileIter& it) {
+    it.k = 0;
+    it.dist = 0;
+    if (H) {
+        it.bands = cta_tiles(p, H) / H;
+        it.q0 = 0;
+        it.bb = 0;
+        it.gsz = (uint32_t)min((int64_t)p.chain_group, it.bands);
+        it.dist = it.gsz;
+        it.lt = (int64_t)blockIdx.x;
+    } else {
+        it.t = t_first(p);
+        while (it.t >= p.comp[it.k].tile_base + p.comp[it.k].n_tiles && it.k + 1 < p.n_comp) ++it.k;
+        it.lt = it.t - p.comp[it.k].tile_base;
+    }
+}
+__device__ __forceinline__ void tile_next(const TiledParams& p, uint32_t H, TileIter& it) {
+    if (H) {
+        if (++it.bb == it.gsz) {
+            it.bb = 0;
+            if (++it.k == H) {                         // next group of bands
+                it.k = 0;
+                it.q0 += it.gsz;
+                it.gsz = (uint32_t)min((int64_t)p.chain_group, it.bands - it.q0);
+                it.dist = it.gsz;
+            }
+        }
+        it.lt = (int64_t)blockIdx.x + (it.q0 + it.bb) * (int64_t)gridDim.x;
+    } else {
+        it.t += t_step(p);
+        while (it.t >= p.comp[it.k].tile_base + p.comp[it.k].n_tiles && it.k + 1 < p.n_comp) ++it.k;
+        it.lt = it.t - p.comp[it.k].tile_base;
+    }
+}
+
 // 9 warps per CTA: the register file is split over the 4 SM sub-partitions (16K registers
 // each) and one of them holds 3 warps, so a thread may use at most 16384 / 96 = 168 registers;
 // __launch_bounds__(NTHREADS, 1) gives ptxas exactly that budget.
@@ -134,8 +190,12 @@ __global__ void __launch_bounds__(TMAC ? NTHREADS_TMA : NTHREADS, 1)
     const uint32_t in0 = sbase + HDR_BYTES;
     const uint32_t out0 = in0 + p.s_in * p.stage_bytes;
 
+    // fused chain hops (unit mode, table classes up to EMAX 8 only: the largest class has no
+    // registers to spare), 0 = plain
+    const uint32_t H = (NG == 0 && EMAX <= 8) ? p.chain : 0u;
     const uint32_t ofull0 = sbase + 16 * MAX_S_IN;     // s_out mbarriers: output tile permuted (tma_copy)
     const uint32_t oempty0 = ofull0 + 8 * S_OUT_MAX;   // s_out mbarriers: output tile read by its bulk store
+    const uint32_t stored0 = oempty0 + 8 * S_OUT_MAX;  // 8 mbarriers (chain): tile i's stores are visible
     if (threadIdx.x == 0) {
         for (uint32_t s = 0; s < p.s_in; ++s) {
             mbar_init(full0 + 8 * s, 1);
@@ -145,6 +205,7 @@ __global__ void __launch_bounds__(TMAC ? NTHREADS_TMA : NTHREADS, 1)
             mbar_init(ofull0 + 8 * o, NCONS * 32);
             mbar_init(oempty0 + 8 * o, 1);
         }
+        for (uint32_t o = 0; o < 8; ++o) mbar_init(stored0 + 8 * o, NCONS * 32);
         fence_mbarrier_init();
     }
     __syncthreads();
@@ -200,9 +261,13 @@ __global__ void __launch_bounds__(TMAC ? NTHREADS_TMA : NTHREADS, 1)
         int kp = -1;
         uint32_t stage = 0, phase = 0, k = 0;
         ADHA_PT(long long pw = 0; long long pi = 0);
-        for (int64_t t = t_first(p), te = t_end(p); t < te; t += t_step(p)) {
-            while (t >= p.comp[k].tile_base + p.comp[k].n_tiles) ++k;
-            const int64_t lt = t - p.comp[k].tile_base;
+        const int64_t nt = cta_tiles(p, H);
+        TileIter it;
+        tile_begin(p, H, it);
+        for (int64_t i = 0; i < nt; ++i, tile_next(p, H, it)) {
+            k = it.k;
+            const int64_t lt = it.lt;
+            const uint32_t dist = it.dist;
             if ((int)k != kp) {
                 kp = (int)k;
                 const uint32_t T = p.comp[k].T;
@@ -237,6 +302,13 @@ __global__ void __launch_bounds__(TMAC ? NTHREADS_TMA : NTHREADS, 1)
             }
             ADHA_PT(const long long pt0 = clock64());
             mbar_wait(empty0 + 8 * stage, phase ^ 1);
+            // chain: hop k reads what this CTA's consumers stored for the same band at hop k-1
+            // (a ring of 8: consumers finish at most tile i-1 by now, so tile i-dist's phase is the
+            // last one completed on its barrier)
+            if (H && k > 0) {
+                mbar_wait(stored0 + 8 * ((i - dist) & 7), (uint32_t)((i - dist) >> 3) & 1u);
+                fence_proxy_async_global();      // the consumers' stores (released to us) -> our TMA load
+            }
             ADHA_PT(const long long pt1 = clock64(); pw += pt1 - pt0);
             const uint32_t ib = in0 + stage * p.stage_bytes;
             if (lane == 0) mbar_arrive_expect_tx(full0 + 8 * stage, p.comp[k].tile_bytes);
@@ -245,7 +317,7 @@ __global__ void __launch_bounds__(TMAC ? NTHREADS_TMA : NTHREADS, 1)
             for (uint32_t q = 0; q < PMAX; ++q) {
                 if (q < np) {
                     const void* g = (const void*)(pg[q] + (uint64_t)lt * pstep[q]);
-                    if (p.l2_hints & 1) bulk_load_hint(ib + psm[q], g, pbytes[q], full0 + 8 * stage, pol);
+                    if ((p.l2_hints & 1) || (H && p.chain_hints)) bulk_load_hint(ib + psm[q], g, pbytes[q], full0 + 8 * stage, pol);
                     else bulk_load(ib + psm[q], g, pbytes[q], full0 + 8 * stage);
                 }
             }
@@ -298,6 +370,7 @@ __global__ void __launch_bounds__(TMAC ? NTHREADS_TMA : NTHREADS, 1)
         named_bar_sync(1, NCONS * 32);
     }
     const uint64_t spol = policy_evict_first();
+    const uint64_t kpol = policy_evict_last();       // chain: intermediates, read back by the next hop
     uint32_t ioff[EMAX], ooff[EMAX], din[EMAX], dout[EMAX];
     // byte-group mode: per slot j, source words m and output words o of this lane's group
     uint32_t gsrc[GMAX][4], gsst[GMAX][4], gout[GMAX][4], gost[GMAX][4], gsel[GMAX][4][2];
@@ -322,14 +395,15 @@ __global__ void __launch_bounds__(TMAC ? NTHREADS_TMA : NTHREADS, 1)
             const int64_t lo = K.n_tiles * (int64_t)K.T;
             const int64_t n_tail = p.n_records - lo;
             if (n_tail <= 0) continue;
-            const bool own = (K.flags & CF_TAIL_ZERO) != 0;
+            // chain: hop kk's tail reads hop kk-1's tail output, so one CTA runs all hops' tails in order
+            const bool own = (K.flags & CF_TAIL_ZERO) != 0 || H;
             const int64_t items = n_tail * (int64_t)(K.f_hi - K.f_lo);
             // (short tails of many components would otherwise all land on the first CTAs)
             const int64_t gfirst = (gid - acc % gstride + gstride) % gstride;
             if (!own) acc += items;
-            if (own && gridDim.x - 1 - (kk % gridDim.x) != blockIdx.x) continue;
+            if (own && gridDim.x - 1 - (H ? 0u : kk % gridDim.x) != blockIdx.x) continue;
             const int64_t first = own ? tid : gfirst, step = own ? (int64_t)(NCONS * 32) : gstride;
-            if (own) {
+            if (own && (K.flags & CF_TAIL_ZERO)) {
                 // every dst cluster of the component: bytes [lo*stride, ceil(N/B)*B*stride) := 0
                 for (uint32_t f = K.f_lo; f < K.f_hi; ++f) {
                     const FieldDesc fd = et.fields[f];
@@ -375,6 +449,7 @@ __global__ void __launch_bounds__(TMAC ? NTHREADS_TMA : NTHREADS, 1)
                         if (j < nu[m]) dp[m][j] = v[m];
                 }
             }
+            if (H) named_bar_sync(2, NCONS * 32);             // hop kk's tail stored before hop kk+1 reads it
         }
     }
 
@@ -384,9 +459,14 @@ __global__ void __launch_bounds__(TMAC ? NTHREADS_TMA : NTHREADS, 1)
     ADHA_PT(long long ntile = 0);
     constexpr bool tmac = TMAC;      // compile-time: the STG instantiations are the plain kernel
     uint32_t i_t = 0, zeroed = 0;
-    for (int64_t t = t_first(p), te = t_end(p); t < te; t += t_step(p)) {
-        while (t >= p.comp[k].tile_base + p.comp[k].n_tiles) ++k;
-        const int64_t lt = t - p.comp[k].tile_base;
+    const int64_t nt = cta_tiles(p, H);
+    TileIter it;
+    tile_begin(p, H, it);
+    bool stored_pending = false;     // chain: tile i-1's stores not yet fenced and signalled
+    for (int64_t i = 0; i < nt; ++i, tile_next(p, H, it)) {
+        k = it.k;
+        const int64_t lt = it.lt;
+        const uint32_t dist = it.dist;
         const uint32_t T = p.comp[k].T;
         if ((int)k != k_cur) {
             // this warp's instructions of component k: i = warp + NCONS*e; lane's unit = entry i*32 + lane
@@ -567,6 +647,13 @@ __global__ void __launch_bounds__(TMAC ? NTHREADS_TMA : NTHREADS, 1)
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(empty0 + 8 * stage);    // input stage free for the producer
+            if (stored_pending) {
+                // chain: tile i-1's stores were issued a permutation ago, so this fence rarely waits;
+                // then signal that the next hop may load them
+                fence_proxy_async_global();
+                mbar_arrive(stored0 + 8 * ((uint32_t)(i - 1) & 7u));
+                stored_pending = false;
+            }
             ADHA_PT(const long long c2 = clock64(); ph[1] += c2 - c1);
             if (tmac) {
                 fence_proxy_async_smem();                       // this thread's smem writes -> the bulk store
@@ -575,8 +662,21 @@ __global__ void __launch_bounds__(TMAC ? NTHREADS_TMA : NTHREADS, 1)
             } else {
                 named_bar_sync(1, NCONS * 32);                  // output tile complete
                 ADHA_PT(const long long c3 = clock64(); ph[2] += c3 - c2);
-                if (p.l2_hints & 2) copy_out<true>((uint8_t*)p.dst, ob, tid, lt, nv, gofs, gstep, spol);
+                if (H && p.chain_hints)
+                    copy_out<true>((uint8_t*)p.dst, ob, tid, lt, nv, gofs, gstep, k + 1 < H ? kpol : spol);
+                else if (p.l2_hints & 2) copy_out<true>((uint8_t*)p.dst, ob, tid, lt, nv, gofs, gstep, spol);
                 else copy_out<false>((uint8_t*)p.dst, ob, tid, lt, nv, gofs, gstep, spol);
+                if (H) {
+                    // tile i stored: signal after the next tile's permutation (the fence then finds
+                    // the stores done) unless a tile of dist 1 -- a single-band group -- loads them
+                    // next, or this is the CTA's last tile
+                    if (dist >= 2 && i + 1 < nt) {
+                        stored_pending = true;
+                    } else {
+                        fence_proxy_async_global();
+                        mbar_arrive(stored0 + 8 * ((uint32_t)i & 7u));
+                    }
+                }
                 ADHA_PT(ph[3] += clock64() - c3);
                 if (p.s_out == 2) oslot ^= 1;
             }

@@ -512,7 +512,7 @@ namespace detail {
 // unblocked layouts, <= CHAIN_NF fields, <= CHAIN_NH hops, pairwise disjoint buffers).  Returns
 // ADHA_ERR_UNSUPPORTED (no error recorded) when the chain does not qualify.
 adha_status chain_small(void* const* buffers, const adha_layout* const* layouts, int32_t n_layouts, int64_t n,
-                        cudaStream_t st) {
+                        cudaStream_t st, bool launch = true) {
     const char* e = std::getenv("ADHA_CHAIN_FUSE");
     if ((e && *e == '0') || n <= 0 || n_layouts - 1 > CHAIN_NH) return ADHA_ERR_UNSUPPORTED;
     const Layout& l0 = layouts[0]->L;
@@ -533,6 +533,7 @@ adha_status chain_small(void* const* buffers, const adha_layout* const* layouts,
     for (size_t a = 0; a < ranges.size(); ++a)
         for (size_t b = a + 1; b < ranges.size(); ++b)
             if (ranges[a].first < ranges[b].second && ranges[b].first < ranges[a].second) return ADHA_ERR_UNSUPPORTED;
+    if (!launch) return ADHA_OK;
     int n_sm = 0;
     adha_status s = device_setup(nullptr, &n_sm);
     if (s != ADHA_OK) return s;
@@ -558,6 +559,177 @@ adha_status chain_small(void* const* buffers, const adha_layout* const* layouts,
     if (ce != cudaSuccess) return cuda_fail(ce, "remap_chain_small_kernel launch");
     return ADHA_OK;
 }
+
+// Payload per hop from which adha_remap_chain runs a chain as ONE fused tiled launch; 0 (the
+// default) disables it.  Opt in with ADHA_CHAIN_TILED_BYTES.  Measured on B200 (DESIGN.md 6,
+// profiles/r02m_*): on C4 the fused chain moves 8.6 GB through HBM instead of 12.9 and draws
+// 2.4 % less power, but takes 2.04 ms against 2.02 per hop -- the SM side (four shared-memory
+// passes per byte) binds at that rate, not HBM -- and P2 is 8 % slower.
+uint64_t chain_tiled_bytes() {
+    const char* e = std::getenv("ADHA_CHAIN_TILED_BYTES");
+    if (e && *e) return (uint64_t)std::strtoull(e, nullptr, 10);
+    return 0;
+}
+
+// A chain of H remaps as ONE launch of the tiled kernel in chain mode (TiledParams::chain):
+// component h is hop h's merged plan (every field in one component), all hops share the tile
+// size T, and a CTA runs each of its bands through every hop before the next pair of bands, so
+// hop h reads hop h-1's output of the band back from L2 while it is still being written to HBM
+// (each intermediate is still materialised).  HBM traffic drops from 2H to
+// H+1 buffer passes.  Conditions: 2 <= H <= 8, packed unblocked layouts, pairwise disjoint
+// buffers, unit mode with one unit size, >= chain_tiled_bytes() per hop and at least two bands
+// per SM; returns ADHA_ERR_UNSUPPORTED (no error recorded) otherwise.
+adha_status chain_tiled(void* const* buffers, const adha_layout* const* layouts, int32_t n_layouts, int64_t n,
+                        cudaStream_t st, bool launch = true) {
+    const int H = n_layouts - 1;
+    const uint64_t thr = chain_tiled_bytes();
+    if (thr == 0 || H < 2 || H > 8 || n <= 0) return ADHA_ERR_UNSUPPORTED;
+    const Layout& l0 = layouts[0]->L;
+    if ((uint64_t)n * l0.record_bytes < thr) return ADHA_ERR_UNSUPPORTED;
+    std::vector<Checked> ck(H);
+    for (int h = 0; h < H; ++h) {
+        adha_status s = validate(buffers[h], layouts[h], buffers[h + 1], layouts[h + 1], n, &ck[h], true);
+        if (s != ADHA_OK) return s;
+    }
+    std::vector<std::pair<uintptr_t, uintptr_t>> ranges;
+    for (int k = 0; k < n_layouts; ++k) {
+        const Layout& L = layouts[k]->L;
+        for (int c = 0; c < L.n_clusters(); ++c)
+            if (L.block[c] != 1 || L.stride[c] != L.payload(c)) return ADHA_ERR_UNSUPPORTED;
+        const uint64_t bytes = k < H ? ck[k].bytes_s : ck[H - 1].bytes_d;
+        ranges.push_back({(uintptr_t)buffers[k], (uintptr_t)buffers[k] + bytes});
+    }
+    for (size_t a = 0; a < ranges.size(); ++a)
+        for (size_t b = a + 1; b < ranges.size(); ++b)
+            if (ranges[a].first < ranges[b].second && ranges[b].first < ranges[a].second) return ADHA_ERR_UNSUPPORTED;
+    std::vector<std::shared_ptr<const RemapPlan>> plans;
+    uint32_t T = 0, unit = 0, max_w = 0;
+    uint64_t n_ent = 0, n_sc = 0, n_dc = 0, n_f = 0, stage = 0;
+    for (int h = 0; h < H; ++h) {
+        auto pl = get_plan(layouts[h]->L, layouts[h + 1]->L, true);
+        if (!pl->tiled || pl->byte_groups || pl->comps.size() != 1) return ADHA_ERR_UNSUPPORTED;
+        if (unit && pl->unit != unit) return ADHA_ERR_UNSUPPORTED;
+        unit = pl->unit;
+        T = T ? std::min(T, pl->comps[0].T_max) : pl->comps[0].T_max;
+        max_w = std::max(max_w, pl->comps[0].identity ? 0u : pl->comps[0].n_instr);
+        n_ent += pl->ent_off.size();
+        n_sc += pl->src_order.size();
+        n_dc += pl->dst_order.size();
+        n_f += pl->comps[0].fields.size();
+        plans.push_back(pl);
+    }
+    for (int h = 0; h < H; ++h)
+        stage = std::max<uint64_t>(stage, (uint64_t)T * std::max(plans[h]->comps[0].Rs, plans[h]->comps[0].Rd));
+    stage = (stage + 127) / 128 * 128;
+    int cls = -1;
+    for (int c = 0; c < 3 && cls < 0; ++c)       // (the kernel runs chain mode up to class 2)
+        if (n_ent <= (uint64_t)CLASS_NENT[c] && max_w <= (uint32_t)(NCONS * CLASS_EMAX[c])) cls = c;
+    const uint64_t n16 = (n_ent + 15) / 16 * 16;
+    const uint64_t tbl = (6 * n16 + 16 * (n_sc + n_dc) + 127) / 128 * 128;
+    const uint64_t smem = HDR_BYTES + 128 + 4 * stage + tbl;
+    if (cls < 0 || n_sc > MAXC || n_dc > MAXC || n_f > MAXF || stage > STAGE_MAX || smem > 232448)
+        return ADHA_ERR_UNSUPPORTED;
+    int n_sm = 0;
+    adha_status s = device_setup(nullptr, &n_sm);
+    if (s != ADHA_OK) {
+        if (launch) return s;
+        clear_error();          // route query on a host without a device: a B200's 148 SMs
+        n_sm = 148;
+    }
+    const int64_t bands = n / T;
+    if (bands < 8 * (int64_t)n_sm) return ADHA_ERR_UNSUPPORTED;      // a group of bands per CTA
+    if (!launch) return ADHA_OK;
+
+    auto P = std::make_unique<TiledParams>();
+    std::memset(P.get(), 0, sizeof(TiledParams));
+    P->n_records = n;
+    P->stage_bytes = (uint32_t)stage;
+    P->s_in = 2;
+    P->s_out = 2;
+    P->n_comp = (uint32_t)H;
+    P->unit = unit;
+    P->chain = (uint32_t)H;
+    {
+        const char* g = std::getenv("ADHA_CHAIN_GROUP");   // bands per group (1..8)
+        const uint32_t gb = g && *g ? (uint32_t)std::strtoul(g, nullptr, 10) : 8u;
+        P->chain_group = std::min<uint32_t>(8, std::max<uint32_t>(1, gb));
+        const char* ch = std::getenv("ADHA_CHAIN_HINTS");
+        P->chain_hints = (ch && *ch == '0') ? 0u : 1u;
+    }
+    P->total_tiles = bands * H;
+    {
+        const char* hh = std::getenv("ADHA_L2_HINTS");
+        P->l2_hints = hh && *hh ? (uint32_t)std::strtoul(hh, nullptr, 10) : 0u;
+    }
+    // the table image of class cls: off[NENT] | sc[NENT] | dc[NENT] | fields[MAXF]; hop h's
+    // cluster indices are offset by the clusters of hops < h
+    const uint32_t NE = (uint32_t)CLASS_NENT[cls];
+    std::vector<uint32_t> table((6ull * NE + sizeof(FieldDesc) * MAXF + 3) / 4, 0u);
+    uint8_t* img = reinterpret_cast<uint8_t*>(table.data());
+    FieldDesc* fds = reinterpret_cast<FieldDesc*>(img + 6ull * NE);
+    uint32_t sc = 0, dc = 0, ent = 0, instr = 0, fi = 0;
+    for (int h = 0; h < H; ++h) {
+        const RemapPlan& pl = *plans[h];
+        const RemapPlan::Comp& K = pl.comps[0];
+        const Layout& ls = layouts[h]->L;
+        const Layout& ld = layouts[h + 1]->L;
+        CompDesc& D = P->comp[h];
+        D.T = T;
+        D.tile_bytes = T * K.Rs;
+        D.out_bytes = T * K.Rd;
+        D.n_tiles = bands;
+        D.tile_base = (int64_t)h * bands;
+        D.identity = K.identity ? 1 : 0;
+        D.flags = 0;
+        D.instr_base = instr;
+        D.n_instr = K.n_instr;
+        const uint32_t sc0 = sc, dc0 = dc;
+        D.sc_lo = (uint16_t)sc;
+        uint32_t off = 0;
+        for (int c : pl.src_order) {
+            P->srcc[sc++] = {(uint64_t)(uintptr_t)buffers[h] + ck[h].bs[c], (uint32_t)ls.stride[c], off};
+            off += T * (uint32_t)ls.stride[c];
+        }
+        D.sc_hi = (uint16_t)sc;
+        D.dc_lo = (uint16_t)dc;
+        off = 0;
+        for (int c : pl.dst_order) {
+            P->dstc[dc++] = {(uint64_t)(uintptr_t)buffers[h + 1] + ck[h].bd[c], (uint32_t)ld.stride[c], off};
+            off += T * (uint32_t)ld.stride[c];
+        }
+        D.dc_hi = (uint16_t)dc;
+        for (size_t e = 0; e < pl.ent_off.size(); ++e, ++ent) {
+            reinterpret_cast<uint32_t*>(img)[ent] = pl.ent_off[e];
+            img[4ull * NE + ent] = (uint8_t)(pl.ent_sc[e] + sc0);
+            img[5ull * NE + ent] = (uint8_t)(pl.ent_dc[e] + dc0);
+        }
+        instr += K.n_instr;
+        D.f_lo = (uint16_t)fi;
+        for (int f : K.fields) {
+            FieldDesc d;
+            d.sc = (uint8_t)(pl.src_slot[ls.cluster[f]] + sc0);
+            d.dc = (uint8_t)(pl.dst_slot[ld.cluster[f]] + dc0);
+            d.sbl = d.dbl = 0;
+            d.soff = ls.offset[f];
+            d.doff = ld.offset[f];
+            d.width = ls.width[f];
+            fds[fi++] = d;
+        }
+        D.f_hi = (uint16_t)fi;
+    }
+    P->n_ent = ent;
+    P->n_srcc = sc;
+    P->n_dstc = dc;
+    const void* fn = nullptr;
+    TiledLauncher run = pick(unit, cls, false, &fn);
+    s = device_setup(fn, &n_sm, NTHREADS);
+    if (s != ADHA_OK) return s;
+    const int64_t grid = std::min<int64_t>(bands, n_sm);
+    run(dim3((unsigned)grid), dim3(NTHREADS), smem, st, *P, table.data());
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "remap_tiled_kernel (chain) launch");
+    return ADHA_OK;
+}
 }  // namespace detail
 }  // namespace adha
 
@@ -570,10 +742,35 @@ extern "C" adha_status adha_remap_chain(void* const* buffers, const adha_layout*
     const adha_status fused = detail::chain_small(buffers, layouts, n_layouts, n, (cudaStream_t)stream);
     if (fused != ADHA_ERR_UNSUPPORTED) return fused;
     clear_error();
+    const adha_status tiled = detail::chain_tiled(buffers, layouts, n_layouts, n, (cudaStream_t)stream);
+    if (tiled != ADHA_ERR_UNSUPPORTED) return tiled;
+    clear_error();
     for (int32_t k = 0; k + 1 < n_layouts; ++k) {
         adha_status s = adha_remap(buffers[k], layouts[k], buffers[k + 1], layouts[k + 1], n, stream);
         if (s != ADHA_OK) return s;
     }
+    return ADHA_OK;
+}
+
+extern "C" adha_status adha_remap_chain_route(const adha_layout* const* layouts, int32_t n_layouts, int64_t n,
+                                              int32_t* route, int32_t* launches) {
+    clear_error();
+    if (!layouts || n_layouts < 2 || !route || !launches) return fail(ADHA_ERR_INVALID_ARG, "null argument or < 2 layouts");
+    for (int32_t k = 0; k < n_layouts; ++k)
+        if (!layouts[k]) return fail(ADHA_ERR_INVALID_ARG, "null layout");
+    // disjoint stand-in buffers (256-byte aligned, 16 TB apart): the routing assumes the caller's are
+    std::vector<void*> fake(n_layouts);
+    for (int32_t k = 0; k < n_layouts; ++k) fake[k] = (void*)(uintptr_t)((uint64_t)(k + 1) << 44);
+    adha_status s = detail::chain_small(fake.data(), layouts, n_layouts, n, nullptr, false);
+    if (s == ADHA_OK) { *route = 1; *launches = 1; return ADHA_OK; }
+    if (s != ADHA_ERR_UNSUPPORTED) return s;
+    clear_error();
+    s = detail::chain_tiled(fake.data(), layouts, n_layouts, n, nullptr, false);
+    if (s == ADHA_OK) { *route = 2; *launches = 1; return ADHA_OK; }
+    if (s != ADHA_ERR_UNSUPPORTED) return s;
+    clear_error();
+    *route = 0;
+    *launches = n_layouts - 1;
     return ADHA_OK;
 }
 

@@ -98,6 +98,10 @@ struct TiledParams {
     uint32_t n_ent;       // entries used: unit mode 32 * instructions of all components, byte-group mode groups
     uint32_t n_srcc;      // clusters used in srcc / dstc
     uint32_t n_dstc;
+    uint32_t chain;       // 0, or H >= 2: a fused chain of H hops (component k = hop k, adha_remap_chain);
+                          // every component has the same T and n_tiles (bands); regions are absolute
+    uint32_t chain_group; // chain: bands per group (1..8), each group run hop by hop
+    uint32_t chain_hints; // chain: 1 = loads evict_first, intermediates stored evict_last, the last hop evict_first
     CompDesc comp[MAXK];
     ClusterDesc srcc[MAXC];
     ClusterDesc dstc[MAXC];

@@ -668,3 +668,30 @@ def test_inplace_plan_segments_verified_large(shape, monkeypatch):
     widths, ls, ld, n = cases[shape]
     d = _ip(widths, ls, ld, n).describe()
     assert d["moved_slots"] > 0 and d["segments"] * 64 >= d["moved_slots"]
+
+
+def test_remap_chain_route(monkeypatch):
+    """adha_remap_chain's routing (host only): C1's tiny chain -> one fused direct launch; with the
+    fused tiled chain opted in (ADHA_CHAIN_TILED_BYTES), C4 at 2 GiB and P1/P2 at their bench sizes
+    -> one fused tiled launch; a mid-size chain -> one remap per hop; AoSoA-blocked layouts, and
+    the default (fused tiled chain off) -> per hop."""
+    import os
+    monkeypatch.setenv("ADHA_CHAIN_TILED_BYTES", str(64 << 20))
+    w9 = [4] * 9
+    c4 = [A.Layout(w9, l) for l in ([0] * 9, [0, 0, 0, 1, 2, 3, 4, 5, 6], list(range(9)), [0] * 9)]
+    xyz = [A.Layout([4, 4, 4], l) for l in ([0, 0, 0], [0, 1, 2], [0, 0, 0])]
+    assert A.remap_chain_route(xyz, 1024) == ("fused_small", 1)
+    assert A.remap_chain_route(c4, 2 ** 31 // 36) == ("fused_tiled", 1)
+    assert A.remap_chain_route(c4, 300_000) == ("per_hop", 3)
+    p1 = [A.Layout(w9, l) for l in ([0] * 9, [0, 0, 0, 1, 2, 3, 4, 5, 6], list(range(9)))]
+    assert A.remap_chain_route(p1, 256 ** 3) == ("fused_tiled", 1)
+    w32 = [4] * 32
+    p2 = [A.Layout(w32, l) for l in (list(range(32)), [i // 8 for i in range(32)], [0] * 32)]
+    assert A.remap_chain_route(p2, 2 ** 23) == ("fused_tiled", 1)
+    blk = [A.Layout(w9, [0] * 9, blocks=[8] * 9), A.Layout(w9, list(range(9))), A.Layout(w9, [0] * 9)]
+    assert A.remap_chain_route(blk, 2 ** 31 // 36) == ("per_hop", 2)
+    monkeypatch.delenv("ADHA_CHAIN_TILED_BYTES")
+    assert A.remap_chain_route(c4, 2 ** 31 // 36) == ("per_hop", 3)
+    assert os.environ.get("ADHA_CHAIN_TILED_BYTES") is None
+    with pytest.raises(A.AdhaError):
+        A.remap_chain_route([c4[0], A.Layout([4] * 8, [0] * 8)], 10)

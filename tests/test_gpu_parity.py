@@ -337,6 +337,44 @@ def test_small_chain_fused_single_launch(fuse, monkeypatch):
             exp = e
 
 
+@pytest.mark.parametrize("case", ["c4", "p2", "random"])
+def test_chain_fused_tiled(case, monkeypatch):
+    """adha_remap_chain as ONE tiled launch in chain mode (remap.cu chain_tiled; forced with
+    ADHA_CHAIN_TILED_BYTES=1): every band runs through every hop in the same CTA, hop h reading hop
+    h-1's output back; every intermediate is materialised and equals the oracle's chain, byte for
+    byte, including the gaps between regions and ragged tails (a trailing single band per CTA)."""
+    monkeypatch.setenv("ADHA_CHAIN_TILED_BYTES", "1")
+    rng = np.random.default_rng({"c4": 1, "p2": 2, "random": 3}[case])
+    if case == "c4":
+        cases = [([4] * 9, [[0] * 9, AOSV, list(range(9)), [0] * 9], 1_234_567)]
+    elif case == "p2":
+        cases = [([4] * 32, [list(range(32)), [i // 8 for i in range(32)], [0] * 32], 700_001)]
+    else:
+        monkeypatch.setenv("ADHA_TILE_CAP", "512")     # short records: enough bands for two per SM
+        cases = []
+        for _ in range(6):
+            F = int(rng.integers(2, 14))
+            widths = [int(x) for x in rng.choice([4, 4, 8, 12], size=F)]
+            hops = int(rng.integers(2, 5))
+            labs = [[int(x) for x in rng.integers(0, F, size=F)] for _ in range(hops + 1)]
+            cases.append((widths, labs, int(rng.integers(400_000, 900_000))))
+    for widths, labs, n in cases:
+        cols = field_columns(n % 977, n, widths)
+        lays = [A.Layout(widths, l) for l in labs]
+        bufs = [to_dev(O.pack(cols, widths, labs[0], n))] + [sentinel_dev(l.nbytes(n)) for l in lays[1:]]
+        A.remap_chain(bufs, lays, n)
+        torch.cuda.synchronize()
+        exp = O.pack(cols, widths, labs[0], n)
+        for k in range(1, len(labs)):
+            e = np.full(O.layout_bytes(widths, labs[k], n), SENT, np.uint8)
+            O.remap(exp, labs[k - 1], e, labs[k], widths, n, threads=min(8, os.cpu_count() or 1))
+            got = bufs[k].cpu().numpy()[: e.size]
+            if not np.array_equal(got, e):
+                bad = np.nonzero(got != e)[0]
+                raise AssertionError(f"hop {k}: {bad.size} bytes differ, first {bad[:6]} ({widths} {labs} n={n})")
+            exp = e
+
+
 def test_c4_pdl_chain_full_size():
     widths, n = [4] * 9, (2 ** 31) // 36
     labs = [[0] * 9, AOSV, list(range(9)), [0] * 9]

@@ -1,0 +1,13 @@
+# round 2, call k: fused chain with groups of bands
+set -u
+out=gpurun_out
+timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "chain" > $out/k_pytest_chain.log 2>&1; echo "pytest chain=$?"
+for g in 1 2 4 8; do
+  for c in C4 P2; do
+    ADHA_CHAIN_GROUP=$g python bench.py --config $c --no-cpu-baseline --sustained-s 0 --no-e2e --no-copy-ref > $out/k_bench_${c}_g$g.json 2> $out/k_bench_${c}_g$g.err; echo "bench $c g$g=$?"
+  done
+done
+python bench.py --config C4 --steps 6 --warmup 3 --no-cpu-baseline --no-e2e --no-copy-ref --sustained-s 0 > $out/k_plain.log 2>&1 && \
+  ncu --set full --import-source on --clock-control none -k regex:remap_tiled -s 3 -c 1 -o $out/k_prof_c4chain \
+      python bench.py --config C4 --steps 6 --warmup 3 --no-cpu-baseline --no-e2e --no-copy-ref --sustained-s 0 > /dev/null 2>&1
+echo "ncu=$?"
