@@ -178,9 +178,12 @@ using TableOf = typename std::conditional<(NG > 0), GroupTable<NG>, EntryTable<N
 // (GroupTable<NG>, GMAX slots per warp, U = uint8_t for the tails).
 // TMAC: a 10th warp writes the permuted tiles back with TMA bulk stores (TiledParams::tma_copy);
 // otherwise the consumers write them back with STG.
-template <typename U, int NENT, int EMAX, int NG = 0, int GMAX = 1, bool TMAC = false>
+// CHAIN: the fused-chain instantiations (TiledParams::chain; unit mode, STG write-back); the
+// plain ones compile every chain branch away.
+template <typename U, int NENT, int EMAX, int NG = 0, int GMAX = 1, bool TMAC = false, bool CHAIN = false>
 __global__ void __launch_bounds__(TMAC ? NTHREADS_TMA : NTHREADS, 1)
     remap_tiled_kernel(const __grid_constant__ TiledParams p, const __grid_constant__ TableOf<NENT, NG> et) {
+    static_assert(!CHAIN || (NG == 0 && !TMAC), "chain mode: unit mode with STG write-back only");
     extern __shared__ __align__(1024) uint8_t smem[];
     const uint32_t warp = threadIdx.x >> 5;
     const uint32_t lane = threadIdx.x & 31;
@@ -190,9 +193,7 @@ __global__ void __launch_bounds__(TMAC ? NTHREADS_TMA : NTHREADS, 1)
     const uint32_t in0 = sbase + HDR_BYTES;
     const uint32_t out0 = in0 + p.s_in * p.stage_bytes;
 
-    // fused chain hops (unit mode, table classes up to EMAX 8 only: the largest class has no
-    // registers to spare), 0 = plain
-    const uint32_t H = (NG == 0 && EMAX <= 8) ? p.chain : 0u;
+    const uint32_t H = CHAIN ? p.chain : 0u;           // fused chain hops, 0 = plain
     const uint32_t ofull0 = sbase + 16 * MAX_S_IN;     // s_out mbarriers: output tile permuted (tma_copy)
     const uint32_t oempty0 = ofull0 + 8 * S_OUT_MAX;   // s_out mbarriers: output tile read by its bulk store
     const uint32_t stored0 = oempty0 + 8 * S_OUT_MAX;  // 8 mbarriers (chain): tile i's stores are visible
@@ -370,7 +371,7 @@ __global__ void __launch_bounds__(TMAC ? NTHREADS_TMA : NTHREADS, 1)
         named_bar_sync(1, NCONS * 32);
     }
     const uint64_t spol = policy_evict_first();
-    const uint64_t kpol = policy_evict_last();       // chain: intermediates, read back by the next hop
+    const uint64_t kpol = CHAIN ? policy_evict_last() : 0;   // chain: intermediates, read back by the next hop
     uint32_t ioff[EMAX], ooff[EMAX], din[EMAX], dout[EMAX];
     // byte-group mode: per slot j, source words m and output words o of this lane's group
     uint32_t gsrc[GMAX][4], gsst[GMAX][4], gout[GMAX][4], gost[GMAX][4], gsel[GMAX][4][2];

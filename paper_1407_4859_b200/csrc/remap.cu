@@ -63,6 +63,32 @@ const void* tiled_fn() {
     return (const void*)&remap_tiled_kernel<U, NENT, EMAX, 0, 1, TMAC>;
 }
 
+// fused-chain instantiations (classes 0..2; chain_tiled never picks the largest class)
+template <typename U, int CLS>
+void launch_chain(dim3 grid, dim3 block, size_t smem, cudaStream_t st, const TiledParams& p, const void* table) {
+    constexpr int NENT = CLASS_NENT[CLS];
+    constexpr int EMAX = CLASS_EMAX[CLS];
+    remap_tiled_kernel<U, NENT, EMAX, 0, 1, false, true><<<grid, block, smem, st>>>(
+        p, *static_cast<const EntryTable<NENT>*>(table));
+}
+template <typename U, int CLS>
+const void* chain_fn() {
+    return (const void*)&remap_tiled_kernel<U, CLASS_NENT[CLS], CLASS_EMAX[CLS], 0, 1, false, true>;
+}
+template <typename U>
+TiledLauncher pick_chain_cls(int cls, const void** fn) {
+    switch (cls) {
+        case 0: *fn = chain_fn<U, 0>(); return &launch_chain<U, 0>;
+        case 1: *fn = chain_fn<U, 1>(); return &launch_chain<U, 1>;
+        default: *fn = chain_fn<U, 2>(); return &launch_chain<U, 2>;
+    }
+}
+TiledLauncher pick_chain(uint32_t unit, int cls, const void** fn) {
+    if (unit == 4) return pick_chain_cls<uint32_t>(cls, fn);
+    if (unit == 2) return pick_chain_cls<uint16_t>(cls, fn);
+    return pick_chain_cls<uint8_t>(cls, fn);
+}
+
 template <typename U, bool TMAC>
 TiledLauncher pick_cls(int cls, const void** fn) {
     switch (cls) {
@@ -721,7 +747,7 @@ adha_status chain_tiled(void* const* buffers, const adha_layout* const* layouts,
     P->n_srcc = sc;
     P->n_dstc = dc;
     const void* fn = nullptr;
-    TiledLauncher run = pick(unit, cls, false, &fn);
+    TiledLauncher run = pick_chain(unit, cls, &fn);
     s = device_setup(fn, &n_sm, NTHREADS);
     if (s != ADHA_OK) return s;
     const int64_t grid = std::min<int64_t>(bands, n_sm);
