@@ -349,6 +349,12 @@ ADHA_API void adha_inplace_plan_destroy(adha_inplace_plan* plan);
 ADHA_API adha_status adha_remap_plan_describe(const adha_layout* src_layout, const adha_layout* dst_layout,
                                      char** json_out);
 
+/* The same for the MERGED plan of the pair (merged != 0: every cluster in one component, the
+ * plan adha_remap runs for multi-component remaps of up to ADHA_MERGE_BYTES), or for the
+ * component plan (merged == 0, = adha_remap_plan_describe). */
+ADHA_API adha_status adha_remap_plan_describe_ex(const adha_layout* src_layout, const adha_layout* dst_layout,
+                                               int32_t merged, char** json_out);
+
 /* ------------------------------------------------------------------ planner (host)
  *
  * Inputs are UTF-8 JSON documents in the SPEC.md schemas (schema_version 1):

@@ -64,6 +64,7 @@ _SIGS = {
     "adha_remap_host": (ctypes.c_int, [_vp, _L, _vp, _L, _i64, _vp, _u64, _vp]),
     "adha_remap_peer": (ctypes.c_int, [_vp, _L, _i32, _vp, _L, _i32, _i64, _vp]),
     "adha_remap_plan_describe": (ctypes.c_int, [_L, _L, ctypes.POINTER(_vp)]),
+    "adha_remap_plan_describe_ex": (ctypes.c_int, [_L, _L, _i32, ctypes.POINTER(_vp)]),
     "adha_plan_ods": (ctypes.c_int, [_cp, _cp, _cp, _cp, ctypes.POINTER(_vp)]),
     "adha_plan_pdl": (ctypes.c_int, [_cp, _cp, _cp, ctypes.POINTER(_vp)]),
     "adha_plan_candidates": (ctypes.c_int, [_cp, _cp, _cp, ctypes.POINTER(_vp)]),
@@ -365,9 +366,11 @@ def _take_string(p: ctypes.c_void_p) -> str:
     return s
 
 
-def plan_describe(src_layout: Layout, dst_layout: Layout) -> dict:
+def plan_describe(src_layout: Layout, dst_layout: Layout, merged: bool = False) -> dict:
+    """The compiled remap plan (adha_remap_plan_describe_ex): the component plan, or with
+    merged=True the one-component plan used for small and mid-size multi-component remaps."""
     p = _vp()
-    _check(_lib.adha_remap_plan_describe(src_layout.handle, dst_layout.handle, ctypes.byref(p)))
+    _check(_lib.adha_remap_plan_describe_ex(src_layout.handle, dst_layout.handle, 1 if merged else 0, ctypes.byref(p)))
     return json.loads(_take_string(p))
 
 

@@ -909,12 +909,17 @@ extern "C" __attribute__((visibility("default"))) int adha_debug_phase(unsigned 
 
 // ---------------------------------------------------------------------------- host end-to-end
 extern "C" adha_status adha_remap_plan_describe(const adha_layout* hs, const adha_layout* hd, char** json_out) {
+    return adha_remap_plan_describe_ex(hs, hd, 0, json_out);
+}
+
+extern "C" adha_status adha_remap_plan_describe_ex(const adha_layout* hs, const adha_layout* hd, int32_t merged,
+                                                   char** json_out) {
     clear_error();
     if (!hs || !hd || !json_out) return fail(ADHA_ERR_INVALID_ARG, "null argument");
     if (hs->L.n_fields != hd->L.n_fields) return fail(ADHA_ERR_LAYOUT_MISMATCH, "layouts differ in field count");
     for (int f = 0; f < hs->L.n_fields; ++f)
         if (hs->L.width[f] != hd->L.width[f]) return fail(ADHA_ERR_LAYOUT_MISMATCH, "widths differ");
-    auto plan = get_plan(hs->L, hd->L);
+    auto plan = get_plan(hs->L, hd->L, merged != 0);
     std::string s = describe_plan(*plan, hs->L, hd->L);
     // routing threshold of adha_remap for this pair (device dst): payload <= direct_bytes takes the
     // direct kernel (ADHA_SMALL_BYTES overrides, read now)

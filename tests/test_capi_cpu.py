@@ -218,13 +218,16 @@ def test_cpp_planner_equals_oracle_random():
 
 # ---------------------------------------------------------------- remap-plan compiler (host)
 
-def _plan_checks(widths, ls, ld):
+def _plan_checks(widths, ls, ld, merged=False):
     from tests.test_oracle_remap import clusters_in_order
     Ls, Ld = A.Layout(widths, ls), A.Layout(widths, ld)
-    d = A.plan_describe(Ls, Ld)
+    d = A.plan_describe(Ls, Ld, merged=merged)
     assert d["tiled"], d["why_naive"]
+    if merged:
+        assert len(d["components"]) == 1
     if d["byte_groups"]:
-        _check_byte_groups(widths, ls, ld)
+        if not merged:
+            _check_byte_groups(widths, ls, ld)
         return d
     g = d["unit"]
     cs, cd = clusters_in_order(ls), clusters_in_order(ld)          # canonical clusters (field lists)
@@ -296,6 +299,29 @@ def test_plan_compiler_tables():
         F = rng.randint(1, 10)
         widths = [rng.choice([1, 2, 3, 4, 8]) for _ in range(F)]
         _plan_checks(widths, [rng.randrange(F) for _ in range(F)], [rng.randrange(F) for _ in range(F)])
+
+
+def test_merged_plan_tables():
+    """The merged plan (one component over every cluster; remap.cu runs it for multi-component
+    remaps up to ADHA_MERGE_BYTES) passes the same table checks: every unit of the 32-record period
+    moved once to the oracle's address, 32 distinct banks per instruction on both sides."""
+    w64 = [8 if i % 4 == 3 else 4 for i in range(64)]
+    hyb = P.parse_layout(golden("expected.json")["c3_hybrid"]["value"], {f"f{i}": i for i in range(64)})
+    lab = [0] * 64
+    for c, cl in enumerate(hyb):
+        for n in cl:
+            lab[int(n[1:])] = c
+    d = _plan_checks(w64, list(range(64)), lab, merged=True)             # C3 SoA -> hybrid
+    assert d["matched"] and d["components"][0]["n_instr"] == 80
+    _plan_checks(w64, lab, list(range(64)), merged=True)                 # C3 hybrid -> SoA
+    med = [4] * 9
+    _plan_checks(med, [0, 0, 0, 1, 2, 3, 4, 5, 6], list(range(9)), merged=True)   # Medical AoSV -> SoA
+    rng = random.Random(12)
+    for _ in range(40):
+        F = rng.randint(2, 16)
+        widths = [rng.choice([4, 4, 8, 12]) for _ in range(F)]
+        _plan_checks(widths, [rng.randrange(F) for _ in range(F)], [rng.randrange(F) for _ in range(F)],
+                     merged=True)
 
 
 def test_plan_falls_back_beyond_limits():

@@ -13,7 +13,7 @@ import pytest
 
 from adha_inputs import config_widths, field_columns, tagged_columns, fill_random_device, SEED_BASE
 from oracle import remap as O
-from tests.gpu_util import SENT, run_remap, sample_records, gather_fields_dev, sentinel_dev, to_dev, exact_chunked_check
+from tests.gpu_util import SENT, run_remap, sentinel_dev, to_dev, exact_chunked_check
 from tests.test_oracle_remap import set_partitions
 
 pytestmark = pytest.mark.gpu
@@ -204,23 +204,6 @@ def test_c2_full_size_every_byte():
     assert np.array_equal(dst.cpu().numpy(), exp)
 
 
-def sampled_check(src, Ls_lab, dst, Ld_lab, widths, n, T, seed=0, extra=()):
-    recs = sample_records(n, T, seed=seed)
-    if len(extra):
-        recs = np.unique(np.concatenate([recs, np.asarray([r for r in extra if 0 <= r < n], np.int64)]))
-    bs, ss, os_, _ = O.field_addresses(widths, Ls_lab, n)
-    bd, sd, od, tot = O.field_addresses(widths, Ld_lab, n)
-    a = gather_fields_dev(src, widths, bs, ss, os_, recs)
-    b = gather_fields_dev(dst, widths, bd, sd, od, recs)
-    assert np.array_equal(a, b), f"{np.count_nonzero((a != b).any(1))} sampled records differ"
-    # gap bytes (between regions) still hold the sentinel
-    regions = sorted({(int(bd[f]), int(sd[f])) for f in range(len(widths))})
-    for (b0, s0), (b1, _) in zip(regions, regions[1:]):
-        gap = dst[b0 + n * s0: b1]
-        if gap.numel():
-            assert bool((gap == SENT).all())
-
-
 @pytest.mark.parametrize("cfg", ["C3", "C3R", "C5"])
 def test_full_size_exact(cfg):
     """The bench workloads at full size, EVERY payload byte against the oracle by record-range
@@ -245,8 +228,8 @@ def test_full_size_exact(cfg):
 @pytest.mark.parametrize("widths", [[4, 4], [1, 2, 1]], ids=["unit4", "byte-groups"])
 def test_max_size_beyond_2_31_records(widths):
     """Maximum sizes: N > 2^31 records, so record indices need 64 bits and region offsets pass
-    2^32 bytes (unit-4 permute path and byte-group path).  Sampled records around every 2^k
-    boundary that a 32-bit index or byte offset would break at."""
+    2^32 bytes (unit-4 permute path and byte-group path); every payload byte against the oracle,
+    so every 2^k boundary a 32-bit index or byte offset would break at is covered."""
     n = 2 ** 31 + 4099
     F = len(widths)
     aos, soa = [0] * F, list(range(F))
@@ -256,19 +239,16 @@ def test_max_size_beyond_2_31_records(widths):
     dst = sentinel_dev(Ls.nbytes(n))
     A.remap(src, La, dst, Ls, n)
     torch.cuda.synchronize()
-    R = sum(widths)
-    edges = []
-    for b in (2 ** 30, 2 ** 31, 2 ** 32 // R, 2 ** 31 // R, 2 ** 32 // widths[0]):
-        edges += list(range(b - 40, b + 40))
-    sampled_check(src, aos, dst, soa, widths, n, plan_T(widths, aos, soa), extra=edges)
+    assert exact_chunked_check(O, src, aos, dst, soa, widths, n, chunk=1 << 24) == n * sum(widths)
     del src, dst
     torch.cuda.empty_cache()
 
 
 @pytest.mark.parametrize("cfg", ["P1", "P2"])
-def test_paper_shaped_chains_full_size_sampled(cfg):
+def test_paper_shaped_chains_full_size_exact(cfg):
     """The extra paper-shaped bench configs at their bench sizes (P1 Medical 256^3 AoS->AoSV->SoA,
-    P2 K-Means 2^23 SoA->4xAoS8->AoS), through adha_remap_chain; sampled records per edge."""
+    P2 K-Means 2^23 SoA->4xAoS8->AoS), through adha_remap_chain; every payload byte of every hop
+    against the oracle (record-range chunks)."""
     if cfg == "P1":
         widths, n, labs = [4] * 9, 256 ** 3, [[0] * 9, AOSV, list(range(9))]
     else:
@@ -281,17 +261,16 @@ def test_paper_shaped_chains_full_size_sampled(cfg):
     A.remap_chain(bufs, lays, n)
     torch.cuda.synchronize()
     for k in range(len(labs) - 1):
-        sampled_check(bufs[k], labs[k], bufs[k + 1], labs[k + 1], widths, n,
-                      plan_T(widths, labs[k], labs[k + 1]), seed=k)
+        assert exact_chunked_check(O, bufs[k], labs[k], bufs[k + 1], labs[k + 1], widths, n) == n * sum(widths)
     del bufs
     torch.cuda.empty_cache()
 
 
 @pytest.mark.parametrize("widths,kind", [([2, 4, 6, 4] * 4, "aos2soa"), ([2, 4, 6, 4] * 4, "soa2aos"),
                                          ([1] * 24 + [8], "aos2soa"), ([1, 3, 4, 8] * 4, "soa2aos")])
-def test_byte_groups_large_n_sampled(widths, kind):
+def test_byte_groups_large_n_exact(widths, kind):
     """The byte-group path (1/2-byte units) at the narrow-probe size N = 20M, in the tile
-    configuration it runs there; sampled records around tile and tail boundaries."""
+    configuration it runs there; every payload byte against the oracle (record-range chunks)."""
     n = 20_000_003
     F = len(widths)
     ls, ld = ([0] * F, list(range(F))) if kind == "aos2soa" else (list(range(F)), [0] * F)
@@ -302,7 +281,7 @@ def test_byte_groups_large_n_sampled(widths, kind):
     dst = sentinel_dev(Ld.nbytes(n))
     A.remap(src, Ls, dst, Ld, n)
     torch.cuda.synchronize()
-    sampled_check(src, ls, dst, ld, widths, n, plan_T(widths, ls, ld))
+    assert exact_chunked_check(O, src, ls, dst, ld, widths, n) == n * sum(widths)
     del src, dst
     torch.cuda.empty_cache()
 
