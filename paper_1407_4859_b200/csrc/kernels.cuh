@@ -1,6 +1,7 @@
 // kernels.cuh -- device code of the remap (included by remap.cu only): the tiled kernel
-// (TMA-staged tiles, shared-memory permutation in unit or byte-group mode, 16-byte copy-out),
-// the direct kernel for small remaps / layouts beyond the tiled kernel's limits, and the zero
+// (TMA-staged tiles, shared-memory permutation in unit or byte-group mode, 16-byte copy-out;
+// its CHAIN instantiations run a whole PDL chain in one launch), the direct kernel for small
+// remaps / layouts beyond the tiled kernel's limits, the fused small-chain kernel, and the zero
 // kernel.  Design: remap.cu header comment and DESIGN.md section 6.
 #pragma once
 

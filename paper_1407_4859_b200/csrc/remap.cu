@@ -1,7 +1,7 @@
 // remap.cu -- host side of the ADHA remap on B200 (sm_100a): plan cache, per-device setup,
 // kernel-parameter assembly and launch, and the remap entry points of the C ABI
-// (adha_remap, adha_remap_regions, adha_remap_chain, adha_remap_sharded,
-// adha_remap_plan_describe).  Device code: kernels.cuh.
+// (adha_remap, adha_remap_regions, adha_remap_chain, adha_remap_chain_route, adha_remap_sharded,
+// adha_remap_peer, adha_remap_plan_describe[_ex]).  Device code: kernels.cuh.
 //
 // What it computes (adha.h): for all records i and fields f
 //     dst[addr_Ld(f,i) .. +w_f) = src[addr_Ls(f,i) .. +w_f)
@@ -11,8 +11,12 @@
 // Routing per call: the tiled kernel (persistent CTAs, one per SM: a TMA producer warp
 // streams src chunks of T-record tiles into shared memory, eight consumer warps permute them
 // -- conflict-free 4-byte units, or PRMT byte groups for 1/2-byte units -- and write the dst
-// chunks back with 16-byte stores); the direct kernel for remaps of <= ADHA_SMALL_BYTES
-// (launch-latency bound) and layouts beyond the tiled limits (> 256 fields, ...).
+// chunks back with 16-byte stores), on the component plan at large N and on the merged
+// one-component plan for multi-component remaps up to merge_bytes(); the direct kernel for
+// remaps up to direct_bytes(plan) (latency bound) and layouts beyond the tiled limits (> 256
+// fields, ...).  adha_remap_chain adds two one-launch routes: the fused direct chain for tiny
+// chains and (opt-in) the tiled kernel in chain mode, which keeps each intermediate in L2
+// between hops (chain_tiled below).
 #include <cuda_runtime.h>
 
 #include <cstdlib>
