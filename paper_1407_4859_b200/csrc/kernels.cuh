@@ -486,18 +486,38 @@ __global__ void __launch_bounds__(TMAC ? NTHREADS_TMA : NTHREADS, 1)
             if constexpr (NG > 0) {
                 // G groups per period -> I instructions of 32 lanes; with I < NCONS the periods are
                 // split over P = NCONS / I warps per instruction (slot s -> instruction s % I,
-                // periods q = s / I (mod P))
+                // periods q = s / I (mod P)).  When NCONS * GMAX slots do not divide evenly by I
+                // (GMAX = 2, I = 3, 5, 6, 7) that leaves some warps a slot more than others, so the
+                // I x periods (instruction, period) items are cut into NCONS equal contiguous
+                // ranges instead -- one per warp, at most two instructions each, periods step 1.
+                // grho[j] = first period | end period << 16 of slot j.
                 const uint32_t G = p.comp[k].n_instr;
                 const uint32_t I = (G + 31) / 32;
-                gP = I ? max(1u, (uint32_t)(NCONS * GMAX) / I) : 1u;
+                const uint32_t P = T / 32;
+                const bool bal = GMAX == 2 && I > 0 && I <= (uint32_t)NCONS && ((uint32_t)(NCONS * GMAX) % I) != 0;
+                gP = bal ? 1u : (I ? max(1u, (uint32_t)(NCONS * GMAX) / I) : 1u);
 #pragma unroll
                 for (int j = 0; j < GMAX; ++j) {
                     gns[j] = gno[j] = 0;
                     grho[j] = 0;
-                    const uint32_t slot = warp + NCONS * j;
-                    if (I && slot < I * gP) {
-                        const uint32_t i = slot % I, gi = i * 32 + lane;
-                        grho[j] = slot / I;
+                    uint32_t i, q0, q1;
+                    bool ok;
+                    if (bal) {
+                        const uint32_t items = I * P, lo = warp * items / NCONS, hi = (warp + 1) * items / NCONS;
+                        i = lo / P + (uint32_t)j;
+                        q0 = j == 0 ? lo - (lo / P) * P : 0u;
+                        q1 = hi > i * P ? min(P, hi - i * P) : 0u;
+                        ok = i < I && q0 < q1;
+                    } else {
+                        const uint32_t slot = warp + NCONS * j;
+                        ok = I && slot < I * gP;
+                        i = ok ? slot % I : 0u;
+                        q0 = ok ? slot / I : 0u;
+                        q1 = P;
+                    }
+                    if (ok) {
+                        const uint32_t gi = i * 32 + lane;
+                        grho[j] = q0 | (q1 << 16);
                         if (gi < G) {
                             // the group from its shared-memory copy (13 words, ByteGroup layout)
                             const uint32_t ga = tbl + (uint32_t)sizeof(ByteGroup) * (p.comp[k].instr_base + gi);
@@ -584,11 +604,11 @@ __global__ void __launch_bounds__(TMAC ? NTHREADS_TMA : NTHREADS, 1)
                 }
                 for (; v < tb; v += NCONS * 32 * 16) sts128(ob + v, lds128(ib + v));
             } else if constexpr (NG > 0) {
-                const uint32_t periods = T / 32;
 #pragma unroll
                 for (int j = 0; j < GMAX; ++j) {
                     if (gno[j]) {
-                        uint32_t q = grho[j];
+                        uint32_t q = grho[j] & 0xFFFFu;
+                        const uint32_t periods = grho[j] >> 16;      // this slot's end period
                         // two periods per iteration: 8 independent shared loads in flight
                         for (; q + gP < periods; q += 2 * gP) {
                             uint32_t w[2][4];

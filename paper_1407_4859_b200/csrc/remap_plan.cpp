@@ -606,7 +606,10 @@ RemapPlan compile_plan(const Layout& ls, const Layout& ld, bool merge) {
                 const uint32_t S = (uint32_t)(NCONS * GCLASS_GMAX[1]);
                 std::vector<ByteGroup> v;
                 double vt = 1e300;
+                // the busiest warp's share of one period's instructions (kernels.cuh: with
+                // I <= NCONS not dividing the slots, warps take equal (instruction, period) ranges)
                 auto busy = [&](uint32_t I) {
+                    if (I <= (uint32_t)NCONS && S % I != 0) return (double)I / NCONS;
                     const uint32_t gP = std::max<uint32_t>(1, S / I);
                     return (double)((I * gP + NCONS - 1) / NCONS) / gP;
                 };
