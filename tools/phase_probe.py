@@ -60,6 +60,35 @@ if "--small" in sys.argv:
                                    ("g2 AoS->SoA", [2, 4, 6, 4] * 4, [0] * 16, list(range(16))),
                                    ("Medical AoSV->SoA", [4] * 9, [0, 0, 0, 1, 2, 3, 4, 5, 6], list(range(9)))]
              for mb in (1, 32)]
+lib.adha_remap_chain.argtypes = [ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_void_p), ctypes.c_int32,
+                                 ctypes.c_int64, ctypes.c_void_p]
+if "--chain" in sys.argv:
+    # C4's chain AoS -> AoSV -> SoA -> AoS at 2 GiB, per hop or fused (ADHA_CHAIN_TILED_BYTES)
+    labs = [[0] * 9, [0, 0, 0, 1, 2, 3, 4, 5, 6], list(range(9)), [0] * 9]
+    n = (2 ** 31) // 36
+    hs = [layout([4] * 9, l) for l in labs]
+    bufs = [torch.empty(nbytes(h, n), dtype=torch.uint8, device="cuda") for h in hs]
+    bp = (ctypes.c_void_p * 4)(*[b.data_ptr() for b in bufs])
+    lp = (ctypes.c_void_p * 4)(*[h.value for h in hs])
+    stream = torch.cuda.current_stream().cuda_stream
+    for _ in range(2):
+        assert lib.adha_remap_chain(bp, lp, 4, n, stream) == 0
+    torch.cuda.synchronize()
+    phases(reset=True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(5):
+        lib.adha_remap_chain(bp, lp, 4, n, stream)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 5
+    p = phases(reset=True)
+    tiles = max(1, p[4])
+    per = [x / tiles for x in p[:4]]
+    print(f"C4 chain ({os.environ.get('ADHA_CHAIN_TILED_BYTES', 'per hop')}): {ms:.3f} ms, {3 * 2 * n * 36 / ms / 1e6:.0f} GB/s; "
+          f"per tile & warp (clk): wait_full {per[0]:.0f} permute {per[1]:.0f} barrier {per[2]:.0f} copy_out {per[3]:.0f}; "
+          f"producer wait_empty/tile {p[5] / (tiles / 8):.0f} issue/tile {p[6] / (tiles / 8):.0f}", flush=True)
+    sys.exit(0)
 stream = torch.cuda.current_stream().cuda_stream
 for name, w, ls, ld, n in cases:
     Ls, Ld = layout(w, ls), layout(w, ld)
