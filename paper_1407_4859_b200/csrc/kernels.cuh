@@ -181,10 +181,12 @@ using TableOf = typename std::conditional<(NG > 0), GroupTable<NG>, EntryTable<N
 // otherwise the consumers write them back with STG.
 // CHAIN: the fused-chain instantiations (TiledParams::chain; unit mode, STG write-back); the
 // plain ones compile every chain branch away.
+// The plan's table (TableOf<NENT, NG>) is read from its device copy at p.table.
 template <typename U, int NENT, int EMAX, int NG = 0, int GMAX = 1, bool TMAC = false, bool CHAIN = false>
 __global__ void __launch_bounds__(TMAC ? NTHREADS_TMA : NTHREADS, 1)
-    remap_tiled_kernel(const __grid_constant__ TiledParams p, const __grid_constant__ TableOf<NENT, NG> et) {
+    remap_tiled_kernel(const __grid_constant__ TiledParams p) {
     static_assert(!CHAIN || (NG == 0 && !TMAC), "chain mode: unit mode with STG write-back only");
+    const TableOf<NENT, NG>& et = *reinterpret_cast<const TableOf<NENT, NG>*>(p.table);
     extern __shared__ __align__(1024) uint8_t smem[];
     const uint32_t warp = threadIdx.x >> 5;
     const uint32_t lane = threadIdx.x & 31;
@@ -332,35 +334,29 @@ __global__ void __launch_bounds__(TMAC ? NTHREADS_TMA : NTHREADS, 1)
 
     // ---------------------------------------------------------------- consumers
     const uint32_t tid = threadIdx.x;
-    // Unit mode: copy the entry table (off | sc | dc, the n_ent entries in use) and the cluster
-    // descriptors from the kernel parameters into shared memory once.  A component switch then
-    // reads its lanes' entries with LDS; from the parameters every lane-divergent index is a
-    // serialised constant-bank load (7 per entry: ~50 us for C3's 24 components at small N).
-    // The copy overlaps the producer's first TMA loads.
-    // Byte-group mode: the ByteGroups in use (13 words each) and the cluster descriptors, likewise.
-    // 128-bit loads: a lane-divergent constant load costs one access per distinct address, so
-    // 16 bytes per access instead of 4 (the tables and descriptors are 16-byte aligned).
-    // A one-component unit-mode plan switches component once per CTA: its lanes read their entries
-    // straight from the parameters then, and only the cluster descriptors are copied.
+    // Copy the plan's table into shared memory once per CTA -- unit mode: the entry table
+    // (off | sc | dc, the n_ent entries in use); byte-group mode: the ByteGroups in use (13 words
+    // each) -- plus the cluster descriptors.  The table comes from its device copy with coalesced
+    // 16-byte loads (L2-resident after the first CTAs), overlapped with the producer's first TMA
+    // loads; a component switch then reads its lanes' entries with LDS.  (Read from the kernel
+    // parameters instead, every lane-divergent index was a serialised constant-bank access: C3's
+    // merged plan spent ~17 % of its 1-32 MB launches there, profiles/r02y_*.)
     uint32_t tbl = out0 + p.s_out * p.stage_bytes, scl, dcl, n4 = 0;
-    const bool stbl = NG > 0 || p.n_comp > 1;
     if constexpr (NG == 0) {
         n4 = (p.n_ent + 15) & ~15u;                    // <= NENT (a multiple of 16)
         scl = tbl + 6 * n4;
-        if (stbl) {
-            const uint4* offv = reinterpret_cast<const uint4*>(et.off);
-            const uint4* scv = reinterpret_cast<const uint4*>(et.sc);
-            const uint4* dcv = reinterpret_cast<const uint4*>(et.dc);
-            for (uint32_t i = tid; i < n4 / 4; i += NCONS * 32) sts128(tbl + 16 * i, offv[i]);
-            for (uint32_t i = tid; i < n4 / 16; i += NCONS * 32) {
-                sts128(tbl + 4 * n4 + 16 * i, scv[i]);
-                sts128(tbl + 5 * n4 + 16 * i, dcv[i]);
-            }
+        const uint4* offv = reinterpret_cast<const uint4*>(et.off);
+        const uint4* scv = reinterpret_cast<const uint4*>(et.sc);
+        const uint4* dcv = reinterpret_cast<const uint4*>(et.dc);
+        for (uint32_t i = tid; i < n4 / 4; i += NCONS * 32) sts128(tbl + 16 * i, ldg_nc128(offv + i));
+        for (uint32_t i = tid; i < n4 / 16; i += NCONS * 32) {
+            sts128(tbl + 4 * n4 + 16 * i, ldg_nc128(scv + i));
+            sts128(tbl + 5 * n4 + 16 * i, ldg_nc128(dcv + i));
         }
     } else {
         const uint32_t gbytes = ((uint32_t)sizeof(ByteGroup) * p.n_ent + 15) & ~15u;   // <= sizeof(et.g)
         const uint4* gv = reinterpret_cast<const uint4*>(et.g);
-        for (uint32_t i = tid; i < gbytes / 16; i += NCONS * 32) sts128(tbl + 16 * i, gv[i]);
+        for (uint32_t i = tid; i < gbytes / 16; i += NCONS * 32) sts128(tbl + 16 * i, ldg_nc128(gv + i));
         scl = tbl + gbytes;
     }
     dcl = scl + 16 * p.n_srcc;
@@ -555,9 +551,9 @@ __global__ void __launch_bounds__(TMAC ? NTHREADS_TMA : NTHREADS, 1)
                 ioff[e] = ooff[e] = din[e] = dout[e] = 0;
                 if ((uint32_t)e < ne) {
                     const uint32_t idx = (p.comp[k].instr_base + warp + NCONS * e) * 32 + lane;
-                    const uint32_t v = stbl ? lds<uint32_t>(tbl + 4 * idx) : et.off[idx];
-                    const uint32_t sc = stbl ? (uint32_t)lds<uint8_t>(tbl + 4 * n4 + idx) : (uint32_t)et.sc[idx];
-                    const uint32_t dc = stbl ? (uint32_t)lds<uint8_t>(tbl + 5 * n4 + idx) : (uint32_t)et.dc[idx];
+                    const uint32_t v = lds<uint32_t>(tbl + 4 * idx);
+                    const uint32_t sc = (uint32_t)lds<uint8_t>(tbl + 4 * n4 + idx);
+                    const uint32_t dc = (uint32_t)lds<uint8_t>(tbl + 5 * n4 + idx);
                     const uint32_t s_stride = lds<uint32_t>(scl + 16 * sc + 8), s_smem = lds<uint32_t>(scl + 16 * sc + 12);
                     const uint32_t d_stride = lds<uint32_t>(dcl + 16 * dc + 8), d_smem = lds<uint32_t>(dcl + 16 * dc + 12);
                     ioff[e] = s_smem + (v & 0xFFFFu) * (uint32_t)sizeof(U);
@@ -711,6 +707,18 @@ __global__ void __launch_bounds__(TMAC ? NTHREADS_TMA : NTHREADS, 1)
         atomicAdd(&g_phase[7], (unsigned long long)ph[4]);
     });
 
+}
+
+// Upload of a plan table inside a captured stream (remap.cu device_table): the image travels as
+// this kernel's parameter and is stored to its device copy.
+struct TableUpload {
+    uint4 w[1600];        // 25 600 bytes >= the largest EntryTable / GroupTable image
+    uint64_t dst;
+    uint32_t n16, pad;
+};
+__global__ void table_upload_kernel(const __grid_constant__ TableUpload u) {
+    uint4* d = reinterpret_cast<uint4*>(u.dst);
+    for (uint32_t i = threadIdx.x; i < u.n16; i += blockDim.x) d[i] = u.w[i];
 }
 
 constexpr int ZMAX = 128;

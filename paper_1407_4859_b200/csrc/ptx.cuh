@@ -137,6 +137,12 @@ __device__ __forceinline__ void stg128_hint(void* p, uint4 v, uint64_t policy) {
                  "r"(v.w), "l"(policy)
                  : "memory");
 }
+// read-only global data (plan tables): 16-byte non-coherent load
+__device__ __forceinline__ uint4 ldg_nc128(const uint4* p) {
+    uint4 v;
+    asm volatile("ld.global.nc.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    return v;
+}
 __device__ __forceinline__ void sts(uint32_t a, uint32_t v) {
     asm volatile("st.shared.b32 [%0], %1;" ::"r"(a), "r"(v));
 }

@@ -41,23 +41,20 @@ namespace adha {
 
 using namespace dev;
 
-static_assert(sizeof(dev::TiledParams) + sizeof(dev::EntryTable<dev::CLASS_NENT[3]>) <= 32764,
-              "tiled kernel parameters exceed the 32764-byte kernel parameter limit");
-static_assert(sizeof(dev::TiledParams) + sizeof(dev::GroupTable<dev::GCLASS_NG[1]>) <= 32764,
-              "byte-group kernel parameters exceed the 32764-byte kernel parameter limit");
+static_assert(sizeof(dev::TiledParams) <= 32764, "tiled kernel parameters exceed the 32764-byte limit");
+static_assert(sizeof(dev::EntryTable<dev::CLASS_NENT[3]>) <= sizeof(dev::TableUpload::w) &&
+                  sizeof(dev::GroupTable<dev::GCLASS_NG[1]>) <= sizeof(dev::TableUpload::w),
+              "a table image must fit one upload kernel's parameters");
 static_assert(sizeof(dev::ByteGroup) == 52, "ByteGroup layout");
 static_assert(sizeof(dev::NaiveParams) <= 32764, "naive kernel parameters too large");
 
 namespace detail {
 
-typedef void (*TiledLauncher)(dim3, dim3, size_t, cudaStream_t, const TiledParams&, const void* table);
+typedef void (*TiledLauncher)(dim3, dim3, size_t, cudaStream_t, const TiledParams&);
 
 template <typename U, int CLS, bool TMAC>
-void launch_tiled(dim3 grid, dim3 block, size_t smem, cudaStream_t st, const TiledParams& p, const void* table) {
-    constexpr int NENT = CLASS_NENT[CLS];
-    constexpr int EMAX = CLASS_EMAX[CLS];
-    remap_tiled_kernel<U, NENT, EMAX, 0, 1, TMAC><<<grid, block, smem, st>>>(
-        p, *static_cast<const EntryTable<NENT>*>(table));
+void launch_tiled(dim3 grid, dim3 block, size_t smem, cudaStream_t st, const TiledParams& p) {
+    remap_tiled_kernel<U, CLASS_NENT[CLS], CLASS_EMAX[CLS], 0, 1, TMAC><<<grid, block, smem, st>>>(p);
 }
 
 template <typename U, int CLS, bool TMAC>
@@ -69,11 +66,8 @@ const void* tiled_fn() {
 
 // fused-chain instantiations (classes 0..2; chain_tiled never picks the largest class)
 template <typename U, int CLS>
-void launch_chain(dim3 grid, dim3 block, size_t smem, cudaStream_t st, const TiledParams& p, const void* table) {
-    constexpr int NENT = CLASS_NENT[CLS];
-    constexpr int EMAX = CLASS_EMAX[CLS];
-    remap_tiled_kernel<U, NENT, EMAX, 0, 1, false, true><<<grid, block, smem, st>>>(
-        p, *static_cast<const EntryTable<NENT>*>(table));
+void launch_chain(dim3 grid, dim3 block, size_t smem, cudaStream_t st, const TiledParams& p) {
+    remap_tiled_kernel<U, CLASS_NENT[CLS], CLASS_EMAX[CLS], 0, 1, false, true><<<grid, block, smem, st>>>(p);
 }
 template <typename U, int CLS>
 const void* chain_fn() {
@@ -104,11 +98,8 @@ TiledLauncher pick_cls(int cls, const void** fn) {
 }
 
 template <int GC, bool TMAC>
-void launch_groups(dim3 grid, dim3 block, size_t smem, cudaStream_t st, const TiledParams& p, const void* table) {
-    constexpr int NG = GCLASS_NG[GC];
-    constexpr int GMAX = GCLASS_GMAX[GC];
-    remap_tiled_kernel<uint8_t, 32, 1, NG, GMAX, TMAC><<<grid, block, smem, st>>>(
-        p, *static_cast<const GroupTable<NG>*>(table));
+void launch_groups(dim3 grid, dim3 block, size_t smem, cudaStream_t st, const TiledParams& p) {
+    remap_tiled_kernel<uint8_t, 32, 1, GCLASS_NG[GC], GCLASS_GMAX[GC], TMAC><<<grid, block, smem, st>>>(p);
 }
 template <int GC, bool TMAC>
 const void* groups_fn() {
@@ -162,6 +153,82 @@ std::shared_ptr<const RemapPlan> get_plan(const Layout& ls, const Layout& ld, bo
 
 adha_status cuda_fail(cudaError_t e, const char* what) {
     return fail(ADHA_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// Device copies of the plan tables (EntryTable / GroupTable images, <= 25 KB each).  The tiled
+// kernel copies its table from here into shared memory with coalesced 16-byte loads; passing it
+// in the kernel parameters instead cost a larger launch (~30 KB of parameters: +2.5 us) and
+// serialised lane-divergent constant-bank loads.  A table is uploaded once per (key, device):
+// synchronously on an internal stream at its first use, or -- when the caller's stream is being
+// captured into a CUDA graph -- by a small kernel in the captured stream itself (the graph then
+// re-uploads on every replay; the copy is not marked resident, so the next uncaptured call
+// uploads it for good).  Memory comes from 4 MB chunks per device that live as long as the
+// process (a table is never freed: in-flight kernels may still read it).
+struct TableStore {
+    std::mutex mu;
+    struct Entry { const void* dptr; bool ready; };
+    std::map<std::pair<std::string, int>, Entry> tables;
+    struct Chunk { uint8_t* base; size_t used, size; };
+    std::map<int, Chunk> chunk;
+    std::map<int, cudaStream_t> upload_stream;
+};
+TableStore& tables() {
+    static TableStore t;
+    return t;
+}
+
+adha_status device_table(const std::string& key, const std::vector<uint32_t>& img, cudaStream_t st,
+                         uint64_t* out) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    TableStore& T = tables();
+    std::lock_guard<std::mutex> g(T.mu);
+    auto it = T.tables.find({key, dev});
+    if (it != T.tables.end() && it->second.ready) {
+        *out = (uint64_t)(uintptr_t)it->second.dptr;
+        return ADHA_OK;
+    }
+    const size_t bytes = (img.size() * 4 + 15) / 16 * 16;
+    if (bytes > sizeof(TableUpload::w)) return fail(ADHA_ERR_UNSUPPORTED, "plan table too large");
+    const void* dptr = nullptr;
+    if (it != T.tables.end()) {
+        dptr = it->second.dptr;
+    } else {
+        TableStore::Chunk& C = T.chunk[dev];
+        if (!C.base || C.used + bytes > C.size) {
+            void* m = nullptr;
+            e = cudaMalloc(&m, 4u << 20);
+            if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc (plan tables)");
+            C = {static_cast<uint8_t*>(m), 0, 4u << 20};
+        }
+        dptr = C.base + C.used;
+        C.used += (bytes + 255) / 256 * 256;
+        it = T.tables.emplace(std::make_pair(key, dev), TableStore::Entry{dptr, false}).first;
+    }
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    e = cudaStreamIsCapturing(st, &cs);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamIsCapturing");
+    if (cs != cudaStreamCaptureStatusNone) {
+        auto U = std::make_unique<TableUpload>();
+        std::memset(U.get(), 0, sizeof(TableUpload));
+        std::memcpy(U->w, img.data(), img.size() * 4);
+        U->dst = (uint64_t)(uintptr_t)dptr;
+        U->n16 = (uint32_t)(bytes / 16);
+        table_upload_kernel<<<1, 256, 0, st>>>(*U);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return cuda_fail(e, "table_upload_kernel launch");
+    } else {
+        cudaStream_t& us = T.upload_stream[dev];
+        if (!us && (e = cudaStreamCreateWithFlags(&us, cudaStreamNonBlocking)) != cudaSuccess)
+            return cuda_fail(e, "cudaStreamCreateWithFlags");
+        e = cudaMemcpyAsync(const_cast<void*>(dptr), img.data(), img.size() * 4, cudaMemcpyHostToDevice, us);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(us);
+        if (e != cudaSuccess) return cuda_fail(e, "plan table upload");
+        it->second.ready = true;
+    }
+    *out = (uint64_t)(uintptr_t)dptr;
+    return ADHA_OK;
 }
 
 // per-device setup: SM count and the kernel's dynamic shared memory opt-in
@@ -274,20 +341,19 @@ uint64_t small_bytes() {
 }
 
 // Payload up to which a remap takes the direct kernel instead of the tiled one.  The tiled kernel
-// has a fixed cost per launch (pipeline fill, per-component setup: 5-8 us for one component,
-// ~12 us for 7, ~50 us for C3's 24 components, 20-30 us in 2-byte byte-group mode; CUDA-graph
-// replay, tools/small_path_probe.py, profiles/r01k_small_path.log) while the direct kernel
-// streams at ~1 TB/s for 4-byte units and ~0.3-0.5 TB/s for 1-/2-byte units after ~2 us.
-// Crossovers measured on B200: 4-8 MB (one component, 4-byte units), 8-16 MB (>= 4
-// components or 2-byte units), > 32 MB (24 components), 1-4 MB (1-byte units).
-// ADHA_SMALL_BYTES, when set, overrides this (tests force either path with it).
+// has a fixed cost per launch (parameters, pipeline fill, table copy, tails: 5-7 us for one
+// component, 6 us for Medical's 7 on the merged plan, 12-19 us for C3's 24; CUDA-graph replay,
+// tools/small_path_probe.py, profiles/r02z_small_path.log) while the direct kernel streams at
+// ~1 TB/s for 4-byte units and ~0.3-0.5 TB/s for 1-/2-byte units after ~2 us.  Crossovers
+// measured on B200: 4-8 MB (4-byte units, any component count below 16), 1-4 MB (1- and 2-byte
+// units), 16-32 MB (C3's 24 components).  ADHA_SMALL_BYTES, when set, overrides this (tests
+// force either path with it).
 uint64_t direct_bytes(const RemapPlan& p) {
     const char* e = std::getenv("ADHA_SMALL_BYTES");
     if (e && *e) return (uint64_t)std::strtoull(e, nullptr, 10);
     const size_t k = p.comps.size();
-    if (p.unit == 1) return 2ull << 20;
-    if (k >= 16) return 32ull << 20;
-    if (k >= 4 || p.unit == 2) return 8ull << 20;
+    if (p.unit < 4) return 2ull << 20;
+    if (k >= 16) return 16ull << 20;
     return 4ull << 20;
 }
 
@@ -453,10 +519,12 @@ adha_status remap_checked(const uint8_t* src, const Layout& ls, uint8_t* dst, co
     const int threads = P->tma_copy ? NTHREADS_TMA : NTHREADS;
     s = device_setup(fn, &n_sm, threads);
     if (s != ADHA_OK) return s;
+    s = device_table("p" + std::to_string(plan->uid), plan->table, st, &P->table);
+    if (s != ADHA_OK) return s;
     // a tail-only call still needs one CTA per component tail
     const int64_t grid = std::max<int64_t>(std::min<int64_t>((int64_t)plan->comps.size(), n_sm),
                                            std::min<int64_t>(tiles, n_sm));
-    launch(dim3((unsigned)std::max<int64_t>(grid, 1)), dim3(threads), plan->smem_bytes, st, *P, plan->table.data());
+    launch(dim3((unsigned)std::max<int64_t>(grid, 1)), dim3(threads), plan->smem_bytes, st, *P);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "remap_tiled_kernel launch");
     return ADHA_OK;
@@ -754,8 +822,13 @@ adha_status chain_tiled(void* const* buffers, const adha_layout* const* layouts,
     TiledLauncher run = pick_chain(unit, cls, &fn);
     s = device_setup(fn, &n_sm, NTHREADS);
     if (s != ADHA_OK) return s;
+    // the chain's table depends only on its hops' plans (and the class)
+    std::string key = "c" + std::to_string(cls);
+    for (const auto& pl : plans) key += "." + std::to_string(pl->uid);
+    s = device_table(key, table, st, &P->table);
+    if (s != ADHA_OK) return s;
     const int64_t grid = std::min<int64_t>(bands, n_sm);
-    run(dim3((unsigned)grid), dim3(NTHREADS), smem, st, *P, table.data());
+    run(dim3((unsigned)grid), dim3(NTHREADS), smem, st, *P);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "remap_tiled_kernel (chain) launch");
     return ADHA_OK;

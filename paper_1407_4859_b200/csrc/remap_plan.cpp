@@ -12,6 +12,7 @@
 #include <climits>
 #include <cstdio>
 #include <cstring>
+#include <atomic>
 #include <map>
 #include <numeric>
 #include <string>
@@ -162,7 +163,9 @@ uint32_t call_tile(const RemapPlan& p, int k, int64_t n, int n_sm) {
 }
 
 RemapPlan compile_plan(const Layout& ls, const Layout& ld, bool merge) {
+    static std::atomic<uint64_t> next_uid{1};
     RemapPlan P;
+    P.uid = next_uid++;
     P.merged = merge;
     const int F = ls.n_fields;
     const int Cs = ls.n_clusters(), Cd = ld.n_clusters();

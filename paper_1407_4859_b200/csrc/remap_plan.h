@@ -102,6 +102,8 @@ struct TiledParams {
                           // every component has the same T and n_tiles (bands); regions are absolute
     uint32_t chain_group; // chain: bands per group (1..8), each group run hop by hop
     uint32_t chain_hints; // chain: 1 = loads evict_first, intermediates stored evict_last, the last hop evict_first
+    uint64_t table;       // device address of the plan's table image (EntryTable<NENT> / GroupTable<NG>),
+                          // uploaded once per plan and device (remap.cu device_table)
     CompDesc comp[MAXK];
     ClusterDesc srcc[MAXC];
     ClusterDesc dstc[MAXC];
@@ -183,6 +185,7 @@ struct RemapPlan {
         uint32_t instr_base = 0, n_instr = 0;
         uint32_t n_groups = 0;        // byte-group mode: groups of one period
     };
+    uint64_t uid = 0;                 // process-unique plan id (key of its device table copies)
     bool tiled = false;
     bool merged = false;              // compiled with every cluster in one component
     std::string why_naive;            // reason when not tiled
@@ -201,7 +204,8 @@ struct RemapPlan {
     std::vector<int> src_slot, dst_slot;     // canonical cluster -> kernel cluster index
     std::vector<uint32_t> ent_off;           // 32 * sum(W_k) entries (local offsets)
     std::vector<uint8_t> ent_sc, ent_dc;     // kernel cluster indices
-    std::vector<uint32_t> table;             // EntryTable<CLASS_NENT[table_class]> image (fields filled)
+    std::vector<uint32_t> table;             // EntryTable<CLASS_NENT[table_class]> / GroupTable image (fields
+                                             // filled); the kernels read a device copy of it
 };
 
 struct Layout;

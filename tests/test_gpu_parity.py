@@ -188,6 +188,37 @@ def test_side_stream():
     assert np.array_equal(d_dst.cpu().numpy(), oracle_dst(src, [0] * 16, list(range(16)), widths, n))
 
 
+@pytest.mark.parametrize("widths,ls,ld", [(config_widths(16), [0] * 16, list(range(16))),
+                                           ([2, 4, 6, 4] * 4, [0] * 16, list(range(16))),
+                                           (config_widths(64), list(range(64)), [i // 8 for i in range(64)])],
+                         ids=["unit4", "byte-groups", "many-regions"])
+def test_first_use_inside_cuda_graph_capture(widths, ls, ld, monkeypatch):
+    """A layout pair's first tiled remap issued while the stream is being captured into a CUDA
+    graph: its plan table is uploaded by a kernel inside the graph (remap.cu device_table), so
+    every replay is correct; a later uncaptured call uploads it for good."""
+    monkeypatch.setenv("ADHA_SMALL_BYTES", "0")
+    n = 40_003
+    cols = field_columns(7, n, widths)
+    src = O.pack(cols, widths, ls, n, fill=0x3C)
+    exp = oracle_dst(src, ls, ld, widths, n)
+    Ls, Ld = A.Layout(widths, ls), A.Layout(widths, ld)          # fresh handles: a new plan
+    d_src = to_dev(src)
+    d_dst = sentinel_dev(Ld.nbytes(n))
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        A.remap(d_src, Ls, d_dst, Ld, n)
+    for _ in range(2):
+        d_dst.fill_(SENT)
+        g.replay()
+        torch.cuda.synchronize()
+        assert np.array_equal(d_dst.cpu().numpy(), exp)
+    d_dst.fill_(SENT)
+    A.remap(d_src, Ls, d_dst, Ld, n)
+    torch.cuda.synchronize()
+    assert np.array_equal(d_dst.cpu().numpy(), exp)
+
+
 # ----------------------------------------------------------------------------- full BASELINE sizes
 
 def test_c2_full_size_every_byte():
