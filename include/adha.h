@@ -182,9 +182,9 @@ ADHA_API void adha_layout_destroy(adha_layout* layout);
  * Asynchronous: the call enqueues one kernel launch on `stream` and returns.
  * The per-call plan travels as kernel parameters; the first tiled remap of a
  * layout pair on a device uploads the plan's permutation table (<= 25 KB) into
- * library-owned device memory (4 MB chunks per device, kept for the process
- * lifetime) with a copy that the call waits for -- or, inside CUDA-graph
- * capture, with a kernel in the captured stream.
+ * library-owned device memory (a static 4 MB arena per device, then 4 MB
+ * chunks, kept for the process lifetime) with a copy that the call waits for
+ * -- or, inside CUDA-graph capture, with a kernel in the captured stream.
  * Launch errors return ADHA_ERR_CUDA; faults during execution surface at the
  * caller's next synchronisation.
  * Errors: INVALID_ARG, LAYOUT_MISMATCH, ALIGNMENT, OVERLAP, TOO_LARGE, CUDA. */

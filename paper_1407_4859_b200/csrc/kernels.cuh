@@ -169,6 +169,47 @@ __device__ __forceinline__ void tile_next(const TiledParams& p, uint32_t H, Tile
     }
 }
 
+// Consumer-side loader (TiledParams::cpa): warp w of the consumers copies bytes [w*B/8, (w+1)*B/8)
+// of tile (k, lt)'s packed src chunks (B = tile_bytes) into input stage `sb` with 16-byte cp.async,
+// 512 contiguous bytes per warp instruction, then arrives on the stage's `full` barrier when its
+// copies land.  Unlike TMA bulk copies, the cost does not grow with the number of src chunks
+// (64 SoA chunks of 512 B per tile: profiles/r02aa_pieces.log).  (c0, b0) cache this warp's first
+// chunk and its packed begin for component ak.
+struct CpaState {
+    int ak;
+    uint32_t c0, b0;
+};
+__device__ __forceinline__ void cpa_issue(const TiledParams& p, uint32_t scl, uint32_t k, int64_t lt, uint32_t sb,
+                                          uint32_t full, uint32_t warp, uint32_t lane, CpaState& cs) {
+    const CompDesc& K = p.comp[k];
+    const uint32_t TV = K.tile_bytes >> 4;
+    const uint32_t w0 = (warp * TV / NCONS) << 4, w1 = ((warp + 1) * TV / NCONS) << 4;
+    if ((int)k != cs.ak) {
+        cs.ak = (int)k;
+        uint32_t c = K.sc_lo, b = 0;
+        for (;;) {
+            const uint32_t e = b + K.T * lds<uint32_t>(scl + 16 * c + 8);
+            if (e > w0 || c + 1 >= K.sc_hi) break;
+            b = e;
+            ++c;
+        }
+        cs.c0 = c;
+        cs.b0 = b;
+    }
+    uint32_t c = cs.c0, b = cs.b0;
+    while (b < w1 && c < K.sc_hi) {
+        const uint4 d = lds128(scl + 16 * c);             // region lo, region hi, stride, smem
+        const uint32_t bytes = K.T * d.z, e = b + bytes;
+        const uint32_t lo = max(b, w0), hi = min(e, w1);
+        const uint8_t* g = (const uint8_t*)(p.src + ((uint64_t)d.x | ((uint64_t)d.y << 32)) + (uint64_t)lt * bytes) - b;
+        const uint32_t sm = sb + d.w - b;
+        for (uint32_t o = lo + lane * 16; o < hi; o += 32 * 16) cp_async16(sm + o, g + o);
+        b = e;
+        ++c;
+    }
+    cp_async_mbar_arrive_noinc(full);
+}
+
 // 9 warps per CTA: the register file is split over the 4 SM sub-partitions (16K registers
 // each) and one of them holds 3 warps, so a thread may use at most 16384 / 96 = 168 registers;
 // __launch_bounds__(NTHREADS, 1) gives ptxas exactly that budget.
@@ -202,7 +243,7 @@ __global__ void __launch_bounds__(TMAC ? NTHREADS_TMA : NTHREADS, 1)
     const uint32_t stored0 = oempty0 + 8 * S_OUT_MAX;  // 8 mbarriers (chain): tile i's stores are visible
     if (threadIdx.x == 0) {
         for (uint32_t s = 0; s < p.s_in; ++s) {
-            mbar_init(full0 + 8 * s, 1);
+            mbar_init(full0 + 8 * s, (!TMAC && !CHAIN && NG == 0 && p.cpa) ? NCONS * 32 : 1);
             mbar_init(empty0 + 8 * s, NCONS);
         }
         for (uint32_t o = 0; o < S_OUT_MAX; ++o) {
@@ -253,6 +294,7 @@ __global__ void __launch_bounds__(TMAC ? NTHREADS_TMA : NTHREADS, 1)
     }
 
     if (warp == NCONS) {
+        if (!TMAC && !CHAIN && NG == 0 && p.cpa) return;   // the consumers load the tiles (cpa_issue)
         // ------------------------------------------------------------ TMA producer
         // Per component, every lane holds up to PMAX bulk-load pieces of the tile (src chunks cut
         // into pieces of at most `split` bytes): smem offset, global offset of tile 0, bytes, and
@@ -461,6 +503,20 @@ __global__ void __launch_bounds__(TMAC ? NTHREADS_TMA : NTHREADS, 1)
     TileIter it;
     tile_begin(p, H, it);
     bool stored_pending = false;     // chain: tile i-1's stores not yet fenced and signalled
+    // consumer-side loads (p.cpa): the first s_in tiles are issued up front; tile i+s_in goes into
+    // tile i's stage as soon as every warp has passed tile i's output barrier (its permutation
+    // done), before tile i's copy-out -- as early as the TMA producer would issue it.  (Never with
+    // the TMA write-back, which has no such barrier.)
+    const bool cpa = !TMAC && !CHAIN && NG == 0 && p.cpa;   // (unit mode: byte groups would spill)
+    TileIter ahead;
+    CpaState cst{-1, 0u, 0u};
+    int64_t ai = 0;
+    if (cpa) {
+        tile_begin(p, 0, ahead);
+        for (; ai < (int64_t)p.s_in && ai < nt; ++ai, tile_next(p, 0, ahead))
+            cpa_issue(p, scl, ahead.k, ahead.lt, in0 + (uint32_t)ai * p.stage_bytes, full0 + 8 * (uint32_t)ai, warp,
+                      lane, cst);
+    }
     for (int64_t i = 0; i < nt; ++i, tile_next(p, H, it)) {
         k = it.k;
         const int64_t lt = it.lt;
@@ -679,6 +735,11 @@ __global__ void __launch_bounds__(TMAC ? NTHREADS_TMA : NTHREADS, 1)
                 ++i_t;
             } else {
                 named_bar_sync(1, NCONS * 32);                  // output tile complete
+                if (cpa && ai < nt) {                           // this tile's input stage is free
+                    cpa_issue(p, scl, ahead.k, ahead.lt, ib, full0 + 8 * stage, warp, lane, cst);
+                    ++ai;
+                    tile_next(p, 0, ahead);
+                }
                 ADHA_PT(const long long c3 = clock64(); ph[2] += c3 - c2);
                 if (H && p.chain_hints)
                     copy_out<true>((uint8_t*)p.dst, ob, tid, lt, nv, gofs, gstep, k + 1 < H ? kpol : spol);

@@ -162,8 +162,11 @@ adha_status cuda_fail(cudaError_t e, const char* what) {
 // synchronously on an internal stream at its first use, or -- when the caller's stream is being
 // captured into a CUDA graph -- by a small kernel in the captured stream itself (the graph then
 // re-uploads on every replay; the copy is not marked resident, so the next uncaptured call
-// uploads it for good).  Memory comes from 4 MB chunks per device that live as long as the
-// process (a table is never freed: in-flight kernels may still read it).
+// uploads it for good).  Memory: a 4 MB static __device__ arena per device, then 4 MB cudaMalloc
+// chunks; all live as long as the process (a table is never freed: in-flight kernels may still
+// read it).
+__device__ __align__(256) uint8_t g_plan_tables[4u << 20];   // ~160 plan tables per device
+
 struct TableStore {
     std::mutex mu;
     struct Entry { const void* dptr; bool ready; };
@@ -196,7 +199,15 @@ adha_status device_table(const std::string& key, const std::vector<uint32_t>& im
         dptr = it->second.dptr;
     } else {
         TableStore::Chunk& C = T.chunk[dev];
-        if (!C.base || C.used + bytes > C.size) {
+        if (!C.base) {
+            // the first chunk is the module's static arena: no allocation, so a first call
+            // inside CUDA-graph capture works too
+            void* a = nullptr;
+            e = cudaGetSymbolAddress(&a, g_plan_tables);
+            if (e != cudaSuccess) return cuda_fail(e, "cudaGetSymbolAddress (plan tables)");
+            C = {static_cast<uint8_t*>(a), 0, sizeof(g_plan_tables)};
+        }
+        if (C.used + bytes > C.size) {
             void* m = nullptr;
             e = cudaMalloc(&m, 4u << 20);
             if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc (plan tables)");
@@ -512,6 +523,28 @@ adha_status remap_checked(const uint8_t* src, const Layout& ls, uint8_t* dst, co
             }
         }
         P->tma_copy = tma ? 1u : 0u;
+    }
+    // Loader: the producer warp's TMA bulk copies, or (cpa) the consumers' own cp.async, issued
+    // for tile i+s_in right after tile i's output barrier.  Each TMA bulk copy has a fixed cost in
+    // the SM's TMA unit, so a tile of >= 32 small src chunks arrives slowly (64 SoA chunks of 640 B:
+    // 3.98 vs 6.34 TB/s for one chunk, profiles/r02aa_pieces.log); cp.async does not care about the
+    // chunk count but puts the load issue on the consumers, which bind at large N (C5 6 361 vs
+    // 6 556 GB/s, profiles/r02ac_loader.log).  So cpa only for >= 32 src chunks per tile up to 24 MB:
+    // K-Means SoA->AoS 8 MB 13.2 -> 11.9 us, C3 SoA->hybrid 1 MB 18.8 -> 13.0 us (tiled;
+    // r02ac_small_path_cpa.log).  ADHA_LOADER = tma | cpa overrides.
+    {
+        const char* ld_env = std::getenv("ADHA_LOADER");
+        bool cpa = (uint64_t)n * ls.record_bytes <= (24ull << 20);
+        bool any = false;
+        for (size_t k = 0; k < plan->comps.size(); ++k) {
+            if (P->comp[k].n_tiles == 0) continue;
+            any = true;
+            if (plan->comps[k].src_clusters.size() < 32) cpa = false;
+        }
+        cpa = cpa && any;
+        if (ld_env && std::strcmp(ld_env, "cpa") == 0) cpa = true;
+        if (ld_env && std::strcmp(ld_env, "tma") == 0) cpa = false;
+        P->cpa = (cpa && !P->tma_copy && !plan->byte_groups) ? 1u : 0u;
     }
     const void* fn = nullptr;
     TiledLauncher launch = plan->byte_groups ? pick_groups(plan->group_class, P->tma_copy != 0, &fn)

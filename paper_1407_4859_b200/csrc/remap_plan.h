@@ -102,6 +102,9 @@ struct TiledParams {
                           // every component has the same T and n_tiles (bands); regions are absolute
     uint32_t chain_group; // chain: bands per group (1..8), each group run hop by hop
     uint32_t chain_hints; // chain: 1 = loads evict_first, intermediates stored evict_last, the last hop evict_first
+    uint32_t cpa;         // 1: the consumer warps load the tiles themselves with cp.async (16 B per lane,
+                          // S-1 tiles ahead) instead of the producer warp's TMA bulk copies (plain STG
+                          // instantiations only: needs the per-tile barrier after the permutation)
     uint64_t table;       // device address of the plan's table image (EntryTable<NENT> / GroupTable<NG>),
                           // uploaded once per plan and device (remap.cu device_table)
     CompDesc comp[MAXK];

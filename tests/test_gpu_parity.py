@@ -821,3 +821,32 @@ def test_write_back_modes(mode, monkeypatch):
     ]
     for w, ls, bs, als, ld, bd, ald, n in cases:
         check_pair_ex(w, ls, bs, als, ld, bd, ald, n, seed=n % 97)
+
+
+@pytest.mark.parametrize("loader", ["tma", "cpa"])
+@pytest.mark.parametrize("merge", ["merged", "components"])
+def test_loaders(loader, merge, monkeypatch):
+    """Both tile loaders of the tiled kernel are bit-exact: the producer warp's TMA bulk copies and
+    the consumers' cp.async (remap.cu: auto for >= 32 src chunks per tile up to 24 MB), forced
+    either way, on the merged one-component plan and on per-component plans (the cp.async
+    look-ahead then crosses component boundaries), with padded / AoSoA dst and ragged N --
+    including N below s_in tiles per CTA and CTAs without tiles."""
+    monkeypatch.setenv("ADHA_LOADER", loader)
+    monkeypatch.setenv("ADHA_SMALL_BYTES", "0")
+    if merge == "components":
+        monkeypatch.setenv("ADHA_MERGE_BYTES", "0")
+    else:
+        monkeypatch.delenv("ADHA_MERGE_BYTES", raising=False)
+    w64 = config_widths(64)
+    cases = [
+        (w64, list(range(64)), None, False, c3_labels(), None, False, 100_003),
+        (w64, list(range(64)), None, False, c3_labels(), None, False, 4_111),
+        ([4] * 32, list(range(32)), None, False, [0] * 32, None, False, 200_003),
+        (config_widths(16), [0] * 16, None, False, list(range(16)), None, False, 70_001),
+        ([4] * 9, [0, 0, 0, 1, 2, 3, 4, 5, 6], None, False, list(range(9)), None, False, 300_007),
+        ([4] * 9, [0, 0, 0, 1, 2, 3, 4, 5, 6], None, False, list(range(9)), None, False, 33),
+        ([4, 8, 4, 4, 8], list(range(5)), None, False, [0] * 5, None, True, 50_017),
+        ([4, 4, 8, 4], list(range(4)), None, False, [0] * 4, [8] * 4, False, 33_333),
+    ]
+    for w, ls, bs, als, ld, bd, ald, n in cases:
+        check_pair_ex(w, ls, bs, als, ld, bd, ald, n, seed=n % 89)

@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <functional>
+#include <string>
 #include <vector>
 
 #include "ptx.cuh"
@@ -238,6 +239,96 @@ __global__ void k_phased(const uint8_t* s, uint8_t* d, size_t bytes, uint32_t TB
     }
 }
 
+
+// Many-region tiles: a stage of TB bytes arrives as P bulk copies of TB/P bytes from P regions
+// (region j = [j*bytes/P, (j+1)*bytes/P), like an SoA src of P fields); warp 8's lanes issue the
+// copies, warps 0-7 write the stage back with LDS.128 -> STG.128 (contiguous dst).  Measures
+// what the per-copy cost of the TMA unit does to a tile of many small chunks.
+__global__ void __launch_bounds__(288, 1) k_pieces(const uint8_t* s, uint8_t* d, size_t bytes, uint32_t TB, uint32_t S,
+                                                   uint32_t P) {
+    extern __shared__ __align__(1024) uint8_t sm[];
+    const uint32_t base = (smem_u32(sm) + 127u) & ~127u;
+    const uint32_t full0 = base, empty0 = base + 8 * 16, buf0 = base + 256;
+    if (threadIdx.x == 0) {
+        for (uint32_t i = 0; i < S; ++i) {
+            mbar_init(full0 + 8 * i, 1);
+            mbar_init(empty0 + 8 * i, 8);
+        }
+        fence_mbarrier_init();
+    }
+    __syncthreads();
+    const uint32_t pb = TB / P;                 // bytes per piece (multiple of 16)
+    const size_t region = bytes / P;            // bytes per region
+    const size_t nt = region / pb;              // tiles
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint32_t st = 0, ph = 0;
+    if (warp == 8) {
+        for (size_t t = blockIdx.x; t < nt; t += gridDim.x) {
+            mbar_wait(empty0 + 8 * st, ph ^ 1);
+            if (lane == 0) mbar_arrive_expect_tx(full0 + 8 * st, pb * P);
+            __syncwarp();
+            for (uint32_t j = lane; j < P; j += 32)
+                bulk_load(buf0 + st * TB + j * pb, s + j * region + t * pb, pb, full0 + 8 * st);
+            if (++st == S) { st = 0; ph ^= 1; }
+        }
+        return;
+    }
+    for (size_t t = blockIdx.x; t < nt; t += gridDim.x) {
+        mbar_wait(full0 + 8 * st, ph);
+        const uint32_t b = buf0 + st * TB;
+        uint8_t* g = d + t * TB;
+        for (uint32_t v = threadIdx.x * 16; v < TB; v += 4 * 256 * 16) {
+            uint4 x[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (v + u * 4096 < TB) x[u] = lds128(b + v + u * 4096);
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (v + u * 4096 < TB) stg128(g + v + u * 4096, x[u]);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty0 + 8 * st);
+        if (++st == S) { st = 0; ph ^= 1; }
+    }
+}
+
+// The same tiles loaded by the consumer warps themselves with cp.async (LDGSTS, 16 B per lane):
+// tile i+S-1 is issued before tile i is written back, S-stage ring, cp.async.wait_group.
+__global__ void __launch_bounds__(256, 1) k_pieces_ldgsts(const uint8_t* s, uint8_t* d, size_t bytes, uint32_t TB,
+                                                          uint32_t S, uint32_t P) {
+    extern __shared__ __align__(1024) uint8_t sm[];
+    const uint32_t buf0 = (smem_u32(sm) + 127u) & ~127u;
+    const uint32_t pb = TB / P;
+    const size_t region = bytes / P;
+    const size_t nt = region / pb;
+    const uint32_t vpp = pb / 16;               // 16-byte vectors per piece
+    auto issue = [&](size_t t, uint32_t stg) {
+        if (t < nt)
+            for (uint32_t v = threadIdx.x; v < TB / 16; v += 256) {
+                const uint32_t j = v / vpp, o = (v - j * vpp) * 16;
+                const uint8_t* src = s + j * region + t * pb + o;
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(buf0 + stg * TB + j * pb + o), "l"(src)
+                             : "memory");
+            }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    size_t t = blockIdx.x;
+    for (uint32_t k = 0; k + 1 < S; ++k) issue(t + k * gridDim.x, k);
+    uint32_t st = 0;
+    for (; t < nt; t += gridDim.x) {
+        issue(t + (S - 1) * (size_t)gridDim.x, (st + S - 1) % S);
+        if (S == 2) asm volatile("cp.async.wait_group 1;" ::: "memory");
+        else asm volatile("cp.async.wait_group 2;" ::: "memory");
+        __syncthreads();
+        const uint32_t b = buf0 + st * TB;
+        uint8_t* g = d + t * TB;
+        for (uint32_t v = threadIdx.x * 16; v < TB; v += 256 * 16) stg128(g + v, lds128(b + v));
+        __syncthreads();
+        st = (st + 1) % S;
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
 static float time_it(cudaStream_t st, int reps, const std::function<void()>& f) {
     cudaEvent_t a, b;
     CK(cudaEventCreate(&a));
@@ -274,6 +365,28 @@ int main(int argc, char** argv) {
     auto rw = [&](float ms) { return 2.0 * bytes / (ms * 1e-3) / 1e9; };
     auto one = [&](float ms) { return 1.0 * bytes / (ms * 1e-3) / 1e9; };
     printf("bytes per buffer %zu, SMs %d\n", bytes, sms);
+    if (argc > 2 && std::string(argv[2]) == "pieces") {
+        for (uint32_t TB : {40960u, 32768u}) {
+            for (uint32_t S : {2u, 3u}) {
+                const size_t smb = 256 + 128 + (size_t)S * TB;
+                if (smb > 232448) continue;
+                CK(cudaFuncSetAttribute(k_pieces, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb));
+                CK(cudaFuncSetAttribute(k_pieces_ldgsts, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb));
+                for (uint32_t P : {1u, 8u, 16u, 32u, 64u, 80u}) {
+                    if (TB % (P * 16)) continue;
+                    float ms = time_it(st, reps, [&] { k_pieces<<<sms, 288, smb, st>>>(s, d, bytes, TB, S, P); });
+                    const size_t moved = (bytes / P / (TB / P)) * TB;
+                    printf("TMA %2u pieces of %5u B, tile %u KB x %u stages   %8.3f ms %7.0f GB/s\n", P, TB / P, TB >> 10, S, ms,
+                           2.0 * moved / (ms * 1e-3) / 1e9);
+                    ms = time_it(st, reps, [&] { k_pieces_ldgsts<<<sms, 256, smb, st>>>(s, d, bytes, TB, S, P); });
+                    printf("LDGSTS %2u pieces of %5u B, tile %u KB x %u stages %8.3f ms %7.0f GB/s\n", P, TB / P, TB >> 10, S, ms,
+                           2.0 * moved / (ms * 1e-3) / 1e9);
+                }
+            }
+        }
+        return 0;
+    }
+
 
     for (int pass = 0; pass < 2; ++pass) {
         printf("---- pass %d\n", pass);
