@@ -419,6 +419,8 @@ def run_inplace(args, rank, world, local, share):
                 "workspace_bytes_per_rank": sum(p.workspace_bytes for p in fwd + bwd),
                 "plans": [p.describe() for p in fwd],
                 "host_plan_ms": plan_ms,
+                "host_plans": len(fwd + bwd),
+                "host_plan_ms_per_plan": plan_ms / len(fwd + bwd),
                 "l2": "inputs larger than L2; no flush" if 2 * n * R > (252 << 20) else "inputs fit in L2 (latency-bound)",
                 "parallelism": f"shard by contiguous record range over {world} GPU(s), no data-path collective",
             },

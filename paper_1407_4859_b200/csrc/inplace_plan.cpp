@@ -6,6 +6,8 @@
 // with dst and src the same buffer.  This file computes, once per (Ls, Ld, N), which S-byte
 // slot goes where (a permutation of slot indices), its cycles, and the workspace layout.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -149,6 +151,26 @@ uint64_t add_cluster(const std::vector<IpBlock>& blocks, uint64_t stride, uint64
 
 constexpr uint32_t NONE_SLOT = 0xFFFFFFFFu;
 
+// ADHA_IP_TIMING=1: host time of the plan's phases on stderr (tools/inplace_probe.py)
+struct PhaseClock {
+    bool on;
+    std::chrono::steady_clock::time_point t;
+    PhaseClock() : on(std::getenv("ADHA_IP_TIMING") && *std::getenv("ADHA_IP_TIMING") == '1'), t(std::chrono::steady_clock::now()) {}
+    void lap(const char* what) {
+        if (!on) return;
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[ip plan] %-28s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(now - t).count());
+        t = now;
+    }
+};
+thread_local PhaseClock* g_pc = nullptr;
+struct PhaseScope {
+    PhaseClock pc;
+    PhaseScope() { g_pc = &pc; }
+    ~PhaseScope() { g_pc = nullptr; }
+};
+inline void lap(const char* what) { if (g_pc) g_pc->lap(what); }
+
 unsigned plan_threads(uint64_t work) {
     const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
     return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>({(uint64_t)hw, 32, work / (1u << 16)}));
@@ -181,27 +203,10 @@ inline bool is_cut(uint32_t x) {   // pseudo-random 1-in-512 cut points along th
 // to NONE_SLOT as they are placed by the cut walks.
 constexpr unsigned WALK_LANES = 16;
 
-void build_segments(uvector<uint32_t>& P, uint64_t nslot, unsigned nthr, InplacePlan* p) {
-    // cut points and fixed points, per thread chunk (concatenated in chunk order: cuts ascend)
-    std::vector<std::vector<uint32_t>> cut_parts(nthr);
-    std::vector<uint64_t> fixed_parts(nthr, 0);
-    parallel_for(nthr, nslot, [&](unsigned chunk, uint64_t x0, uint64_t x1) {
-        auto& cp = cut_parts[chunk];
-        uint64_t fx = 0;
-        for (uint64_t x = x0; x < x1; ++x) {
-            const uint32_t y = P[x];
-            if (y == NONE_SLOT) continue;
-            if (y == (uint32_t)x) { P[x] = NONE_SLOT; ++fx; continue; }
-            if (is_cut((uint32_t)x)) cp.push_back((uint32_t)x);
-        }
-        fixed_parts[chunk] = fx;
-    });
-    std::vector<uint32_t> cuts;
-    for (unsigned c = 0; c < nthr; ++c) {
-        cuts.insert(cuts.end(), cut_parts[c].begin(), cut_parts[c].end());
-        p->fixed_slots += fixed_parts[c];
-        std::vector<uint32_t>().swap(cut_parts[c]);
-    }
+// `cuts`: the cut points, ascending (content slots x with is_cut(x) that are not fixed points --
+// fixed points are NONE_SLOT in P already and counted in p->fixed_slots by the caller).
+void build_segments(uvector<uint32_t>& P, uint64_t nslot, unsigned nthr, InplacePlan* p,
+                    const std::vector<uint32_t>& cuts) {
     const uint64_t nc = cuts.size();
     // walk from every cut point up to (not including) the next cut point on its cycle
     struct Walked { uint32_t ci, len; uint64_t off; };        // cut index, length, offset in pos
@@ -245,6 +250,7 @@ void build_segments(uvector<uint32_t>& P, uint64_t nslot, unsigned nthr, Inplace
             }
         }
     });
+    lap("cut walks");
     // placement in cut order: seq offset and first segment of every walk (prefix sums)
     std::vector<uint64_t> seq_at(nc + 1, 0), seg_at(nc + 1, 0);
     for (uint64_t i = 0; i < nc; ++i) {
@@ -273,6 +279,7 @@ void build_segments(uvector<uint32_t>& P, uint64_t nslot, unsigned nthr, Inplace
         }
     });
     outs.clear();
+    lap("placement");
     p->cycles = 0;   // cut walks do not count cycles; the uncut ones below do
     // Cycles with no cut point (shorter ones): the slot with the smallest index leads its cycle.
     // Every thread tests the unplaced slots of its range -- a walk that meets a smaller index
@@ -311,6 +318,7 @@ void build_segments(uvector<uint32_t>& P, uint64_t nslot, unsigned nthr, Inplace
             ++p->cycles;
         }
     }
+    lap("uncut cycles");
     // (P is not consumed by the uncut pass; the caller drops it)
 }
 
@@ -338,6 +346,7 @@ std::string verify_segments(const uvector<uint32_t>& P0, const InplacePlan& p) {
 }  // namespace
 
 adha_status inplace_plan_build(const Layout& ls, const Layout& ld, int64_t n, InplacePlan* p) {
+    PhaseScope phase_scope;
     if (n < 0) return fail(ADHA_ERR_INVALID_ARG, "n_records < 0");
     if (ls.n_fields != ld.n_fields) return fail(ADHA_ERR_LAYOUT_MISMATCH, "layouts differ in field count");
     for (int32_t f = 0; f < ls.n_fields; ++f)
@@ -469,18 +478,36 @@ adha_status inplace_plan_build(const Layout& ls, const Layout& ld, int64_t n, In
     if (nslot >= 0xFFFFFFFFull) return fail(ADHA_ERR_TOO_LARGE, "in-place remap: more than 2^32 slots");
     constexpr uint32_t NONE = NONE_SLOT;
     uvector<uint32_t> P;
-    uvector<uint8_t> in_d;
     p->seq.clear();
     p->segs.clear();
     p->content_slots = p->moved_slots = p->fixed_slots = p->junk_slots = p->cycles = 0;
     if (m > 0) {
         const unsigned nthr = plan_threads(nslot);
-        P.resize(nslot);
-        in_d.resize(nslot);
+        P.resize(nslot);                          // uninitialised: every slot is written once below
+        // Body slot ranges: src cluster c's m tiles are slots [bs/S, bs/S + m*Ks) and dst cluster
+        // c's are [bd/S, bd/S + m*Kd).  The slot map below is a bijection from the src body slots
+        // onto the dst body slots (every dst body slot holds one run piece of one src tile), so a
+        // slot "receives content" iff it lies in a dst range -- no scattered marking pass needed.
+        struct Range { uint64_t lo, hi; };
+        std::vector<Range> src_r, dst_r;
+        for (int32_t c = 0; c < Cs; ++c) src_r.push_back({p->bs[c] / S, p->bs[c] / S + m * (ls.stride[c] / u)});
+        for (int32_t c = 0; c < Cd; ++c) dst_r.push_back({p->bd[c] / S, p->bd[c] / S + m * (ld.stride[c] / u)});
+        auto by_lo = [](const Range& a, const Range& b) { return a.lo < b.lo; };
+        std::sort(src_r.begin(), src_r.end(), by_lo);
+        std::sort(dst_r.begin(), dst_r.end(), by_lo);
+        // slots outside every src body range carry no content: NONE (gaps, the src tail)
         parallel_for(nthr, nslot, [&](unsigned, uint64_t x0, uint64_t x1) {
-            std::fill(P.begin() + x0, P.begin() + x1, NONE);
-            std::fill(in_d.begin() + x0, in_d.begin() + x1, (uint8_t)0);
+            uint64_t x = x0;
+            for (const Range& r : src_r) {
+                if (r.hi <= x) continue;
+                if (r.lo >= x1) break;
+                if (r.lo > x) std::fill(P.begin() + x, P.begin() + r.lo, NONE);
+                x = std::max(x, r.hi);
+                if (x >= x1) break;
+            }
+            if (x < x1) std::fill(P.begin() + x, P.begin() + x1, NONE);
         });
+        lap("alloc + clear");
         // per src cluster, per unit column k: slots s0 + t*K + k (t < m) -> d0 + t*Kd (+ k when raw)
         struct Col { uint64_t s0, d0; uint32_t K, Kd, k; bool raw; };
         std::vector<Col> colv;
@@ -499,45 +526,67 @@ adha_status inplace_plan_build(const Layout& ls, const Layout& ld, int64_t n, In
                 colv.push_back({s0, p->bd[cd] / S + b.peer_off / u + q, K, (uint32_t)(ld.stride[cd] / u), k, false});
             }
         }
-        parallel_for(nthr, m, [&](unsigned, uint64_t t0, uint64_t t1) {
+        // the slot map; fixed points (a slot mapped onto itself: NONE, counted) and the cut points
+        // of the cycle decomposition (build_segments) are found on the way
+        std::vector<std::vector<uint32_t>> cut_parts(nthr);
+        std::vector<uint64_t> fixed_parts(nthr, 0);
+        parallel_for(nthr, m, [&](unsigned chunk, uint64_t t0, uint64_t t1) {
+            auto& cp = cut_parts[chunk];
+            uint64_t fx = 0;
             for (const Col& cv : colv)
-                for (uint64_t t = t0; t < t1; ++t)
-                    P[cv.s0 + t * cv.K + cv.k] = (uint32_t)(cv.d0 + t * cv.Kd + (cv.raw ? cv.k : 0));
-        });
-        // P is injective, so the in_d writes of different threads never collide
-        std::vector<uint64_t> cnt(nthr, 0);
-        parallel_for(nthr, nslot, [&](unsigned chunk, uint64_t x0, uint64_t x1) {
-            uint64_t k = 0;
-            for (uint64_t x = x0; x < x1; ++x)
-                if (P[x] != NONE) { in_d[P[x]] = 1; ++k; }
-            cnt[chunk] = k;
-        });
-        for (uint64_t k : cnt) p->content_slots += k;
-        std::vector<uint32_t> free_in, free_out;   // dst-only slots, src-only slots (ascending)
-        {
-            std::vector<std::vector<uint32_t>> fi(nthr), fo(nthr);
-            parallel_for(nthr, nslot, [&](unsigned chunk, uint64_t x0, uint64_t x1) {
-                for (uint64_t x = x0; x < x1; ++x) {
-                    const bool ins = P[x] != NONE;
-                    if (in_d[x] && !ins) fi[chunk].push_back((uint32_t)x);
-                    if (ins && !in_d[x]) fo[chunk].push_back((uint32_t)x);
+                for (uint64_t t = t0; t < t1; ++t) {
+                    const uint32_t x = (uint32_t)(cv.s0 + t * cv.K + cv.k);
+                    const uint32_t y = (uint32_t)(cv.d0 + t * cv.Kd + (cv.raw ? cv.k : 0));
+                    if (x == y) {
+                        P[x] = NONE;
+                        ++fx;
+                        continue;
+                    }
+                    P[x] = y;
+                    if (is_cut(x)) cp.push_back(x);
                 }
-            });
-            for (unsigned c = 0; c < nthr; ++c) {
-                free_in.insert(free_in.end(), fi[c].begin(), fi[c].end());
-                free_out.insert(free_out.end(), fo[c].begin(), fo[c].end());
+            fixed_parts[chunk] = fx;
+        });
+        lap("slot map");
+        for (const Range& r : src_r) p->content_slots += r.hi - r.lo;
+        // dst-only slots (receive content, old bytes are src tail / gap) and src-only slots (content
+        // that no dst slot overwrites), ascending: plain interval differences of the two range lists
+        auto minus = [](const std::vector<Range>& A, const std::vector<Range>& B) {
+            std::vector<uint32_t> out;
+            size_t j = 0;
+            for (const Range& a : A) {
+                uint64_t x = a.lo;
+                while (j < B.size() && B[j].hi <= x) ++j;
+                for (size_t k = j; k < B.size() && B[k].lo < a.hi && x < a.hi; ++k) {
+                    for (; x < std::min(B[k].lo, a.hi); ++x) out.push_back((uint32_t)x);
+                    x = std::max(x, B[k].hi);
+                }
+                for (; x < a.hi; ++x) out.push_back((uint32_t)x);
             }
-        }
+            return out;
+        };
+        const std::vector<uint32_t> free_in = minus(dst_r, src_r), free_out = minus(src_r, dst_r);
+        lap("free lists");
         if (free_in.size() != free_out.size()) return fail(ADHA_ERR_UNSUPPORTED, "in-place plan: slot count mismatch");
         // a dst slot whose old bytes are not content (src tail, gap) receives content; its junk goes
         // to a src-only slot (which becomes dst tail / gap): the permutation closes on U
-        for (size_t i = 0; i < free_in.size(); ++i) P[free_in[i]] = free_out[i];
+        std::vector<uint32_t> cuts;
+        for (size_t i = 0; i < free_in.size(); ++i) {
+            P[free_in[i]] = free_out[i];
+            if (is_cut(free_in[i])) cuts.push_back(free_in[i]);
+        }
         p->junk_slots = free_in.size();
+        for (unsigned c = 0; c < nthr; ++c) {
+            cuts.insert(cuts.end(), cut_parts[c].begin(), cut_parts[c].end());
+            p->fixed_slots += fixed_parts[c];
+        }
+        std::sort(cuts.begin(), cuts.end());
+        lap("cut points");
         const char* ve = std::getenv("ADHA_IP_VERIFY");
         const bool verify = ve && *ve == '1';
         uvector<uint32_t> P0;
         if (verify) P0 = P;
-        build_segments(P, nslot, nthr, p);
+        build_segments(P, nslot, nthr, p, cuts);
         if (verify) {
             const std::string why = verify_segments(P0, *p);
             if (!why.empty()) return fail(ADHA_ERR_PLANNER, "in-place plan verification: " + why);

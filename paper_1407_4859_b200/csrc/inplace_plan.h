@@ -19,18 +19,38 @@
 // (the tail) are saved to the workspace first and written to their dst positions last.
 #pragma once
 
+#include <sys/mman.h>
+
+#include <cstdlib>
 #include <memory>
+#include <new>
 #include <utility>
 #include <vector>
 
 namespace adha {
 // std::allocator whose default construction leaves trivial values uninitialised: the plan's
 // large index arrays (tens of MB at C3's size) are filled in parallel, not zeroed serially first
+// Arrays of >= 4 MB are 2 MB-aligned and advised as transparent huge pages: their first touch
+// (the parallel fill) then faults 512x fewer pages -- the first plan of a process spent about a
+// third of its time in page faults at C3's size.
 template <class T>
 struct UninitAlloc : std::allocator<T> {
     using std::allocator<T>::allocator;
     template <class U>
     struct rebind { using other = UninitAlloc<U>; };
+    T* allocate(size_t n) {
+        const size_t bytes = n * sizeof(T);
+        if (bytes < (4u << 20)) return std::allocator<T>::allocate(n);
+        const size_t huge = 2u << 20, rounded = (bytes + huge - 1) / huge * huge;
+        void* p = std::aligned_alloc(huge, rounded);
+        if (!p) throw std::bad_alloc();
+        madvise(p, rounded, MADV_HUGEPAGE);
+        return static_cast<T*>(p);
+    }
+    void deallocate(T* p, size_t n) {
+        if (n * sizeof(T) < (4u << 20)) std::allocator<T>::deallocate(p, n);
+        else std::free(p);
+    }
     template <class U, class... Args>
     void construct(U* p, Args&&... args) {
         if constexpr (sizeof...(Args) == 0) ::new ((void*)p) U;
