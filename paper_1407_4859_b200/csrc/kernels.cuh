@@ -175,6 +175,20 @@ __device__ __forceinline__ void tile_next(const TiledParams& p, uint32_t H, Tile
 // copies land.  Unlike TMA bulk copies, the cost does not grow with the number of src chunks
 // (64 SoA chunks of 512 B per tile: profiles/r02aa_pieces.log).  (c0, b0) cache this warp's first
 // chunk and its packed begin for component ak.
+// one 16-byte FieldDesc of the plan table (device memory, read-only)
+__device__ __forceinline__ FieldDesc ldg_field(const FieldDesc* f) {
+    const uint4 v = ldg_nc128(reinterpret_cast<const uint4*>(f));
+    FieldDesc d;
+    d.sc = (uint8_t)(v.x & 0xFFu);
+    d.dc = (uint8_t)((v.x >> 8) & 0xFFu);
+    d.sbl = (uint8_t)((v.x >> 16) & 0xFFu);
+    d.dbl = (uint8_t)(v.x >> 24);
+    d.soff = v.y;
+    d.doff = v.z;
+    d.width = v.w;
+    return d;
+}
+
 struct CpaState {
     int ak;
     uint32_t c0, b0;
@@ -223,10 +237,14 @@ using TableOf = typename std::conditional<(NG > 0), GroupTable<NG>, EntryTable<N
 // CHAIN: the fused-chain instantiations (TiledParams::chain; unit mode, STG write-back); the
 // plain ones compile every chain branch away.
 // The plan's table (TableOf<NENT, NG>) is read from its device copy at p.table.
-template <typename U, int NENT, int EMAX, int NG = 0, int GMAX = 1, bool TMAC = false, bool CHAIN = false>
+// CPA: the consumer cp.async loader instantiations (TiledParams::cpa; 4-byte unit mode, STG
+// write-back); the plain ones compile the loader away.
+template <typename U, int NENT, int EMAX, int NG = 0, int GMAX = 1, bool TMAC = false, bool CHAIN = false,
+          bool CPA = false>
 __global__ void __launch_bounds__(TMAC ? NTHREADS_TMA : NTHREADS, 1)
     remap_tiled_kernel(const __grid_constant__ TiledParams p) {
     static_assert(!CHAIN || (NG == 0 && !TMAC), "chain mode: unit mode with STG write-back only");
+    static_assert(!CPA || (NG == 0 && !TMAC && !CHAIN), "cp.async loader: unit mode with STG write-back only");
     const TableOf<NENT, NG>& et = *reinterpret_cast<const TableOf<NENT, NG>*>(p.table);
     extern __shared__ __align__(1024) uint8_t smem[];
     const uint32_t warp = threadIdx.x >> 5;
@@ -243,7 +261,7 @@ __global__ void __launch_bounds__(TMAC ? NTHREADS_TMA : NTHREADS, 1)
     const uint32_t stored0 = oempty0 + 8 * S_OUT_MAX;  // 8 mbarriers (chain): tile i's stores are visible
     if (threadIdx.x == 0) {
         for (uint32_t s = 0; s < p.s_in; ++s) {
-            mbar_init(full0 + 8 * s, (!TMAC && !CHAIN && NG == 0 && p.cpa) ? NCONS * 32 : 1);
+            mbar_init(full0 + 8 * s, CPA ? NCONS * 32 : 1);
             mbar_init(empty0 + 8 * s, NCONS);
         }
         for (uint32_t o = 0; o < S_OUT_MAX; ++o) {
@@ -294,7 +312,7 @@ __global__ void __launch_bounds__(TMAC ? NTHREADS_TMA : NTHREADS, 1)
     }
 
     if (warp == NCONS) {
-        if (!TMAC && !CHAIN && NG == 0 && p.cpa) return;   // the consumers load the tiles (cpa_issue)
+        if (CPA) return;                                // the consumers load the tiles (cpa_issue)
         // ------------------------------------------------------------ TMA producer
         // Per component, every lane holds up to PMAX bulk-load pieces of the tile (src chunks cut
         // into pieces of at most `split` bytes): smem offset, global offset of tile 0, bytes, and
@@ -446,7 +464,7 @@ __global__ void __launch_bounds__(TMAC ? NTHREADS_TMA : NTHREADS, 1)
             if (own && (K.flags & CF_TAIL_ZERO)) {
                 // every dst cluster of the component: bytes [lo*stride, ceil(N/B)*B*stride) := 0
                 for (uint32_t f = K.f_lo; f < K.f_hi; ++f) {
-                    const FieldDesc fd = et.fields[f];
+                    const FieldDesc fd = ldg_field(et.fields + f);
                     const uint64_t B = 1ull << fd.dbl, st = p.dstc[fd.dc].stride;
                     const uint64_t a0 = p.dst + p.dstc[fd.dc].region + (uint64_t)lo * st;
                     const uint64_t a1 = p.dst + p.dstc[fd.dc].region + ((uint64_t)p.n_records + B - 1) / B * B * st;
@@ -469,7 +487,7 @@ __global__ void __launch_bounds__(TMAC ? NTHREADS_TMA : NTHREADS, 1)
                         const uint32_t q = (uint32_t)x / (uint32_t)n_tail;
                         const uint32_t f = K.f_lo + q;
                         const uint64_t r = (uint64_t)(lo + ((uint32_t)x - q * (uint32_t)n_tail));
-                        const FieldDesc fd = et.fields[f];
+                        const FieldDesc fd = ldg_field(et.fields + f);
                         const uint64_t ss = p.srcc[fd.sc].stride, ds = p.dstc[fd.dc].stride;
                         sp[m] = (const U*)(p.src + p.srcc[fd.sc].region + (r >> fd.sbl) * (ss << fd.sbl) +
                                            ((uint64_t)fd.soff << fd.sbl) + (r & ((1u << fd.sbl) - 1)) * fd.width);
@@ -507,7 +525,7 @@ __global__ void __launch_bounds__(TMAC ? NTHREADS_TMA : NTHREADS, 1)
     // tile i's stage as soon as every warp has passed tile i's output barrier (its permutation
     // done), before tile i's copy-out -- as early as the TMA producer would issue it.  (Never with
     // the TMA write-back, which has no such barrier.)
-    const bool cpa = !TMAC && !CHAIN && NG == 0 && p.cpa;   // (unit mode: byte groups would spill)
+    constexpr bool cpa = CPA;
     TileIter ahead;
     CpaState cst{-1, 0u, 0u};
     int64_t ai = 0;
@@ -715,7 +733,16 @@ __global__ void __launch_bounds__(TMAC ? NTHREADS_TMA : NTHREADS, 1)
                             sts(oa + (q + 2) * dO, v2);
                             sts(oa + (q + 3) * dO, v3);
                         }
-                        for (; q < periods; ++q) sts(oa + q * dO, lds<U>(ia + q * di));
+                        // the last periods % 4 (short tiles: all of them), loads first as above
+                        const uint32_t r = periods - q;
+                        if (r) {
+                            const U v0 = lds<U>(ia + q * di);
+                            const U v1 = r > 1 ? lds<U>(ia + (q + 1) * di) : v0;
+                            const U v2 = r > 2 ? lds<U>(ia + (q + 2) * di) : v0;
+                            sts(oa + q * dO, v0);
+                            if (r > 1) sts(oa + (q + 1) * dO, v1);
+                            if (r > 2) sts(oa + (q + 2) * dO, v2);
+                        }
                     }
                 }
             }

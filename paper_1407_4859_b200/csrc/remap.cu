@@ -87,6 +87,24 @@ TiledLauncher pick_chain(uint32_t unit, int cls, const void** fn) {
     return pick_chain_cls<uint8_t>(cls, fn);
 }
 
+// consumer cp.async loader instantiations (4-byte units)
+template <int CLS>
+void launch_cpa(dim3 grid, dim3 block, size_t smem, cudaStream_t st, const TiledParams& p) {
+    remap_tiled_kernel<uint32_t, CLASS_NENT[CLS], CLASS_EMAX[CLS], 0, 1, false, false, true><<<grid, block, smem, st>>>(p);
+}
+template <int CLS>
+const void* cpa_fn() {
+    return (const void*)&remap_tiled_kernel<uint32_t, CLASS_NENT[CLS], CLASS_EMAX[CLS], 0, 1, false, false, true>;
+}
+TiledLauncher pick_cpa(int cls, const void** fn) {
+    switch (cls) {
+        case 0: *fn = cpa_fn<0>(); return &launch_cpa<0>;
+        case 1: *fn = cpa_fn<1>(); return &launch_cpa<1>;
+        case 2: *fn = cpa_fn<2>(); return &launch_cpa<2>;
+        default: *fn = cpa_fn<3>(); return &launch_cpa<3>;
+    }
+}
+
 template <typename U, bool TMAC>
 TiledLauncher pick_cls(int cls, const void** fn) {
     switch (cls) {
@@ -544,10 +562,11 @@ adha_status remap_checked(const uint8_t* src, const Layout& ls, uint8_t* dst, co
         cpa = cpa && any;
         if (ld_env && std::strcmp(ld_env, "cpa") == 0) cpa = true;
         if (ld_env && std::strcmp(ld_env, "tma") == 0) cpa = false;
-        P->cpa = (cpa && !P->tma_copy && !plan->byte_groups) ? 1u : 0u;
+        P->cpa = (cpa && !P->tma_copy && !plan->byte_groups && plan->unit == 4) ? 1u : 0u;
     }
     const void* fn = nullptr;
     TiledLauncher launch = plan->byte_groups ? pick_groups(plan->group_class, P->tma_copy != 0, &fn)
+                           : P->cpa          ? pick_cpa(plan->table_class, &fn)
                                              : pick(plan->unit, plan->table_class, P->tma_copy != 0, &fn);
     const int threads = P->tma_copy ? NTHREADS_TMA : NTHREADS;
     s = device_setup(fn, &n_sm, threads);
