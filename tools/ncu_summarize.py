@@ -12,7 +12,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 ALGO = {"C2": 2 * 10_000_000 * 80, "C3": 2 * 50_000_000 * 320, "C3R": 2 * 50_000_000 * 320, "C4": 2 * 59_652_323 * 36,
-        "C5": 2 * 107_374_182 * 80, "P1": 2 * 16_777_216 * 36, "P2": 2 * 8_388_608 * 128}
+        "C5": 2 * 107_374_182 * 80, "C4M": 2 * 59_652_323 * 12, "P1": 2 * 16_777_216 * 36, "P2": 2 * 8_388_608 * 128}
 SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-9, "us": 1e-6, "usecond": 1e-6,
          "ms": 1e-3, "msecond": 1e-3, "nsecond": 1e-9, "s": 1.0, "%": 1.0}
 
