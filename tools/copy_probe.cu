@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <functional>
+#include <cstring>
 #include <string>
 #include <vector>
 
@@ -365,6 +366,27 @@ int main(int argc, char** argv) {
     auto rw = [&](float ms) { return 2.0 * bytes / (ms * 1e-3) / 1e9; };
     auto one = [&](float ms) { return 1.0 * bytes / (ms * 1e-3) / 1e9; };
     printf("bytes per buffer %zu, SMs %d\n", bytes, sms);
+
+    if (argc > 2 && std::string(argv[2]) == "h2d") {
+        // H2D of 256 MB as one copy, and as P copies of 256/P MB from P regions 4 GB/P apart (an
+        // SoA chunk of adha_remap_host)
+        const size_t chunk = 256u << 20, hbytes = 1ull << 32;
+        uint8_t* h = nullptr;
+        CK(cudaMallocHost(&h, hbytes));
+        memset(h, 3, hbytes);
+        for (int P : {1, 16, 64, 256}) {
+            const size_t piece = chunk / P, stride = hbytes / P;
+            std::vector<void*> dsts(P), srcs(P);
+            std::vector<size_t> sizes(P, piece);
+            for (int j = 0; j < P; ++j) { dsts[j] = d + j * piece; srcs[j] = h + j * stride; }
+            float ms = time_it(st, 5, [&] {
+                for (int j = 0; j < P; ++j) CK(cudaMemcpyAsync(dsts[j], srcs[j], piece, cudaMemcpyHostToDevice, st));
+            });
+            printf("H2D 256 MB as %3d copies of %7zu B: %7.3f ms %6.1f GB/s\n", P, piece, ms, chunk / (ms * 1e-3) / 1e9);
+        }
+        CK(cudaFreeHost(h));
+        return 0;
+    }
     if (argc > 2 && std::string(argv[2]) == "pieces") {
         for (uint32_t TB : {40960u, 32768u}) {
             for (uint32_t S : {2u, 3u}) {
