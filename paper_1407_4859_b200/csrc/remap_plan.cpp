@@ -248,7 +248,7 @@ RemapPlan compile_plan(const Layout& ls, const Layout& ld, bool merge) {
 
     // unit mode: the consumers copy the entry table (off | sc | dc) and the cluster descriptors
     // into shared memory once per CTA, so a component switch reads its entries with LDS instead of
-    // lane-divergent (serialised) constant-bank loads from the kernel parameters
+    // lane-divergent loads (the table itself comes from its device copy, remap.cu device_table)
     {
         uint64_t w = 0;
         for (auto& K : P.comps)
@@ -458,7 +458,7 @@ RemapPlan compile_plan(const Layout& ls, const Layout& ld, bool merge) {
                 perms.push_back({ps[0], ps[1], ps[2], ps[3], po[0], po[1], po[2], po[3]});
             }
         };
-        // Dense packing (the fallback when the balanced tables below exceed the parameter space):
+        // Dense packing (the fallback when the balanced tables below exceed the largest group table):
         // the largest conflict-free pick of each instruction is topped up with the next groups.
         auto pack = [&](std::vector<ByteGroup> cg, size_t ki) {
             std::vector<ByteGroup> out;
@@ -594,7 +594,7 @@ RemapPlan compile_plan(const Layout& ls, const Layout& ld, bool merge) {
         };
         {
             // per component: the instruction count with the smallest estimated busiest-warp time;
-            // if the tables do not fit the parameter space, the dense packing instead
+            // if the tables do not fit the largest group table (GCLASS_NG[1]), the dense packing instead
             groups.clear();
             bool fits = true;
             for (size_t ki = 0; ki < P.comps.size() && fits; ++ki) {
@@ -753,7 +753,8 @@ RemapPlan compile_plan(const Layout& ls, const Layout& ld, bool merge) {
         instr += K.n_instr;
     }
 
-    // kernel-parameter image of EntryTable<NENT>: off[NENT] | sc[NENT] | dc[NENT] | fields[MAXF]
+    // table image of EntryTable<NENT> (uploaded to device memory once per plan and device, remap.cu
+    // device_table): off[NENT] | sc[NENT] | dc[NENT] | fields[MAXF]
     const uint32_t nent = (uint32_t)CLASS_NENT[cls];
     const size_t bytes = 6ull * nent + sizeof(FieldDesc) * MAXF;
     P.table.assign((bytes + 3) / 4, 0u);
