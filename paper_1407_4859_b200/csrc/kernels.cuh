@@ -169,12 +169,13 @@ __device__ __forceinline__ void tile_next(const TiledParams& p, uint32_t H, Tile
     }
 }
 
-// Consumer-side loader (TiledParams::cpa): warp w of the consumers copies bytes [w*B/8, (w+1)*B/8)
-// of tile (k, lt)'s packed src chunks (B = tile_bytes) into input stage `sb` with 16-byte cp.async,
-// 512 contiguous bytes per warp instruction, then arrives on the stage's `full` barrier when its
-// copies land.  Unlike TMA bulk copies, the cost does not grow with the number of src chunks
-// (64 SoA chunks of 512 B per tile: profiles/r02aa_pieces.log).  (c0, b0) cache this warp's first
-// chunk and its packed begin for component ak.
+// cp.async loader (TiledParams::cpa, the CPA instantiations): loader warp lw of NLOAD copies
+// bytes [lw*B/NLOAD, (lw+1)*B/NLOAD) of tile (k, lt)'s packed src chunks (B = tile_bytes) into
+// input stage `sb` with 16-byte cp.async, 512 contiguous bytes per warp instruction, then arrives
+// on the stage's `full` barrier when its copies land (count NLOAD*32).  Unlike TMA bulk copies,
+// the cost does not grow with the number of src chunks (64 SoA chunks of 640 B per tile:
+// profiles/r02aa_pieces.log).  Cluster descriptors come from the kernel parameters (uniform per
+// warp); (c0, b0) cache this warp's first chunk and its packed begin for component ak.
 // one 16-byte FieldDesc of the plan table (device memory, read-only)
 __device__ __forceinline__ FieldDesc ldg_field(const FieldDesc* f) {
     const uint4 v = ldg_nc128(reinterpret_cast<const uint4*>(f));
@@ -193,16 +194,16 @@ struct CpaState {
     int ak;
     uint32_t c0, b0;
 };
-__device__ __forceinline__ void cpa_issue(const TiledParams& p, uint32_t scl, uint32_t k, int64_t lt, uint32_t sb,
-                                          uint32_t full, uint32_t warp, uint32_t lane, CpaState& cs) {
+__device__ __forceinline__ void cpa_issue(const TiledParams& p, uint32_t k, int64_t lt, uint32_t sb, uint32_t full,
+                                          uint32_t lw, uint32_t lane, CpaState& cs) {
     const CompDesc& K = p.comp[k];
     const uint32_t TV = K.tile_bytes >> 4;
-    const uint32_t w0 = (warp * TV / NCONS) << 4, w1 = ((warp + 1) * TV / NCONS) << 4;
+    const uint32_t w0 = (lw * TV / NLOAD) << 4, w1 = ((lw + 1) * TV / NLOAD) << 4;
     if ((int)k != cs.ak) {
         cs.ak = (int)k;
         uint32_t c = K.sc_lo, b = 0;
         for (;;) {
-            const uint32_t e = b + K.T * lds<uint32_t>(scl + 16 * c + 8);
+            const uint32_t e = b + K.T * p.srcc[c].stride;
             if (e > w0 || c + 1 >= K.sc_hi) break;
             b = e;
             ++c;
@@ -212,11 +213,11 @@ __device__ __forceinline__ void cpa_issue(const TiledParams& p, uint32_t scl, ui
     }
     uint32_t c = cs.c0, b = cs.b0;
     while (b < w1 && c < K.sc_hi) {
-        const uint4 d = lds128(scl + 16 * c);             // region lo, region hi, stride, smem
-        const uint32_t bytes = K.T * d.z, e = b + bytes;
+        const ClusterDesc d = p.srcc[c];
+        const uint32_t bytes = K.T * d.stride, e = b + bytes;
         const uint32_t lo = max(b, w0), hi = min(e, w1);
-        const uint8_t* g = (const uint8_t*)(p.src + ((uint64_t)d.x | ((uint64_t)d.y << 32)) + (uint64_t)lt * bytes) - b;
-        const uint32_t sm = sb + d.w - b;
+        const uint8_t* g = (const uint8_t*)(p.src + d.region + (uint64_t)lt * bytes) - b;
+        const uint32_t sm = sb + d.smem - b;
         for (uint32_t o = lo + lane * 16; o < hi; o += 32 * 16) cp_async16(sm + o, g + o);
         b = e;
         ++c;
@@ -237,11 +238,11 @@ using TableOf = typename std::conditional<(NG > 0), GroupTable<NG>, EntryTable<N
 // CHAIN: the fused-chain instantiations (TiledParams::chain; unit mode, STG write-back); the
 // plain ones compile every chain branch away.
 // The plan's table (TableOf<NENT, NG>) is read from its device copy at p.table.
-// CPA: the consumer cp.async loader instantiations (TiledParams::cpa; 4-byte unit mode, STG
-// write-back); the plain ones compile the loader away.
+// CPA: the cp.async loader instantiations (TiledParams::cpa; 4-byte unit mode, STG write-back):
+// NLOAD loader warps replace the TMA producer warp.
 template <typename U, int NENT, int EMAX, int NG = 0, int GMAX = 1, bool TMAC = false, bool CHAIN = false,
           bool CPA = false>
-__global__ void __launch_bounds__(TMAC ? NTHREADS_TMA : NTHREADS, 1)
+__global__ void __launch_bounds__(TMAC ? NTHREADS_TMA : CPA ? NTHREADS_CPA : NTHREADS, 1)
     remap_tiled_kernel(const __grid_constant__ TiledParams p) {
     static_assert(!CHAIN || (NG == 0 && !TMAC), "chain mode: unit mode with STG write-back only");
     static_assert(!CPA || (NG == 0 && !TMAC && !CHAIN), "cp.async loader: unit mode with STG write-back only");
@@ -261,7 +262,7 @@ __global__ void __launch_bounds__(TMAC ? NTHREADS_TMA : NTHREADS, 1)
     const uint32_t stored0 = oempty0 + 8 * S_OUT_MAX;  // 8 mbarriers (chain): tile i's stores are visible
     if (threadIdx.x == 0) {
         for (uint32_t s = 0; s < p.s_in; ++s) {
-            mbar_init(full0 + 8 * s, CPA ? NCONS * 32 : 1);
+            mbar_init(full0 + 8 * s, CPA ? NLOAD * 32 : 1);
             mbar_init(empty0 + 8 * s, NCONS);
         }
         for (uint32_t o = 0; o < S_OUT_MAX; ++o) {
@@ -311,8 +312,23 @@ __global__ void __launch_bounds__(TMAC ? NTHREADS_TMA : NTHREADS, 1)
         return;
     }
 
+    if (CPA && warp >= NCONS) {
+        // ------------------------------------------------------------ cp.async loader warps
+        // the TMA producer's protocol (empty -> load -> full), the copies split over NLOAD warps
+        CpaState cs{-1, 0u, 0u};
+        uint32_t stage = 0, phase = 0;
+        const int64_t nt = cta_tiles(p, 0);
+        TileIter it;
+        tile_begin(p, 0, it);
+        for (int64_t i = 0; i < nt; ++i, tile_next(p, 0, it)) {
+            mbar_wait(empty0 + 8 * stage, phase ^ 1);
+            cpa_issue(p, it.k, it.lt, in0 + stage * p.stage_bytes, full0 + 8 * stage, warp - NCONS, lane, cs);
+            if (++stage == p.s_in) { stage = 0; phase ^= 1; }
+        }
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        return;
+    }
     if (warp == NCONS) {
-        if (CPA) return;                                // the consumers load the tiles (cpa_issue)
         // ------------------------------------------------------------ TMA producer
         // Per component, every lane holds up to PMAX bulk-load pieces of the tile (src chunks cut
         // into pieces of at most `split` bytes): smem offset, global offset of tile 0, bytes, and
@@ -521,20 +537,6 @@ __global__ void __launch_bounds__(TMAC ? NTHREADS_TMA : NTHREADS, 1)
     TileIter it;
     tile_begin(p, H, it);
     bool stored_pending = false;     // chain: tile i-1's stores not yet fenced and signalled
-    // consumer-side loads (p.cpa): the first s_in tiles are issued up front; tile i+s_in goes into
-    // tile i's stage as soon as every warp has passed tile i's output barrier (its permutation
-    // done), before tile i's copy-out -- as early as the TMA producer would issue it.  (Never with
-    // the TMA write-back, which has no such barrier.)
-    constexpr bool cpa = CPA;
-    TileIter ahead;
-    CpaState cst{-1, 0u, 0u};
-    int64_t ai = 0;
-    if (cpa) {
-        tile_begin(p, 0, ahead);
-        for (; ai < (int64_t)p.s_in && ai < nt; ++ai, tile_next(p, 0, ahead))
-            cpa_issue(p, scl, ahead.k, ahead.lt, in0 + (uint32_t)ai * p.stage_bytes, full0 + 8 * (uint32_t)ai, warp,
-                      lane, cst);
-    }
     for (int64_t i = 0; i < nt; ++i, tile_next(p, H, it)) {
         k = it.k;
         const int64_t lt = it.lt;
@@ -762,11 +764,6 @@ __global__ void __launch_bounds__(TMAC ? NTHREADS_TMA : NTHREADS, 1)
                 ++i_t;
             } else {
                 named_bar_sync(1, NCONS * 32);                  // output tile complete
-                if (cpa && ai < nt) {                           // this tile's input stage is free
-                    cpa_issue(p, scl, ahead.k, ahead.lt, ib, full0 + 8 * stage, warp, lane, cst);
-                    ++ai;
-                    tile_next(p, 0, ahead);
-                }
                 ADHA_PT(const long long c3 = clock64(); ph[2] += c3 - c2);
                 if (H && p.chain_hints)
                     copy_out<true>((uint8_t*)p.dst, ob, tid, lt, nv, gofs, gstep, k + 1 < H ? kpol : spol);

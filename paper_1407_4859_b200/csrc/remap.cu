@@ -568,7 +568,7 @@ adha_status remap_checked(const uint8_t* src, const Layout& ls, uint8_t* dst, co
     TiledLauncher launch = plan->byte_groups ? pick_groups(plan->group_class, P->tma_copy != 0, &fn)
                            : P->cpa          ? pick_cpa(plan->table_class, &fn)
                                              : pick(plan->unit, plan->table_class, P->tma_copy != 0, &fn);
-    const int threads = P->tma_copy ? NTHREADS_TMA : NTHREADS;
+    const int threads = P->tma_copy ? NTHREADS_TMA : P->cpa ? NTHREADS_CPA : NTHREADS;
     s = device_setup(fn, &n_sm, threads);
     if (s != ADHA_OK) return s;
     s = device_table("p" + std::to_string(plan->uid), plan->table, st, &P->table);

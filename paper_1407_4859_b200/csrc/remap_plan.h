@@ -42,6 +42,8 @@ namespace dev {
 constexpr int NCONS = 8;                       // consumer warps per CTA
 constexpr int NTHREADS = (NCONS + 1) * 32;     // + one TMA producer warp
 constexpr int NTHREADS_TMA = (NCONS + 2) * 32; // + a TMA write-back warp (tma_copy instantiations)
+constexpr int NLOAD = 3;                       // cp.async loader warps (cpa instantiations)
+constexpr int NTHREADS_CPA = (NCONS + NLOAD) * 32;
 constexpr int MAXC = 128;                      // clusters per side (tiled kernel)
 constexpr int MAXF = 256;                      // fields (tiled kernel tail table, naive chunk)
 constexpr int MAXK = 64;                       // components
@@ -102,9 +104,8 @@ struct TiledParams {
                           // every component has the same T and n_tiles (bands); regions are absolute
     uint32_t chain_group; // chain: bands per group (1..8), each group run hop by hop
     uint32_t chain_hints; // chain: 1 = loads evict_first, intermediates stored evict_last, the last hop evict_first
-    uint32_t cpa;         // 1: the consumer warps load the tiles themselves with cp.async (16 B per lane,
-                          // S-1 tiles ahead) instead of the producer warp's TMA bulk copies (plain STG
-                          // instantiations only: needs the per-tile barrier after the permutation)
+    uint32_t cpa;         // 1: NLOAD loader warps fill the input stages with cp.async (16 B per lane)
+                          // instead of the producer warp's TMA bulk copies (the CPA instantiations)
     uint64_t table;       // device address of the plan's table image (EntryTable<NENT> / GroupTable<NG>),
                           // uploaded once per plan and device (remap.cu device_table)
     CompDesc comp[MAXK];
