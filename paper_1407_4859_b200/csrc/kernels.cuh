@@ -281,6 +281,7 @@ __global__ void __launch_bounds__(TMAC ? NTHREADS_TMA : CPA ? NTHREADS_CPA : NTH
         // bulk group has finished reading shared memory, so the store overlaps the next
         // permutation.  Chosen per launch for components with one large dst chunk per tile.
         if (lane != 0) return;
+        grid_dep_wait();
         const uint64_t pol = policy_evict_first();
         uint32_t i = 0, k = 0;
         int prev_o = -1;
@@ -315,6 +316,7 @@ __global__ void __launch_bounds__(TMAC ? NTHREADS_TMA : CPA ? NTHREADS_CPA : NTH
     if (CPA && warp >= NCONS) {
         // ------------------------------------------------------------ cp.async loader warps
         // the TMA producer's protocol (empty -> load -> full), the copies split over NLOAD warps
+        grid_dep_wait();
         CpaState cs{-1, 0u, 0u};
         uint32_t stage = 0, phase = 0;
         const int64_t nt = cta_tiles(p, 0);
@@ -334,6 +336,7 @@ __global__ void __launch_bounds__(TMAC ? NTHREADS_TMA : CPA ? NTHREADS_CPA : NTH
         // into pieces of at most `split` bytes): smem offset, global offset of tile 0, bytes, and
         // the per-tile global step.  Issue is then one bulk copy per piece per lane, no parameter
         // walks on the critical path (the producer's issue time gates the 2-stage pipeline).
+        grid_dep_wait();                                  // (PDL) the previous kernel's writes are visible
         const uint64_t pol = policy_evict_first();        // src is read once: evict it first from L2
         uint32_t psm[PMAX], pbytes[PMAX], pstep[PMAX];
         uint64_t pg[PMAX];
@@ -443,6 +446,9 @@ __global__ void __launch_bounds__(TMAC ? NTHREADS_TMA : CPA ? NTHREADS_CPA : NTH
         for (uint32_t i = tid; i < p.n_dstc; i += NCONS * 32) sts128(dcl + 16 * i, dv[i]);
         named_bar_sync(1, NCONS * 32);
     }
+    // (PDL) everything above touched only shared memory, the parameters and the plan table; the
+    // tails and the copy-out below read and write the caller's buffers
+    grid_dep_wait();
     const uint64_t spol = policy_evict_first();
     const uint64_t kpol = CHAIN ? policy_evict_last() : 0;   // chain: intermediates, read back by the next hop
     uint32_t ioff[EMAX], ooff[EMAX], din[EMAX], dout[EMAX];

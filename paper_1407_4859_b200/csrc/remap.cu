@@ -50,11 +50,30 @@ static_assert(sizeof(dev::NaiveParams) <= 32764, "naive kernel parameters too la
 
 namespace detail {
 
-typedef void (*TiledLauncher)(dim3, dim3, size_t, cudaStream_t, const TiledParams&);
+typedef void (*TiledLauncher)(dim3, dim3, size_t, cudaStream_t, const TiledParams&, bool);
+
+// Launch with programmatic dependent launch allowed (pdl): the kernel may start while the previous
+// kernel in the stream drains; it touches no global memory the previous kernel could write before
+// its griddepcontrol.wait (kernels.cuh), only its parameters and its plan table.
+template <typename... Args>
+void launch_ex(void (*kernel)(Args...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, bool pdl,
+               const TiledParams& p) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, kernel, p);
+}
 
 template <typename U, int CLS, bool TMAC>
-void launch_tiled(dim3 grid, dim3 block, size_t smem, cudaStream_t st, const TiledParams& p) {
-    remap_tiled_kernel<U, CLASS_NENT[CLS], CLASS_EMAX[CLS], 0, 1, TMAC><<<grid, block, smem, st>>>(p);
+void launch_tiled(dim3 grid, dim3 block, size_t smem, cudaStream_t st, const TiledParams& p, bool pdl) {
+    launch_ex(&remap_tiled_kernel<U, CLASS_NENT[CLS], CLASS_EMAX[CLS], 0, 1, TMAC>, grid, block, smem, st, pdl, p);
 }
 
 template <typename U, int CLS, bool TMAC>
@@ -66,8 +85,8 @@ const void* tiled_fn() {
 
 // fused-chain instantiations (classes 0..2; chain_tiled never picks the largest class)
 template <typename U, int CLS>
-void launch_chain(dim3 grid, dim3 block, size_t smem, cudaStream_t st, const TiledParams& p) {
-    remap_tiled_kernel<U, CLASS_NENT[CLS], CLASS_EMAX[CLS], 0, 1, false, true><<<grid, block, smem, st>>>(p);
+void launch_chain(dim3 grid, dim3 block, size_t smem, cudaStream_t st, const TiledParams& p, bool pdl) {
+    launch_ex(&remap_tiled_kernel<U, CLASS_NENT[CLS], CLASS_EMAX[CLS], 0, 1, false, true>, grid, block, smem, st, pdl, p);
 }
 template <typename U, int CLS>
 const void* chain_fn() {
@@ -89,8 +108,8 @@ TiledLauncher pick_chain(uint32_t unit, int cls, const void** fn) {
 
 // consumer cp.async loader instantiations (4-byte units)
 template <int CLS>
-void launch_cpa(dim3 grid, dim3 block, size_t smem, cudaStream_t st, const TiledParams& p) {
-    remap_tiled_kernel<uint32_t, CLASS_NENT[CLS], CLASS_EMAX[CLS], 0, 1, false, false, true><<<grid, block, smem, st>>>(p);
+void launch_cpa(dim3 grid, dim3 block, size_t smem, cudaStream_t st, const TiledParams& p, bool pdl) {
+    launch_ex(&remap_tiled_kernel<uint32_t, CLASS_NENT[CLS], CLASS_EMAX[CLS], 0, 1, false, false, true>, grid, block, smem, st, pdl, p);
 }
 template <int CLS>
 const void* cpa_fn() {
@@ -116,8 +135,8 @@ TiledLauncher pick_cls(int cls, const void** fn) {
 }
 
 template <int GC, bool TMAC>
-void launch_groups(dim3 grid, dim3 block, size_t smem, cudaStream_t st, const TiledParams& p) {
-    remap_tiled_kernel<uint8_t, 32, 1, GCLASS_NG[GC], GCLASS_GMAX[GC], TMAC><<<grid, block, smem, st>>>(p);
+void launch_groups(dim3 grid, dim3 block, size_t smem, cudaStream_t st, const TiledParams& p, bool pdl) {
+    launch_ex(&remap_tiled_kernel<uint8_t, 32, 1, GCLASS_NG[GC], GCLASS_GMAX[GC], TMAC>, grid, block, smem, st, pdl, p);
 }
 template <int GC, bool TMAC>
 const void* groups_fn() {
@@ -199,7 +218,8 @@ TableStore& tables() {
 }
 
 adha_status device_table(const std::string& key, const std::vector<uint32_t>& img, cudaStream_t st,
-                         uint64_t* out) {
+                         uint64_t* out, bool* enqueued) {
+    *enqueued = false;
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
@@ -247,6 +267,7 @@ adha_status device_table(const std::string& key, const std::vector<uint32_t>& im
         table_upload_kernel<<<1, 256, 0, st>>>(*U);
         e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_fail(e, "table_upload_kernel launch");
+        *enqueued = true;                  // the remap that reads it must not launch early (no PDL)
     } else {
         cudaStream_t& us = T.upload_stream[dev];
         if (!us && (e = cudaStreamCreateWithFlags(&us, cudaStreamNonBlocking)) != cudaSuccess)
@@ -258,6 +279,14 @@ adha_status device_table(const std::string& key, const std::vector<uint32_t>& im
     }
     *out = (uint64_t)(uintptr_t)dptr;
     return ADHA_OK;
+}
+
+// Programmatic dependent launch of the tiled kernel (ADHA_PDL=0 disables): a remap may start its
+// prologue (barrier setup, plan-table copy into shared memory) while the previous kernel in the
+// stream drains; its global memory accesses wait for that kernel (griddepcontrol.wait).
+bool pdl_enabled() {
+    const char* e = std::getenv("ADHA_PDL");
+    return !(e && *e == '0');
 }
 
 // per-device setup: SM count and the kernel's dynamic shared memory opt-in
@@ -571,12 +600,14 @@ adha_status remap_checked(const uint8_t* src, const Layout& ls, uint8_t* dst, co
     const int threads = P->tma_copy ? NTHREADS_TMA : P->cpa ? NTHREADS_CPA : NTHREADS;
     s = device_setup(fn, &n_sm, threads);
     if (s != ADHA_OK) return s;
-    s = device_table("p" + std::to_string(plan->uid), plan->table, st, &P->table);
+    bool enq = false;
+    s = device_table("p" + std::to_string(plan->uid), plan->table, st, &P->table, &enq);
     if (s != ADHA_OK) return s;
+    const bool pdl = pdl_enabled() && !enq;
     // a tail-only call still needs one CTA per component tail
     const int64_t grid = std::max<int64_t>(std::min<int64_t>((int64_t)plan->comps.size(), n_sm),
                                            std::min<int64_t>(tiles, n_sm));
-    launch(dim3((unsigned)std::max<int64_t>(grid, 1)), dim3(threads), plan->smem_bytes, st, *P);
+    launch(dim3((unsigned)std::max<int64_t>(grid, 1)), dim3(threads), plan->smem_bytes, st, *P, pdl);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "remap_tiled_kernel launch");
     return ADHA_OK;
@@ -877,10 +908,11 @@ adha_status chain_tiled(void* const* buffers, const adha_layout* const* layouts,
     // the chain's table depends only on its hops' plans (and the class)
     std::string key = "c" + std::to_string(cls);
     for (const auto& pl : plans) key += "." + std::to_string(pl->uid);
-    s = device_table(key, table, st, &P->table);
+    bool enq = false;
+    s = device_table(key, table, st, &P->table, &enq);
     if (s != ADHA_OK) return s;
     const int64_t grid = std::min<int64_t>(bands, n_sm);
-    run(dim3((unsigned)grid), dim3(NTHREADS), smem, st, *P);
+    run(dim3((unsigned)grid), dim3(NTHREADS), smem, st, *P, pdl_enabled() && !enq);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "remap_tiled_kernel (chain) launch");
     return ADHA_OK;
