@@ -108,6 +108,8 @@ __device__ __forceinline__ void fence_proxy_async_global() {
 // programmatic dependent launch: block until the grids this one depends on have completed and
 // their memory operations are visible (a no-op when launched without the PDL attribute)
 __device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// allow the dependent grid to be scheduled (once every CTA has signalled or exited)
+__device__ __forceinline__ void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
