@@ -399,20 +399,17 @@ uint64_t small_bytes() {
 }
 
 // Payload up to which a remap takes the direct kernel instead of the tiled one.  The tiled kernel
-// has a fixed cost per launch (parameters, pipeline fill, table copy, tails: 5-7 us for one
-// component, 6 us for Medical's 7 on the merged plan, 12-19 us for C3's 24; CUDA-graph replay,
-// tools/small_path_probe.py, profiles/r02z_small_path.log) while the direct kernel streams at
-// ~1 TB/s for 4-byte units and ~0.3-0.5 TB/s for 1-/2-byte units after ~2 us.  Crossovers
-// measured on B200: 4-8 MB (4-byte units, any component count below 16), 1-4 MB (1- and 2-byte
-// units), 16-32 MB (C3's 24 components).  ADHA_SMALL_BYTES, when set, overrides this (tests
-// force either path with it).
+// has a fixed cost per launch (pipeline fill, table copy, tails: 4-6 us for one component, 4.6 us
+// for Medical's 7 on the merged plan, 9-10 us for C3's 24, replayed back to back with
+// programmatic dependent launch; tools/small_path_probe.py, profiles/r02ax_small_path.log) while
+// the direct kernel streams at ~1 TB/s for 4-byte units and ~0.3-0.5 TB/s for 1-/2-byte units
+// after ~2 us.  Crossovers measured on B200: 1-4 MB below 16 components (4 MB: K-Means
+// SoA->AoS 6.3 vs 8.3 us tiled vs direct, C2 6.0 vs 5.4), 8-16 MB for C3's 24 components.
+// ADHA_SMALL_BYTES, when set, overrides this (tests force either path with it).
 uint64_t direct_bytes(const RemapPlan& p) {
     const char* e = std::getenv("ADHA_SMALL_BYTES");
     if (e && *e) return (uint64_t)std::strtoull(e, nullptr, 10);
-    const size_t k = p.comps.size();
-    if (p.unit < 4) return 2ull << 20;
-    if (k >= 16) return 16ull << 20;
-    return 4ull << 20;
+    return p.comps.size() >= 16 ? (8ull << 20) : (2ull << 20);
 }
 
 
