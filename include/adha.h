@@ -180,6 +180,10 @@ ADHA_API void adha_layout_destroy(adha_layout* layout);
  *   stream       cudaStream_t (as void*) the kernel is enqueued on
  *
  * Asynchronous: the call enqueues one kernel launch on `stream` and returns.
+ * The tiled kernel is launched with programmatic dependent launch: it may start
+ * its prologue while the previous kernel on `stream` finishes, but it reads and
+ * writes the caller's buffers only after that kernel has completed (stream
+ * order is unchanged; ADHA_PDL=0 turns it off).
  * The per-call plan travels as kernel parameters; the first tiled remap of a
  * layout pair on a device uploads the plan's permutation table (<= 25 KB) into
  * library-owned device memory (a static 4 MB arena per device, then 4 MB
