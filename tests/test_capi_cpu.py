@@ -721,3 +721,21 @@ def test_remap_chain_route(monkeypatch):
     assert os.environ.get("ADHA_CHAIN_TILED_BYTES") is None
     with pytest.raises(A.AdhaError):
         A.remap_chain_route([c4[0], A.Layout([4] * 8, [0] * 8)], 10)
+
+
+def test_routing_thresholds(monkeypatch):
+    """The routing the plan reports (remap.cu direct_bytes / merge_bytes, read by adha_remap_plan_describe):
+    the direct kernel up to 2 MB of payload, up to 8 MB for plans of >= 16 components (C3's 24), the merged
+    plan for multi-component remaps up to 64 MB; ADHA_SMALL_BYTES / ADHA_MERGE_BYTES override them."""
+    monkeypatch.delenv("ADHA_SMALL_BYTES", raising=False)
+    monkeypatch.delenv("ADHA_MERGE_BYTES", raising=False)
+    w16 = [8 if i % 4 == 3 else 4 for i in range(16)]
+    d = A.plan_describe(A.Layout.aos(w16), A.Layout.soa(w16))
+    assert d["direct_bytes"] == 2 << 20 and d["merge_bytes"] == 0
+    w64 = [8 if i % 4 == 3 else 4 for i in range(64)]
+    c3 = [0] * 26 + [1] * 10 + [2] * 4 + [3] * 3 + [4, 5, 6, 7, 4] + list(range(8, 8 + 16))
+    d = A.plan_describe(A.Layout(w64, list(range(64))), A.Layout(w64, c3))
+    assert len(d["components"]) >= 16
+    assert d["direct_bytes"] == 8 << 20 and d["merge_bytes"] == 64 << 20
+    monkeypatch.setenv("ADHA_SMALL_BYTES", "12345")
+    assert A.plan_describe(A.Layout.aos(w16), A.Layout.soa(w16))["direct_bytes"] == 12345
