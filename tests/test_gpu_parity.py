@@ -850,3 +850,34 @@ def test_loaders(loader, merge, monkeypatch):
     ]
     for w, ls, bs, als, ld, bd, ald, n in cases:
         check_pair_ex(w, ls, bs, als, ld, bd, ald, n, seed=n % 89)
+
+
+@pytest.mark.parametrize("pdl", ["1", "0"])
+def test_back_to_back_hazards(pdl, monkeypatch):
+    """Programmatic dependent launch (remap.cu launch_ex, kernels.cuh grid_dep_wait): a remap may start
+    while the previous one drains, but must not read what it writes (RAW) nor write what it still reads
+    (WAR).  A ring of remaps on one stream -- A->B, B->C, C->A, then around again, every buffer both read
+    and overwritten by neighbouring launches -- must end exactly where the oracle's ring ends."""
+    monkeypatch.setenv("ADHA_PDL", pdl)
+    monkeypatch.setenv("ADHA_SMALL_BYTES", "0")
+    widths = config_widths(16)
+    n = 300_007
+    labs = [[0] * 16, list(range(16)), [i // 4 for i in range(16)]]
+    Ls = [A.Layout(widths, l) for l in labs]
+    cols = field_columns(11, n, widths)
+    src = O.pack(cols, widths, labs[0], n, fill=0x3C)
+    bufs = [to_dev(src), sentinel_dev(Ls[1].nbytes(n)), sentinel_dev(Ls[2].nbytes(n))]
+    torch.cuda.synchronize()
+    for _ in range(4):
+        for k in range(3):
+            A.remap(bufs[k], Ls[k], bufs[(k + 1) % 3], Ls[(k + 1) % 3], n)
+    torch.cuda.synchronize()
+    # a full ring returns every payload byte to its AoS place: the oracle's ring, once, ends there too
+    mid = oracle_dst(src, labs[0], labs[1], widths, n)
+    last = oracle_dst(mid, labs[1], labs[2], widths, n)
+    back = np.full(src.size, 0x3C, np.uint8)
+    O.remap(last, labs[2], back, labs[0], widths, n)
+    got = bufs[0].cpu().numpy()[: Ls[0].nbytes(n)]
+    assert np.array_equal(got, back[: Ls[0].nbytes(n)])
+    assert np.array_equal(bufs[1].cpu().numpy()[: Ls[1].nbytes(n)], mid)
+    assert np.array_equal(bufs[2].cpu().numpy()[: Ls[2].nbytes(n)], last)
