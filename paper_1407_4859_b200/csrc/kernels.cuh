@@ -546,11 +546,11 @@ __global__ void __launch_bounds__(TMAC ? NTHREADS_TMA : CPA ? NTHREADS_CPA : NTH
 #ifndef ADHA_PDL_TRIGGER
 #define ADHA_PDL_TRIGGER 1
 #endif
-    if (ADHA_PDL_TRIGGER && nt == 0) grid_dep_launch();
+    if (ADHA_PDL_TRIGGER && nt < ADHA_PDL_TRIGGER) grid_dep_launch();
     for (int64_t i = 0; i < nt; ++i, tile_next(p, H, it)) {
         // (PDL) this CTA's last tile: the next remap in the stream may be scheduled now, so its
         // launch is done by the time SMs free up (its global accesses still wait for this grid)
-        if (ADHA_PDL_TRIGGER && i + 1 == nt) grid_dep_launch();
+        if (ADHA_PDL_TRIGGER && i + ADHA_PDL_TRIGGER == nt) grid_dep_launch();
         k = it.k;
         const int64_t lt = it.lt;
         const uint32_t dist = it.dist;
