@@ -418,14 +418,22 @@ uint64_t direct_bytes(const RemapPlan& p) {
 // they leave a CTA one short tile per component, each paying the pipeline's latency.  A merged
 // tile carries one chunk per src cluster, so with many src clusters its chunks get small and the
 // TMA unit's cost per bulk copy binds (profiles/r02aa_pieces.log): 64 MB for > 32 src clusters,
-// 128 MB up to 32, no limit up to 8.  Measured on B200 (profiles/r02ax_small_path.log,
-// r02bf_small.log, CUDA-graph replay): C3's SoA -> hybrid (64 src clusters) 32 MB 30.9 us merged
-// vs 46.9 per component, 128 MB 89.1 vs 71.8; hybrid -> SoA (24) 128 MB 66.8 vs 74.7, 512 MB
-// 195.8 vs 188.9; Medical AoSV -> SoA (7) 1 MB 4.6 vs 13 us, 512 MB 163.9 vs 170.6.
-uint64_t merge_bytes(size_t n_src_clusters) {
+// 128 MB otherwise -- and no limit for <= 8 src clusters when the component plan has identity
+// components (singleton clusters on both sides), whose separate copy-through tiles lose to whole-
+// record tiles at any size.  Measured on B200 (profiles/r02ax_small_path.log, r02bf_small.log,
+// r02bh_merge_probe.log): C3's SoA -> hybrid (64 src clusters) 32 MB 30.9 us merged vs 46.9 per
+// component, 128 MB 89.1 vs 71.8; hybrid -> SoA (24) 128 MB 66.8 vs 74.7, 512 MB 195.8 vs 188.9;
+// Medical AoSV -> SoA (7, six identity components) 2 GB 655 vs 671 us, SoA -> AoSV 653 vs 683;
+// without identity components (K-Means 4xAoS8 -> SoA, C2 2xAoS8 -> SoA) 2 GB merged is 1-2 %
+// slower.
+uint64_t merge_bytes(const RemapPlan& p) {
     const char* e = std::getenv("ADHA_MERGE_BYTES");
     if (e && *e) return (uint64_t)std::strtoull(e, nullptr, 10);
-    return n_src_clusters > 32 ? (64ull << 20) : n_src_clusters > 8 ? (128ull << 20) : ~0ull;
+    const size_t ns = p.src_order.size();
+    bool identity = false;
+    for (const auto& K : p.comps) identity = identity || K.identity;
+    if (ns <= 8 && identity) return ~0ull;
+    return ns > 32 ? (64ull << 20) : (128ull << 20);
 }
 
 adha_status validate(const void* src, const adha_layout* hs, const void* dst, const adha_layout* hd, int64_t n,
@@ -460,7 +468,7 @@ adha_status remap_checked(const uint8_t* src, const Layout& ls, uint8_t* dst, co
     // was measured per component count; the merged plan only replaces the tiled side of it)
     const uint64_t thr = (ck.dst_local && ck.src_local) ? direct_bytes(*plan) : small_bytes();
     // (a src in host memory keeps the component plan: its tiles read larger chunks over PCIe)
-    if (plan->comps.size() > 1 && ck.src_local && (uint64_t)n * ls.record_bytes <= merge_bytes(plan->src_order.size())) {
+    if (plan->comps.size() > 1 && ck.src_local && (uint64_t)n * ls.record_bytes <= merge_bytes(*plan)) {
         bool alias = false;
         for (const auto& K : plan->comps)
             alias = alias || (K.identity && (uintptr_t)src + ck.bs[K.src_clusters[0]] ==
@@ -1087,7 +1095,7 @@ extern "C" adha_status adha_remap_plan_describe_ex(const adha_layout* hs, const 
     // direct kernel (ADHA_SMALL_BYTES overrides, read now)
     s.pop_back();
     s += ",\"direct_bytes\":" + std::to_string(direct_bytes(*plan)) + ",\"merge_bytes\":" +
-         std::to_string(plan->comps.size() > 1 ? merge_bytes(plan->src_order.size()) : 0) + "}";
+         std::to_string(plan->comps.size() > 1 ? merge_bytes(*plan) : 0) + "}";
     *json_out = (char*)std::malloc(s.size() + 1);
     if (!*json_out) return fail(ADHA_ERR_OOM, "out of host memory");
     std::memcpy(*json_out, s.c_str(), s.size() + 1);
