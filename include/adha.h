@@ -180,7 +180,7 @@ ADHA_API void adha_layout_destroy(adha_layout* layout);
  *   stream       cudaStream_t (as void*) the kernel is enqueued on
  *
  * Asynchronous: the call enqueues one kernel launch on `stream` and returns.
- * The tiled kernel is launched with programmatic dependent launch: it may start
+ * The remap kernels are launched with programmatic dependent launch: a kernel may start
  * its prologue while the previous kernel on `stream` finishes, but it reads and
  * writes the caller's buffers only after that kernel has completed (stream
  * order is unchanged; ADHA_PDL=0 turns it off).

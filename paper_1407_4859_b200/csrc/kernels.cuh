@@ -842,6 +842,10 @@ __global__ void zero_kernel(const __grid_constant__ ZeroParams z) {
 
 template <int NF>
 __global__ void remap_naive_kernel(const __grid_constant__ NaiveParamsT<NF> p) {
+    // (PDL) the previous kernel's writes first; the next launch may be scheduled once every block
+    // of this grid has started (its own accesses wait for this grid to complete)
+    grid_dep_wait();
+    grid_dep_launch();
     const int64_t n = p.n_records;
     const int64_t total = n * (int64_t)p.n_fields;
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total; k += (int64_t)gridDim.x * blockDim.x) {
@@ -865,6 +869,8 @@ __global__ void remap_naive_kernel(const __grid_constant__ NaiveParamsT<NF> p) {
 }
 
 __global__ void __launch_bounds__(256) remap_chain_small_kernel(const __grid_constant__ ChainParams p) {
+    grid_dep_wait();                     // (PDL) as remap_naive_kernel
+    grid_dep_launch();
     const int64_t n = p.n_records;
     const int64_t per = (n + gridDim.x - 1) / gridDim.x;
     const int64_t lo = (int64_t)blockIdx.x * per;

@@ -52,6 +52,30 @@ namespace detail {
 
 typedef void (*TiledLauncher)(dim3, dim3, size_t, cudaStream_t, const TiledParams&, bool);
 
+// Programmatic dependent launch of the remap kernels (ADHA_PDL=0 disables): a remap may start its
+// prologue (barrier setup, plan-table copy into shared memory) while the previous kernel in the
+// stream drains; its global memory accesses wait for that kernel (griddepcontrol.wait).
+bool pdl_enabled() {
+    const char* e = std::getenv("ADHA_PDL");
+    return !(e && *e == '0');
+}
+
+// any kernel taking one parameter struct, with programmatic dependent launch allowed (pdl)
+template <typename Prm>
+void launch_pdl(void (*kernel)(Prm), dim3 grid, dim3 block, size_t smem, cudaStream_t st, bool pdl, const Prm& p) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, kernel, p);
+}
+
 // Launch with programmatic dependent launch allowed (pdl): the kernel may start while the previous
 // kernel in the stream drains; it touches no global memory the previous kernel could write before
 // its griddepcontrol.wait (kernels.cuh), only its parameters and its plan table.
@@ -281,14 +305,6 @@ adha_status device_table(const std::string& key, const std::vector<uint32_t>& im
     return ADHA_OK;
 }
 
-// Programmatic dependent launch of the tiled kernel (ADHA_PDL=0 disables): a remap may start its
-// prologue (barrier setup, plan-table copy into shared memory) while the previous kernel in the
-// stream drains; its global memory accesses wait for that kernel (griddepcontrol.wait).
-bool pdl_enabled() {
-    const char* e = std::getenv("ADHA_PDL");
-    return !(e && *e == '0');
-}
-
 // per-device setup: SM count and the kernel's dynamic shared memory opt-in
 adha_status device_setup(const void* fn, int* n_sm, int threads = NTHREADS) {
     int dev = 0;
@@ -359,7 +375,7 @@ adha_status launch_naive_t(const uint8_t* src, const Layout& ls, const std::vect
         }
         const int64_t total = (hi - lo) * (int64_t)nf;
         const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, (int64_t)n_sm * 16));
-        remap_naive_kernel<NF><<<(unsigned)blocks, 256, 0, st>>>(*P);
+        launch_pdl(&remap_naive_kernel<NF>, dim3((unsigned)blocks), dim3(256), 0, st, pdl_enabled(), *P);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_fail(e, "remap_naive_kernel launch");
     }
@@ -744,7 +760,7 @@ adha_status chain_small(void* const* buffers, const adha_layout* const* layouts,
     }
     // ~256 (record, field) items per block and hop: enough blocks to spread the latency
     const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((n * l0.n_fields + 255) / 256, n_sm));
-    remap_chain_small_kernel<<<(unsigned)blocks, 256, 0, st>>>(*P);
+    launch_pdl(&remap_chain_small_kernel, dim3((unsigned)blocks), dim3(256), 0, st, pdl_enabled(), *P);
     cudaError_t ce = cudaGetLastError();
     if (ce != cudaSuccess) return cuda_fail(ce, "remap_chain_small_kernel launch");
     return ADHA_OK;

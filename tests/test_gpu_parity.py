@@ -852,14 +852,16 @@ def test_loaders(loader, merge, monkeypatch):
         check_pair_ex(w, ls, bs, als, ld, bd, ald, n, seed=n % 89)
 
 
+@pytest.mark.parametrize("path", ["tiled", "direct"])
 @pytest.mark.parametrize("pdl", ["1", "0"])
-def test_back_to_back_hazards(pdl, monkeypatch):
-    """Programmatic dependent launch (remap.cu launch_ex, kernels.cuh grid_dep_wait): a remap may start
+def test_back_to_back_hazards(pdl, path, monkeypatch):
+    """Programmatic dependent launch (remap.cu launch_ex / launch_pdl, kernels.cuh grid_dep_wait), on the
+    tiled and on the direct kernel: a remap may start
     while the previous one drains, but must not read what it writes (RAW) nor write what it still reads
     (WAR).  A ring of remaps on one stream -- A->B, B->C, C->A, then around again, every buffer both read
     and overwritten by neighbouring launches -- must end exactly where the oracle's ring ends."""
     monkeypatch.setenv("ADHA_PDL", pdl)
-    monkeypatch.setenv("ADHA_SMALL_BYTES", "0")
+    monkeypatch.setenv("ADHA_SMALL_BYTES", "0" if path == "tiled" else str(1 << 40))
     widths = config_widths(16)
     n = 300_007
     labs = [[0] * 16, list(range(16)), [i // 4 for i in range(16)]]
