@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 #include <set>
 #include <string>
@@ -22,9 +23,18 @@
 namespace adha {
 namespace ipdev {
 
+// (programmatic dependent launch) every in-place kernel waits for the previous kernel's writes
+// before its first global access, then lets the next launch be scheduled (its own accesses wait
+// for this grid in turn)
+__device__ __forceinline__ void ip_pdl_begin() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ---------------------------------------------------------------------------- tail
 __global__ void ip_tail_kernel(uint8_t* __restrict__ buf, const IpTailField* __restrict__ tf, uint32_t nf,
                                int64_t r0, int64_t ntail, uint8_t* __restrict__ tailbuf, uint32_t R, int restore) {
+    ip_pdl_begin();
     const int64_t total = ntail * nf;
     for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
          idx += (int64_t)gridDim.x * blockDim.x) {
@@ -187,6 +197,7 @@ template <typename Atom, int to_blocks, bool GROUPED, int MINB>
 __global__ void __launch_bounds__(256, MINB) ip_tile_kernel(uint8_t* __restrict__ buf, const IpPiece* __restrict__ cl,
                                                       const IpCol* __restrict__ cols, uint32_t ncl, uint64_t m,
                                                       uint32_t T, uint32_t tab_cap) {
+    ip_pdl_begin();
     extern __shared__ __align__(16) uint8_t sm[];
     IpCol* tab = reinterpret_cast<IpCol*>(sm);
     Atom* sa = reinterpret_cast<Atom*>(sm + tab_cap);
@@ -316,6 +327,7 @@ template <uint32_t S>
 __global__ void __launch_bounds__(256) ip_cycle_save_kernel(uint8_t* __restrict__ buf, const uint32_t* __restrict__ seq,
                                                             const IpSeg* __restrict__ segs, uint32_t nseg,
                                                             uint8_t* __restrict__ save) {
+    ip_pdl_begin();
     constexpr uint32_t V = S / 16, G = V < 32 ? V : 32, VPL = V / G;
     const uint32_t lane = threadIdx.x % G;
     const uint64_t g0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / G;
@@ -334,6 +346,7 @@ template <uint32_t S>
 __global__ void __launch_bounds__(256) ip_cycle_shift_kernel(uint8_t* buf, const uint32_t* __restrict__ seq,
                                                              const IpSeg* __restrict__ segs, uint32_t nseg,
                                                              const uint8_t* __restrict__ save) {
+    ip_pdl_begin();
     constexpr uint32_t V = S / 16, G = V < 32 ? V : 32, VPL = V / G;
 #ifndef IP_SHIFT_VEC
 #define IP_SHIFT_VEC 8
@@ -376,6 +389,25 @@ __global__ void __launch_bounds__(256) ip_cycle_shift_kernel(uint8_t* buf, const
 }  // namespace ipdev
 
 namespace {
+
+bool ip_pdl() {
+    const char* e = std::getenv("ADHA_PDL");
+    return !(e && *e == '0');
+}
+// cudaLaunchKernelExC with programmatic dependent launch allowed (ADHA_PDL=0: plain launch)
+cudaError_t ip_launch(const void* fn, dim3 grid, dim3 block, void** args, size_t smem, cudaStream_t st) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = ip_pdl() ? 1 : 0;
+    return cudaLaunchKernelExC(&cfg, fn, args);
+}
 
 adha_status cuda_err(cudaError_t e, const char* what) {
     return fail(ADHA_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
@@ -445,7 +477,7 @@ adha_status launch_tiles(const InplacePlan& P, uint8_t* buf, const uint8_t* ws, 
     uint32_t ncl = (uint32_t)v.size(), T = P.T;
     uint64_t m = (uint64_t)P.m;
     void* args[] = {&buf, (void*)&tab, (void*)&cols, &ncl, &m, &T, (void*)&tab_cap};
-    e = cudaLaunchKernel(fn, dim3(grid), dim3(256), args, smem, st);
+    e = ip_launch(fn, dim3(grid), dim3(256), args, smem, st);
     return e == cudaSuccess ? ADHA_OK : cuda_err(e, "ip_tile_kernel launch");
 }
 
@@ -454,10 +486,13 @@ adha_status launch_tail(const InplacePlan& P, uint8_t* buf, uint8_t* ws, bool re
     const uint32_t nf = (uint32_t)P.tail_fields.size();
     const int64_t work = P.tail * nf;
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, 1024));
-    ipdev::ip_tail_kernel<<<grid, 256, 0, st>>>(buf, reinterpret_cast<const IpTailField*>(ws + P.ws_tailf), nf,
-                                                P.m * (int64_t)P.T, P.tail, ws + P.ws_tail,
-                                                (uint32_t)P.ls.record_bytes, restore ? 1 : 0);
-    cudaError_t e = cudaGetLastError();
+    const IpTailField* tf = reinterpret_cast<const IpTailField*>(ws + P.ws_tailf);
+    int64_t r0 = P.m * (int64_t)P.T, ntail = P.tail;
+    uint8_t* tailbuf = ws + P.ws_tail;
+    uint32_t nfv = nf, R = (uint32_t)P.ls.record_bytes;
+    int rs = restore ? 1 : 0;
+    void* args[] = {&buf, (void*)&tf, &nfv, &r0, &ntail, &tailbuf, &R, &rs};
+    cudaError_t e = ip_launch((const void*)&ipdev::ip_tail_kernel, dim3(grid), dim3(256), args, 0, st);
     return e == cudaSuccess ? ADHA_OK : cuda_err(e, "ip_tail_kernel launch");
 }
 
@@ -551,11 +586,13 @@ extern "C" adha_status adha_remap_inplace(void* buf, uint64_t buf_bytes, const a
         const IpSeg* segs = reinterpret_cast<const IpSeg*>(ws + P.ws_segs);
         uint8_t* save = ws + P.ws_save;
         s = with_cycle_kernels(P.S, [&](auto save_k, auto shift_k) {
-            save_k<<<grid, 256, 0, st>>>(b, seq, segs, nseg, save);
-            shift_k<<<grid, 256, 0, st>>>(b, seq, segs, nseg, save);
+            uint32_t nsg = nseg;
+            void* args[] = {&b, (void*)&seq, (void*)&segs, &nsg, &save};
+            e = ip_launch((const void*)save_k, dim3(grid), dim3(256), args, 0, st);
+            if (e == cudaSuccess) e = ip_launch((const void*)shift_k, dim3(grid), dim3(256), args, 0, st);
         });
         if (s != ADHA_OK) return s;
-        e = cudaGetLastError();
+        if (e == cudaSuccess) e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_err(e, "ip_cycle kernels launch");
     }
     s = launch_tiles(P, b, ws, true, dev, sms, st);
