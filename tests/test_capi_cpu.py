@@ -725,8 +725,9 @@ def test_remap_chain_route(monkeypatch):
 
 def test_routing_thresholds(monkeypatch):
     """The routing the plan reports (remap.cu direct_bytes / merge_bytes, read by adha_remap_plan_describe):
-    the direct kernel up to 2 MB of payload, up to 8 MB for plans of >= 16 components (C3's 24), the merged
-    plan for multi-component remaps up to 64 MB; ADHA_SMALL_BYTES / ADHA_MERGE_BYTES override them."""
+    the direct kernel up to 2 MB of payload, up to 8 MB for plans of >= 16 components (C3's 24); the merged
+    plan for multi-component remaps up to a limit set by the src cluster count and identity components;
+    ADHA_SMALL_BYTES / ADHA_MERGE_BYTES override them."""
     monkeypatch.delenv("ADHA_SMALL_BYTES", raising=False)
     monkeypatch.delenv("ADHA_MERGE_BYTES", raising=False)
     w16 = [8 if i % 4 == 3 else 4 for i in range(16)]
@@ -737,5 +738,13 @@ def test_routing_thresholds(monkeypatch):
     d = A.plan_describe(A.Layout(w64, list(range(64))), A.Layout(w64, c3))
     assert len(d["components"]) >= 16
     assert d["direct_bytes"] == 8 << 20 and d["merge_bytes"] == 64 << 20
+    # merged-plan limit: none for <= 8 src clusters with identity components (Medical AoSV -> SoA),
+    # 128 MB for <= 32 src clusters without (K-Means 4xAoS8 -> SoA), 64 MB above 32 (C3 above)
+    w9 = [4] * 9
+    d = A.plan_describe(A.Layout(w9, [0, 0, 0, 1, 2, 3, 4, 5, 6]), A.Layout(w9, list(range(9))))
+    assert any(c["identity"] for c in d["components"]) and d["merge_bytes"] == 2 ** 64 - 1
+    w32 = [4] * 32
+    d = A.plan_describe(A.Layout(w32, [f // 8 for f in range(32)]), A.Layout(w32, list(range(32))))
+    assert not any(c["identity"] for c in d["components"]) and d["merge_bytes"] == 128 << 20
     monkeypatch.setenv("ADHA_SMALL_BYTES", "12345")
     assert A.plan_describe(A.Layout.aos(w16), A.Layout.soa(w16))["direct_bytes"] == 12345
