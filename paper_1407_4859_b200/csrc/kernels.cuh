@@ -169,13 +169,6 @@ __device__ __forceinline__ void tile_next(const TiledParams& p, uint32_t H, Tile
     }
 }
 
-// cp.async loader (TiledParams::cpa, the CPA instantiations): loader warp lw of NLOAD copies
-// bytes [lw*B/NLOAD, (lw+1)*B/NLOAD) of tile (k, lt)'s packed src chunks (B = tile_bytes) into
-// input stage `sb` with 16-byte cp.async, 512 contiguous bytes per warp instruction, then arrives
-// on the stage's `full` barrier when its copies land (count NLOAD*32).  Unlike TMA bulk copies,
-// the cost does not grow with the number of src chunks (64 SoA chunks of 640 B per tile:
-// profiles/r02aa_pieces.log).  Cluster descriptors come from the kernel parameters (uniform per
-// warp); (c0, b0) cache this warp's first chunk and its packed begin for component ak.
 // one 16-byte FieldDesc of the plan table (device memory, read-only)
 __device__ __forceinline__ FieldDesc ldg_field(const FieldDesc* f) {
     const uint4 v = ldg_nc128(reinterpret_cast<const uint4*>(f));
@@ -190,6 +183,13 @@ __device__ __forceinline__ FieldDesc ldg_field(const FieldDesc* f) {
     return d;
 }
 
+// cp.async loader (TiledParams::cpa, the CPA instantiations): loader warp lw of NLOAD copies
+// bytes [lw*B/NLOAD, (lw+1)*B/NLOAD) of tile (k, lt)'s packed src chunks (B = tile_bytes) into
+// input stage `sb` with 16-byte cp.async, 512 contiguous bytes per warp instruction, then arrives
+// on the stage's `full` barrier when its copies land (count NLOAD*32).  Unlike TMA bulk copies,
+// the cost does not grow with the number of src chunks (64 SoA chunks of 640 B per tile:
+// profiles/r02aa_pieces.log).  Cluster descriptors come from the kernel parameters (uniform per
+// warp); (c0, b0) cache this warp's first chunk and its packed begin for component ak.
 struct CpaState {
     int ak;
     uint32_t c0, b0;
